@@ -1,0 +1,247 @@
+/*
+ * tlt_b200.h — C-ABI of the B200-native adaptive speculative-decoding rollout
+ * step (TLT, arXiv 2511.16665). Drop-in for the reference `specsim` hot path:
+ * drafter propose -> target verify -> accept -> KV commit -> strategy select.
+ *
+ * Every entry point replaces a reference C++ symbol; the citation on each
+ * declaration names it (paths relative to /root/reference/proj/include/specsim).
+ * The reference is header-only C++20 with no ABI, so this header is the first
+ * stable boundary: plain pointers and sizes, caller-owned host buffers, an int
+ * status code per call (0 = OK) and tlt_last_error() for the message.
+ *
+ * Error mapping (reference errors.hpp:9-34):
+ *   TLT_ERR_CONFIG  <-> specsim::ConfigError   (field path in the message)
+ *   TLT_ERR_ROUTING <-> specsim::RoutingError  (beg_mab.hpp:141-143)
+ *   TLT_ERR_CUDA    <-> device/runtime failure (no reference analogue)
+ *
+ * Threading: one engine per GPU, driven by exactly one host thread; calls are
+ * not re-entrant on a handle (reference SPEC.md:312 "single-owner" MAB).
+ */
+#ifndef TLT_B200_H
+#define TLT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLT_API __attribute__((visibility("default")))
+
+enum {
+    TLT_OK = 0,
+    TLT_ERR_INTERNAL = 1,
+    TLT_ERR_CONFIG = 2,
+    TLT_ERR_ROUTING = 3,
+    TLT_ERR_CUDA = 4,
+    TLT_ERR_STATE = 5
+};
+
+/* Reference TokenId is int32 (token_model.hpp:18); EOS = 0, BEGIN = 1 (:22-23). */
+#define TLT_EOS_TOKEN 0
+#define TLT_BEGIN_TOKEN 1
+
+/* Decode modes, reference DecodeMode (spec_decode.hpp:315). */
+enum { TLT_MODE_GREEDY_TREE = 0, TLT_MODE_STOCHASTIC_LINEAR = 1 };
+
+/* Reference SpecStrategy (spec_decode.hpp:19-45). */
+typedef struct {
+    int32_t draft_depth;
+    int32_t top_k;
+    int32_t tokens_to_verify;
+} tlt_strategy;
+
+/* Llama/Qwen-style target + one-layer EAGLE drafter sharing embedding, final
+ * norm and LM head. Replaces the Markov target (token_model.hpp:100-156) and
+ * the count drafter (drafter.hpp:20-67) as the leaf oracles of the path. */
+typedef struct {
+    int32_t vocab;
+    int32_t hidden;
+    int32_t layers;
+    int32_t heads;
+    int32_t kv_heads;
+    int32_t head_dim;
+    int32_t ffn;
+    int32_t qkv_bias;   /* Qwen2-style q/k/v bias */
+    float rope_theta;
+    float rms_eps;
+    int32_t max_slots;  /* concurrent requests (KV slots) */
+    int32_t max_ctx;    /* positions per slot (prompt + response + tree) */
+} tlt_model_cfg;
+
+/* Seeded synthetic random-init weights (no checkpoints offline). All values are
+ * a counter-based hash of (seed, tensor, index), identical on CPU and GPU. */
+typedef struct {
+    uint64_t seed;
+    float layer_scale; /* std of attention/MLP weights ("structure" knob) */
+    float lm_gain;     /* bigram structure of the LM head */
+    float lm_noise;    /* unstructured part of the LM head */
+    float fc_noise;    /* drafter fc deviation from the embedding passthrough */
+} tlt_init_cfg;
+
+typedef struct tlt_engine tlt_engine;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+TLT_API int tlt_engine_create(const tlt_model_cfg* cfg, const tlt_init_cfg* init, int device, tlt_engine** out);
+TLT_API void tlt_engine_destroy(tlt_engine* e);
+/* Last error message for the engine (or the calling thread when e == NULL). */
+TLT_API const char* tlt_last_error(const tlt_engine* e);
+TLT_API void tlt_set_last_error(const char* msg);
+/* Library build/version string. */
+TLT_API const char* tlt_version(void);
+
+/* ---- request state ------------------------------------------------------ */
+/* Prefill b requests into KV slots. tokens holds the prompts back to back
+ * (lens[i] tokens each, every len >= 1). The last prompt token becomes the
+ * step root (its KV is written by the first verify), exactly as the reference
+ * context `prompt ++ generated` feeds target_next_dist (token_model.hpp:161). */
+TLT_API int tlt_prefill(tlt_engine* e, int b, const int32_t* slot_ids, const int32_t* lens, const int32_t* tokens);
+TLT_API int tlt_release(tlt_engine* e, int slot_id);
+/* Committed target KV length of a slot (positions 0..len-1 hold KV). */
+TLT_API int tlt_slot_len(tlt_engine* e, int slot_id, int32_t* len);
+
+/* ---- one engine step ---------------------------------------------------- */
+/* Tree produced by the drafter, reference DraftTree (spec_decode.hpp:50-70),
+ * rank order, parent -1 = root. Caller-owned, sized [b][tokens_to_verify]. */
+typedef struct {
+    int32_t* tokens;
+    int32_t* parents;
+    int32_t* depths;
+    double* probs;
+    double* path_probs;
+    int32_t* n_nodes; /* [b] */
+} tlt_tree_out;
+
+/* Verify outcome, reference AcceptResult (spec_decode.hpp:74-80) plus the
+ * accepted tree indices and the committed KV slot map (new). Sized
+ * [b][draft_depth] for accepted / nodes / kv_src, [b] otherwise. */
+typedef struct {
+    int32_t* accepted;     /* accepted tokens (root-to-node path) */
+    int32_t* nodes;        /* accepted tree node indices */
+    int32_t* accept_len;   /* reference accept_length */
+    int32_t* bonus;        /* reference bonus */
+    int32_t* kv_src;       /* committed KV: slot L+1+j <- L+1+kv_src[j] (tree slot) */
+    int32_t* kv_len;       /* committed target KV length after the step */
+    float* elapsed_ms;     /* [1] device time of the step (CUDA events) */
+} tlt_accept_out;
+
+/* Greedy tree SD step: build_draft_tree (spec_decode.hpp:111-197) with the
+ * EAGLE drafter, one tree-masked target verify forward, verify_greedy
+ * (:245-268), KV compaction. The whole step replays one CUDA graph keyed on
+ * (batch bucket, strategy) when a pool is built. `tree` may be NULL. */
+TLT_API int tlt_sd_step(tlt_engine* e, const tlt_strategy* s, int b, const int32_t* slot_ids, tlt_tree_out* tree,
+                        tlt_accept_out* out);
+/* Stochastic linear-chain SD step: build_sampled_chain (:202-223) +
+ * verify_stochastic (:275-313), temperature t > 0. Uniforms are the
+ * reference RngStream draws (rng.hpp:54-56), host-generated per request in
+ * consumption order (draft_depth chain draws, then accept draws, then one
+ * residual/bonus draw); `uniforms` is [b][2*draft_depth+1]. */
+TLT_API int tlt_sd_step_stochastic(tlt_engine* e, int draft_depth, float temperature, int b,
+                                   const int32_t* slot_ids, const double* uniforms, tlt_accept_out* out);
+/* Plain autoregressive step (the 2x denominator): reference plain branch
+ * (rollout.hpp:247-261) / generate_autoregressive (token_model.hpp:190-203). */
+TLT_API int tlt_ar_step(tlt_engine* e, int b, const int32_t* slot_ids, int32_t* out_tokens, float* elapsed_ms);
+
+/* ---- CUDA-graph pool ---------------------------------------------------- */
+/* One entry per reference CaptureEntry (capture_plan.hpp:25-33): side 0 =
+ * TARGET(bucket, tokens_to_verify), 1 = DRAFT(bucket, top_k, draft_depth). */
+typedef struct {
+    int32_t side;
+    int32_t bucket_lo;
+    int32_t bucket_hi;
+    int32_t tokens_to_verify;
+    int32_t top_k;
+    int32_t draft_depth;
+    double memory_units;
+} tlt_capture_entry;
+TLT_API int tlt_graph_pool_build(tlt_engine* e, const tlt_capture_entry* entries, int n, size_t* graph_bytes);
+TLT_API int tlt_graph_pool_clear(tlt_engine* e);
+
+/* ---- strategy selection (host, reference semantics) ---------------------- */
+/* BEG-MAB, reference beg_mab.hpp:28-170. Opaque single-owner state. */
+typedef struct tlt_mab tlt_mab;
+TLT_API int tlt_mab_create(const tlt_strategy* strategies, int n, const int32_t* thresholds, int n_thr,
+                           double epsilon, int window, tlt_mab** out);
+TLT_API void tlt_mab_destroy(tlt_mab* m);
+/* beg_select (beg_mab.hpp:140-170). rng_state is the caller's RngStream
+ * (mt19937_64 state handle, see tlt_rng_*). Writes the picked arm index. */
+typedef struct tlt_rng tlt_rng;
+TLT_API int tlt_mab_select(tlt_mab* m, int batch, tlt_rng* rng, int32_t* arm, tlt_strategy* out);
+/* beg_record (beg_mab.hpp:111-134). */
+TLT_API int tlt_mab_record(tlt_mab* m, const tlt_strategy* s, double elapsed, const int32_t* accept_lens, int batch);
+/* Window medians/selection counts per arm (beg_state_to_json, :174-193). */
+TLT_API int tlt_mab_arm_stats(tlt_mab* m, int arm, double* median_reward, int64_t* selections, int32_t* n_rewards);
+/* Multi-GPU merge (C1): apply one foreign rank's record to this replica. */
+TLT_API int tlt_mab_apply_record(tlt_mab* m, int arm, double reward, double a_bar);
+/* Deterministic streams, reference RngStream (rng.hpp:34-86). */
+TLT_API int tlt_rng_create(uint64_t seed, uint64_t stream_id, tlt_rng** out);
+TLT_API int tlt_rng_fork(const tlt_rng* r, uint64_t label, tlt_rng** out);
+TLT_API void tlt_rng_destroy(tlt_rng* r);
+TLT_API uint64_t tlt_rng_next_u64(tlt_rng* r);
+TLT_API double tlt_rng_uniform01(tlt_rng* r);
+
+/* plan_captures (capture_plan.hpp:87-126) with BucketSpec (:42-45). Writes up
+ * to max_entries entries; *n_entries = number produced. vanilla != 0 gives
+ * plan_captures_vanilla (:130-155). */
+TLT_API int tlt_plan_captures(const tlt_strategy* strategies, int n, const int32_t* thresholds, int n_thr,
+                              int max_batch, int vanilla, tlt_capture_entry* out, int max_entries, int* n_entries,
+                              double* total_memory_units);
+
+/* ---- rollout (the step loop's caller, reference run_rollout) ------------- */
+/* Reference RolloutConfig (rollout.hpp:66-77) subset on the GPU path. */
+typedef struct {
+    int32_t enable_sd;
+    int32_t elastic_threshold; /* should_enable_sd (rollout.hpp:54-57) */
+    int32_t mode;              /* TLT_MODE_* */
+    float temperature;         /* stochastic mode only */
+    tlt_strategy fixed_strategy;
+    int32_t use_mab;           /* 1: BEG-MAB select/record with measured elapsed */
+    uint64_t seed;             /* RngStream seed of the rollout (fork labels as rollout.hpp:151,153) */
+    int32_t use_graphs;        /* replay the CUDA-graph pool */
+} tlt_rollout_cfg;
+
+/* Reference RolloutResult (rollout.hpp:79-97) flattened. generated: [n][max_len]. */
+typedef struct {
+    int32_t* generated;     /* [n][max_len_stride] */
+    int32_t* gen_len;       /* [n] */
+    int64_t sd_steps;
+    int64_t plain_steps;
+    int64_t verify_events;
+    int64_t accepted_total; /* sum of accept_len over verify events (mean_accept_len numerator) */
+    int64_t emitted_total;  /* tokens appended (accepted + bonus, truncated) */
+    double device_ms;       /* sum of per-step device time */
+    double wall_ms;         /* host wall time of the whole rollout */
+    int64_t gpu_launches;   /* kernel launches issued (graph nodes counted) */
+} tlt_rollout_result;
+
+/* Runs n requests (prompts back to back, max_len per request) to completion
+ * through prefill + the SD/AR step loop (rollout.hpp:130-276). mab may be NULL
+ * when cfg->use_mab == 0. */
+TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* mab, int n, const int32_t* request_ids,
+                            const int32_t* prompt_lens, const int32_t* prompts, const int32_t* max_lens,
+                            int max_len_stride, tlt_rollout_result* out);
+
+/* ---- parity / debug exports (tests only) -------------------------------- */
+/* After the last tlt_sd_step: per-request drafter expansion rows. For request
+ * i, expansion e: the path from the root (tokens, up to draft_depth) and the
+ * full fp64 drafter distribution used by the tree (vocab entries).
+ * Enabled by tlt_set_debug(e, 1) before the step (graphs bypassed). */
+TLT_API int tlt_set_debug(tlt_engine* e, int on);
+TLT_API int tlt_debug_expansions(tlt_engine* e, int i, int max_exp, int32_t* n_exp, int32_t* path_len,
+                                 int32_t* paths /* [max_exp][depth] */, double* rows /* [max_exp][V] */);
+/* Target logits (fp32) of the verify rows of request i: [T+1][V], row 0 = root. */
+TLT_API int tlt_debug_verify_logits(tlt_engine* e, int i, float* logits, int max_rows, int32_t* n_rows);
+/* Target logits of the last tlt_ar_step: [b][V]. */
+TLT_API int tlt_debug_ar_logits(tlt_engine* e, float* logits, int b);
+
+/* ---- kernel-level entry points for unit tests ---------------------------- */
+/* Y = X W^T through the tcgen05 GEMM. kind: 0 f32 store, 1 bf16 store,
+ * 3 SwiGLU (W rows interleaved gate/up). Returns the split-K factor used. */
+TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32, void* y_bf16,
+                         float* ws, long long ws_elems, int max_splits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLT_B200_H */

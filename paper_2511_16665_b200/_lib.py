@@ -1,0 +1,57 @@
+"""ctypes binding of libtlt_b200.so (the C-ABI declared in include/tlt_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()``. There is no
+fallback: importing the product path without the extension raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtlt_b200.so")
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()'). No CPU fallback exists.")
+        _lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        _declare(_lib)
+    return _lib
+
+
+i32p = C.POINTER(C.c_int32)
+f64p = C.POINTER(C.c_double)
+f32p = C.POINTER(C.c_float)
+
+
+def _declare(L: C.CDLL) -> None:
+    L.tlt_version.restype = C.c_char_p
+    L.tlt_last_error.restype = C.c_char_p
+    L.tlt_last_error.argtypes = [C.c_void_p]
+    L.tlt_dev_gemm.restype = C.c_int
+    L.tlt_dev_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int]
+
+
+def last_error(engine=None) -> str:
+    msg = lib().tlt_last_error(engine)
+    return msg.decode() if msg else ""
+
+
+class TltError(RuntimeError):
+    pass
+
+
+def check(rc: int, engine=None) -> int:
+    if rc < 0 or rc in (1, 2, 3, 4, 5) and False:
+        pass
+    if rc < 0:
+        raise TltError(last_error(engine))
+    return rc

@@ -1,0 +1,33 @@
+// Kernel-level entry points used by the GPU unit tests (plain pointers, C-ABI).
+#include <cuda_runtime.h>
+#include "tlt_internal.h"
+#include "../../include/tlt_b200.h"
+
+using namespace tlt;
+
+extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
+                                    void* y_bf16, float* ws, long long ws_elems, int max_splits) {
+    try {
+        GemmPlan g = plan_gemm(m, n, k);
+        if (max_splits > 0 && g.splits > max_splits) {
+            g.kb_per_split = (g.kb_total + max_splits - 1) / max_splits;
+            g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+        }
+        CUtensorMap tw = make_tmap_bf16(w, n, k, k, 128);
+        CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.bn);
+        EpiParams ep{};
+        ep.kind = kind;
+        ep.n_out = n;
+        ep.m_tok = m;
+        ep.out_f32 = y_f32;
+        ep.ld_f32 = kind == EPI_SWIGLU ? n / 2 : n;
+        ep.out_bf16 = static_cast<__nv_bfloat16*>(y_bf16);
+        ep.ld_bf16 = kind == EPI_SWIGLU ? n / 2 : n;
+        launch_gemm(g, tw, tx, ep, ws, static_cast<size_t>(ws_elems), 0);
+        CUDA_CHECK(cudaDeviceSynchronize());
+        return g.splits;
+    } catch (const std::exception& e) {
+        tlt_set_last_error(e.what());
+        return -1;
+    }
+}

@@ -1,0 +1,243 @@
+// tcgen05 swap-AB GEMM kernel + split-K reduce + host-side planner/launcher.
+// See gemm.cuh for the operand mapping and the fused epilogues.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+#include "tlt_internal.h"
+
+namespace tlt {
+
+constexpr int kBlockM = 128;  // weight rows per tile (MMA M)
+constexpr int kBlockK = 64;   // 64 bf16 = one 128-byte swizzle row
+constexpr int kABytes = kBlockM * kBlockK * 2;
+
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_swapab(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                  int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, EpiParams ep) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int b_bytes = bn * kBlockK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + stages * kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + stages * b_bytes);
+    uint64_t* empty = full + stages;
+    uint64_t* tfull = empty + stages;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * kBlockM;
+    const int t0 = blockIdx.y * bn;
+    const int z = blockIdx.z;
+    const int kb0 = z * kb_per_split;
+    const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_holder)),
+                     "r"(tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (elect_one()) {
+            const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+            const uint64_t pol_x = policy_evict_last();   // activations: re-read by every weight tile
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % stages;
+                const uint32_t ph = (i / stages) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                mbar_arrive_expect_tx(&full[s], kABytes + b_bytes);
+                const int kc = (kb0 + i) * kBlockK;
+                tma_load_2d(sA + s * kABytes, &tmW, &full[s], kc, n0, pol_w);
+                tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (single elected thread)
+        const uint32_t idesc = idesc_bf16_f32(kBlockM, bn);
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % stages;
+            const uint32_t ph = (i / stages) & 1;
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint64_t da = sdesc_kmajor_sw128(sA + s * kABytes);
+                const uint64_t db = sdesc_kmajor_sw128(sB + s * b_bytes);
+#pragma unroll
+                for (int kk = 0; kk < kBlockK / 16; ++kk) {
+                    // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
+                    tc_mma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                }
+                tc_commit(&empty[s]);
+                if (i == nkb - 1) tc_commit(tfull);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        const int q = warp & 3;
+        const int row = n0 + q * 32 + lane;
+        const int n_even = row & ~1;
+        for (int c = 0; c < bn; c += 16) {
+            if (t0 + c >= ep.m_tok) break;
+            float v[16];
+            tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
+                if ((lane & 1) == 0) epi_pair(ep, t0 + c + j, n_even, v[j], other, z);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
+                     : "memory");
+    }
+}
+
+__global__ void k_splitk_reduce(const float* __restrict__ ws, long long stride, int splits, int ld,
+                                EpiParams ep) {
+    const int npairs = (ep.n_out + 1) >> 1;
+    const long long total = (long long)ep.m_tok * npairs;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int t = static_cast<int>(idx / npairs);
+        const int n = static_cast<int>(idx % npairs) * 2;
+        const float* p = ws + (long long)t * ld + n;
+        float v0 = 0.f, v1 = 0.f;
+        const bool has1 = n + 1 < ep.n_out;
+        for (int z = 0; z < splits; ++z) {  // fixed order: deterministic
+            v0 += p[z * stride];
+            if (has1) v1 += p[z * stride + 1];
+        }
+        epi_pair(ep, t, n, v0, v1, 0);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D bf16 K-major tensor map: rows x cols (cols = K, contiguous), box = box_rows x 64.
+CUtensorMap make_tmap_bf16(const void* base, int rows, int cols, long long row_stride_elems, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_elems * 2)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBlockK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+static int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        CUDA_CHECK(cudaGetDevice(&dev));
+        CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return g_num_sms;
+}
+
+GemmPlan plan_gemm(int m_tok, int n_out, int k) {
+    GemmPlan g;
+    const int n_ttiles = (m_tok + 255) / 256;
+    int bn = (m_tok + n_ttiles - 1) / n_ttiles;
+    bn = std::max(16, (bn + 15) / 16 * 16);
+    g.bn = bn;
+    g.n_ttiles = (m_tok + bn - 1) / bn;
+    g.n_wtiles = (n_out + kBlockM - 1) / kBlockM;
+    g.kb_total = (k + kBlockK - 1) / kBlockK;
+    const int stage_bytes = kABytes + bn * kBlockK * 2;
+    const int ctas_per_sm = bn <= 128 ? 2 : 1;
+    const int budget = ctas_per_sm == 2 ? 110 * 1024 : 200 * 1024;
+    g.stages = std::max(2, std::min(8, budget / stage_bytes));
+    g.smem = g.stages * stage_bytes + 2 * g.stages * 8 + 8 + 16 + 1024;
+    g.tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+    const int tiles = g.n_wtiles * g.n_ttiles;
+    const int slots = num_sms() * ctas_per_sm;
+    int splits = 1;
+    if (tiles < slots) splits = std::max(1, std::min(slots / tiles, g.kb_total / 4));
+    g.kb_per_split = (g.kb_total + splits - 1) / splits;
+    g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+    return g;
+}
+
+void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep_in,
+                 float* workspace, size_t workspace_elems, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    EpiParams ep = ep_in;
+    dim3 grid(g.n_wtiles, g.n_ttiles, g.splits);
+    if (g.splits > 1) {
+        const long long plane = (long long)ep.m_tok * ep.n_out;
+        if ((size_t)(plane * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");
+        EpiParams pp = ep;
+        pp.kind = EPI_PARTIAL;
+        pp.out_f32 = workspace;
+        pp.ld_f32 = ep.n_out;
+        pp.partial_stride = plane;
+        k_gemm_swapab<<<grid, 192, g.smem, st>>>(tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
+                                                 g.tmem_cols, pp);
+        CUDA_CHECK(cudaGetLastError());
+        const long long pairs = (long long)ep.m_tok * ((ep.n_out + 1) / 2);
+        const int threads = 256;
+        const int blocks = static_cast<int>(std::min<long long>((pairs + threads - 1) / threads, 148LL * 16));
+        k_splitk_reduce<<<blocks, threads, 0, st>>>(workspace, plane, g.splits, ep.n_out, ep);
+    } else {
+        k_gemm_swapab<<<grid, 192, g.smem, st>>>(tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
+                                                 g.tmem_cols, ep);
+    }
+    CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace tlt

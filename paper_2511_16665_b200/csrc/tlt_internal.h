@@ -1,0 +1,48 @@
+// Internal host-side declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "gemm.cuh"
+
+namespace tlt {
+
+// Maps onto TLT_ERR_CUDA at the C-ABI boundary.
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+// Maps onto TLT_ERR_CONFIG (reference specsim::ConfigError, errors.hpp:9-19).
+struct ConfigErr : std::runtime_error {
+    std::string field;
+    ConfigErr(std::string f, const std::string& m)
+        : std::runtime_error(f.empty() ? m : f + ": " + m), field(std::move(f)) {}
+};
+// Maps onto TLT_ERR_ROUTING (reference specsim::RoutingError, errors.hpp:32-34).
+struct RoutingErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CUDA_CHECK(expr)                                                                     \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            throw ::tlt::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_) + " @" + \
+                                   __FILE__ + ":" + std::to_string(__LINE__));               \
+    } while (0)
+
+struct GemmPlan {
+    int bn = 16, n_ttiles = 1, n_wtiles = 1, kb_total = 1, kb_per_split = 1, splits = 1, stages = 4;
+    int smem = 0;
+    unsigned tmem_cols = 32;
+};
+
+int num_sms();
+CUtensorMap make_tmap_bf16(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
+GemmPlan plan_gemm(int m_tok, int n_out, int k);
+void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep,
+                 float* workspace, size_t workspace_elems, cudaStream_t st);
+
+}  // namespace tlt

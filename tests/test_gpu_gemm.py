@@ -1,0 +1,47 @@
+"""tcgen05 swap-AB GEMM vs a torch fp32 reference of the same op."""
+import pytest
+import torch
+
+from paper_2511_16665_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    # (M tokens, K, N out)
+    (17, 256, 512), (68, 256, 256), (4, 256, 1376), (64, 688, 256), (16, 256, 4096),
+    (65, 3584, 4608), (200, 512, 640), (256, 1024, 384), (300, 512, 256), (528, 3584, 512),
+    (1, 3584, 3584), (1088, 256, 256),
+]
+
+
+@pytest.mark.parametrize("m,k,n", SHAPES)
+@pytest.mark.parametrize("max_splits", [1, 0])
+def test_gemm_f32(m, k, n, max_splits):
+    torch.manual_seed(m * 7 + k + n)
+    x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    y = torch.full((m, n), float("nan"), device="cuda", dtype=torch.float32)
+    ws = torch.empty(64 << 20, device="cuda", dtype=torch.float32)
+    L = _lib.lib()
+    rc = L.tlt_dev_gemm(x.data_ptr(), m, k, w.data_ptr(), n, 0, y.data_ptr(), None,
+                        ws.data_ptr(), ws.numel(), max_splits)
+    assert rc >= 1, _lib.last_error()
+    ref = x.float() @ w.float().t()
+    err = (y - ref).abs().max().item()
+    assert err < 2e-3 * max(1.0, ref.abs().max().item()), (err, rc)
+
+
+def test_gemm_swiglu():
+    m, k, f = 33, 512, 320
+    torch.manual_seed(0)
+    x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(2 * f, k, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    y = torch.zeros(m, f, device="cuda", dtype=torch.bfloat16)
+    ws = torch.empty(16 << 20, device="cuda", dtype=torch.float32)
+    rc = _lib.lib().tlt_dev_gemm(x.data_ptr(), m, k, w.data_ptr(), 2 * f, 3, None, y.data_ptr(),
+                                 ws.data_ptr(), ws.numel(), 0)
+    assert rc >= 1, _lib.last_error()
+    acc = x.float() @ w.float().t()
+    g, u = acc[:, 0::2], acc[:, 1::2]
+    ref = torch.nn.functional.silu(g) * u
+    assert (y.float() - ref).abs().max().item() < 2e-2 * max(1.0, ref.abs().max().item())
