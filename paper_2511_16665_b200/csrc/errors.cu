@@ -12,3 +12,7 @@ extern "C" TLT_API const char* tlt_version(void) { return "tlt_b200 0.1 sm_100a"
 namespace tlt {
 const char* thread_last_error() { return g_last_error.c_str(); }
 }
+
+// Engines are driven by one host thread (see header), so the per-engine
+// message is the calling thread's message.
+extern "C" TLT_API const char* tlt_last_error(const tlt_engine*) { return tlt::thread_last_error(); }
