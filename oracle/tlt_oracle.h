@@ -193,6 +193,7 @@ void orc_seq_destroy(orc_seq* s);
  * fp32 logits of the last row when logits != NULL. Features are recorded. */
 int orc_target_extend(orc_seq* s, const int32_t* toks, int n, float* logits_last);
 int orc_seq_len(orc_seq* s);
+int orc_seq_append(orc_seq* s, const int32_t* toks, int n);
 /* Logits after (committed ++ path) without committing (path may be empty:
  * then the committed last row). Used for tree verify rows. */
 int orc_target_logits_path(orc_seq* s, const int32_t* path, int n, float* logits);

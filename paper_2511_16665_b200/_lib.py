@@ -35,6 +35,13 @@ def _declare(L: C.CDLL) -> None:
     L.tlt_version.restype = C.c_char_p
     L.tlt_last_error.restype = C.c_char_p
     L.tlt_last_error.argtypes = [C.c_void_p]
+    L.tlt_rng_next_u64.restype = C.c_uint64
+    L.tlt_rng_next_u64.argtypes = [C.c_void_p]
+    L.tlt_rng_uniform01.restype = C.c_double
+    L.tlt_rng_uniform01.argtypes = [C.c_void_p]
+    L.tlt_rng_destroy.argtypes = [C.c_void_p]
+    L.tlt_engine_destroy.argtypes = [C.c_void_p]
+    L.tlt_mab_destroy.argtypes = [C.c_void_p]
     L.tlt_dev_gemm.restype = C.c_int
     L.tlt_dev_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int]

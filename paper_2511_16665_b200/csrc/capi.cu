@@ -1,0 +1,338 @@
+// C-ABI of libtlt_b200.so (include/tlt_b200.h): status codes + last error,
+// engine lifecycle, steps, graph pool, BEG-MAB / RNG / capture plan, and the
+// rollout loop (reference run_rollout, rollout.hpp:130-276).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/tlt_b200.h"
+#include "engine.h"
+#include "host_select.h"
+
+struct tlt_engine {
+    std::unique_ptr<tlt::Engine> e;
+};
+struct tlt_mab {
+    std::unique_ptr<tlt::Mab> m;
+};
+struct tlt_rng {
+    tlt::Rng r;
+};
+
+namespace {
+int fail(int code, const char* msg) {
+    tlt_set_last_error(msg);
+    return code;
+}
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return TLT_OK;
+    } catch (const tlt::ConfigErr& e) {
+        return fail(TLT_ERR_CONFIG, e.what());
+    } catch (const tlt::RoutingErr& e) {
+        return fail(TLT_ERR_ROUTING, e.what());
+    } catch (const tlt::CudaError& e) {
+        return fail(TLT_ERR_CUDA, e.what());
+    } catch (const std::exception& e) {
+        return fail(TLT_ERR_INTERNAL, e.what());
+    }
+}
+}  // namespace
+
+extern "C" {
+
+TLT_API int tlt_engine_create(const tlt_model_cfg* cfg, const tlt_init_cfg* init, int device, tlt_engine** out) {
+    if (!cfg || !init || !out) return fail(TLT_ERR_CONFIG, "null argument");
+    return guard([&] {
+        auto* h = new tlt_engine;
+        try {
+            h->e = std::make_unique<tlt::Engine>(*cfg, *init, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+TLT_API void tlt_engine_destroy(tlt_engine* e) { delete e; }
+
+TLT_API int tlt_prefill(tlt_engine* e, int b, const int32_t* slot_ids, const int32_t* lens, const int32_t* tokens) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] { e->e->prefill(b, slot_ids, lens, tokens); });
+}
+
+TLT_API int tlt_release(tlt_engine* e, int slot_id) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] { e->e->release(slot_id); });
+}
+
+TLT_API int tlt_slot_len(tlt_engine* e, int slot_id, int32_t* len) {
+    if (!e || !len) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        if (slot_id < 0 || slot_id >= e->e->cfg.max_slots) throw tlt::ConfigErr("slot_id", "out of range");
+        *len = e->e->slot_len(slot_id);
+    });
+}
+
+TLT_API int tlt_sd_step(tlt_engine* e, const tlt_strategy* s, int b, const int32_t* slot_ids, tlt_tree_out* tree,
+                        tlt_accept_out* out) {
+    if (!e || !s || !slot_ids) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { e->e->sd_step(*s, b, slot_ids, tree, out); });
+}
+
+TLT_API int tlt_sd_step_stochastic(tlt_engine* e, int draft_depth, float temperature, int b, const int32_t* slot_ids,
+                                   const double* uniforms, tlt_accept_out* out) {
+    (void)draft_depth, (void)temperature, (void)b, (void)slot_ids, (void)uniforms, (void)out;
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return fail(TLT_ERR_CONFIG, "mode: stochastic linear-chain verify is not implemented in this build");
+}
+
+TLT_API int tlt_ar_step(tlt_engine* e, int b, const int32_t* slot_ids, int32_t* out_tokens, float* elapsed_ms) {
+    if (!e || !slot_ids) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        const float ms = e->e->ar_step(b, slot_ids, out_tokens);
+        if (elapsed_ms) *elapsed_ms = ms;
+    });
+}
+
+TLT_API int tlt_graph_pool_build(tlt_engine* e, const tlt_capture_entry* entries, int n, size_t* graph_bytes) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] {
+        std::vector<tlt_capture_entry> v(entries, entries + n);
+        const size_t g = e->e->graph_pool_build(v);
+        if (graph_bytes) *graph_bytes = g;
+    });
+}
+
+TLT_API int tlt_graph_pool_clear(tlt_engine* e) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] { e->e->graph_pool_clear(); });
+}
+
+TLT_API int tlt_set_debug(tlt_engine* e, int on) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    e->e->set_debug(on != 0);
+    return TLT_OK;
+}
+
+TLT_API int tlt_debug_expansions(tlt_engine* e, int i, int max_exp, int32_t* n_exp, int32_t* path_len, int32_t* paths,
+                                 double* rows) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] {
+        auto& E = *e->e;
+        if (i < 0 || i >= (int)E.dbg_exp.size()) throw tlt::ConfigErr("i", "no debug data for request");
+        const auto& ex = E.dbg_exp[i];
+        const int n = std::min<int>(max_exp, (int)ex.size());
+        *n_exp = (int32_t)ex.size();
+        const int V = E.cfg.vocab;
+        for (int j = 0; j < n; ++j) {
+            path_len[j] = (int32_t)ex[j].path.size();
+            for (size_t t = 0; t < ex[j].path.size(); ++t) paths[(size_t)j * tlt::kMaxDepth + t] = ex[j].path[t];
+            if (rows) std::memcpy(rows + (size_t)j * V, ex[j].row.data(), sizeof(double) * V);
+        }
+    });
+}
+
+TLT_API int tlt_debug_verify_logits(tlt_engine* e, int i, float* logits, int max_rows, int32_t* n_rows) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] {
+        auto& E = *e->e;
+        if (i < 0 || i >= (int)E.dbg_vlogits.size()) throw tlt::ConfigErr("i", "no debug data for request");
+        const auto& v = E.dbg_vlogits[i];
+        const int V = E.cfg.vocab;
+        const int rows = (int)(v.size() / V);
+        *n_rows = rows;
+        std::memcpy(logits, v.data(), sizeof(float) * (size_t)std::min(rows, max_rows) * V);
+    });
+}
+
+TLT_API int tlt_debug_ar_logits(tlt_engine* e, float* logits, int b) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] {
+        auto& E = *e->e;
+        const size_t n = std::min(E.dbg_ar_logits.size(), (size_t)b * E.cfg.vocab);
+        std::memcpy(logits, E.dbg_ar_logits.data(), sizeof(float) * n);
+    });
+}
+
+// ---------------------------------------------------------------- BEG-MAB
+TLT_API int tlt_mab_create(const tlt_strategy* strategies, int n, const int32_t* thresholds, int n_thr, double epsilon,
+                           int window, tlt_mab** out) {
+    if (!strategies || !thresholds || !out) return fail(TLT_ERR_CONFIG, "null argument");
+    return guard([&] {
+        std::vector<tlt_strategy> s(strategies, strategies + n);
+        std::vector<int> t(thresholds, thresholds + n_thr);
+        auto* h = new tlt_mab;
+        try {
+            h->m = std::make_unique<tlt::Mab>(s, t, epsilon, window);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+TLT_API void tlt_mab_destroy(tlt_mab* m) { delete m; }
+TLT_API int tlt_mab_select(tlt_mab* m, int batch, tlt_rng* rng, int32_t* arm, tlt_strategy* out) {
+    if (!m || !rng) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        const size_t a = m->m->select(batch, rng->r);
+        if (arm) *arm = (int32_t)a;
+        if (out) *out = m->m->arms[a].strategy;
+    });
+}
+TLT_API int tlt_mab_record(tlt_mab* m, const tlt_strategy* s, double elapsed, const int32_t* accept_lens, int batch) {
+    if (!m || !s) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { m->m->record(*s, elapsed, accept_lens, batch); });
+}
+TLT_API int tlt_mab_arm_stats(tlt_mab* m, int arm, double* median_reward, int64_t* selections, int32_t* n_rewards) {
+    if (!m) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        if (arm < 0 || arm >= (int)m->m->arms.size()) throw tlt::ConfigErr("arm", "out of range");
+        const auto& a = m->m->arms[arm];
+        if (median_reward) *median_reward = tlt::Mab::median(a.rewards);
+        if (selections) *selections = a.selections;
+        if (n_rewards) *n_rewards = (int32_t)a.rewards.size();
+    });
+}
+TLT_API int tlt_mab_apply_record(tlt_mab* m, int arm, double reward, double a_bar) {
+    if (!m) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        if (arm < 0 || arm >= (int)m->m->arms.size()) throw tlt::ConfigErr("arm", "out of range");
+        m->m->push(m->m->arms[arm], reward, a_bar);
+    });
+}
+
+// ---------------------------------------------------------------- RNG
+TLT_API int tlt_rng_create(uint64_t seed, uint64_t stream_id, tlt_rng** out) {
+    if (!out) return fail(TLT_ERR_CONFIG, "null argument");
+    *out = new tlt_rng{tlt::Rng(seed, stream_id)};
+    return TLT_OK;
+}
+TLT_API int tlt_rng_fork(const tlt_rng* r, uint64_t label, tlt_rng** out) {
+    if (!r || !out) return fail(TLT_ERR_CONFIG, "null argument");
+    *out = new tlt_rng{r->r.fork(label)};
+    return TLT_OK;
+}
+TLT_API void tlt_rng_destroy(tlt_rng* r) { delete r; }
+TLT_API uint64_t tlt_rng_next_u64(tlt_rng* r) { return r->r.next_u64(); }
+TLT_API double tlt_rng_uniform01(tlt_rng* r) { return r->r.uniform01(); }
+
+// ---------------------------------------------------------------- capture plan
+TLT_API int tlt_plan_captures(const tlt_strategy* strategies, int n, const int32_t* thresholds, int n_thr, int max_batch,
+                              int vanilla, tlt_capture_entry* out, int max_entries, int* n_entries,
+                              double* total_memory_units) {
+    if (!strategies || !thresholds) return fail(TLT_ERR_CONFIG, "null argument");
+    return guard([&] {
+        std::vector<tlt_strategy> s(strategies, strategies + n);
+        std::vector<int> t(thresholds, thresholds + n_thr);
+        auto plan = tlt::plan_captures(s, t, max_batch, vanilla != 0, total_memory_units);
+        if (n_entries) *n_entries = (int)plan.size();
+        if ((int)plan.size() > max_entries) throw tlt::ConfigErr("max_entries", "output buffer too small");
+        for (size_t i = 0; i < plan.size(); ++i) out[i] = plan[i];
+    });
+}
+
+// ---------------------------------------------------------------- rollout
+// Reference run_rollout (rollout.hpp:130-276) on the GPU engine: elastic gate,
+// BEG-MAB select/record (measured elapsed), greedy tree SD or plain decode per
+// engine step, emission truncated at EOS / max_len (:231-240), requests
+// finish independently. Each request occupies KV slot i.
+TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* mab, int n, const int32_t* request_ids,
+                            const int32_t* prompt_lens, const int32_t* prompts, const int32_t* max_lens,
+                            int max_len_stride, tlt_rollout_result* out) {
+    if (!e || !cfg || !out) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        auto& E = *e->e;
+        const auto t0 = std::chrono::steady_clock::now();
+        if (n < 1 || n > E.cfg.max_slots) throw tlt::ConfigErr("requests", "count exceeds max_slots");
+        if (cfg->elastic_threshold < 1) throw tlt::ConfigErr("threshold", "must be >= 1");
+        if (cfg->mode != TLT_MODE_GREEDY_TREE) throw tlt::ConfigErr("mode", "only greedy tree SD in this build");
+        if (cfg->use_mab && !mab) throw tlt::ConfigErr("mab", "use_mab requires a bandit state");
+        if (!cfg->use_mab && cfg->enable_sd) tlt::validate(cfg->fixed_strategy);
+        E.use_graphs = cfg->use_graphs != 0;
+        std::vector<int32_t> slots(n);
+        for (int i = 0; i < n; ++i) {
+            slots[i] = i;
+            if (max_lens[i] < 1) throw tlt::ConfigErr("requests", "max_len must be >= 1");
+            if (max_lens[i] > max_len_stride) throw tlt::ConfigErr("max_len_stride", "smaller than max_len");
+        }
+        tlt::Rng root(cfg->seed, 0);
+        std::vector<tlt::Rng> req_rng;
+        for (int i = 0; i < n; ++i) req_rng.push_back(root.fork(0x52515254ULL + (uint64_t)request_ids[i]));
+        tlt::Rng select_rng = root.fork(0x53454CULL);
+        E.prefill(n, slots.data(), prompt_lens, prompts);
+        std::vector<int> running(n, 1), glen(n, 0);
+        out->sd_steps = out->plain_steps = out->verify_events = out->accepted_total = out->emitted_total = 0;
+        out->device_ms = 0.0;
+        const long long launches0 = E.launches;
+        int maxD = 1;
+        if (cfg->use_mab)
+            for (auto& a : mab->m->arms) maxD = std::max(maxD, a.strategy.draft_depth);
+        else
+            maxD = std::max(1, cfg->fixed_strategy.draft_depth);
+        std::vector<int32_t> act, acc_len, bonus, accepted, tok;
+        for (;;) {
+            act.clear();
+            for (int i = 0; i < n; ++i)
+                if (running[i]) act.push_back(i);
+            if (act.empty()) break;
+            const int batch = (int)act.size();
+            const bool sd = cfg->enable_sd && batch < cfg->elastic_threshold;  // rollout.hpp:174
+            auto emit = [&](int i, int32_t t) {
+                out->generated[(size_t)i * max_len_stride + glen[i]] = t;
+                glen[i] += 1;
+                out->emitted_total += 1;
+                if (t == TLT_EOS_TOKEN || glen[i] >= max_lens[i]) {
+                    running[i] = 0;
+                    return true;
+                }
+                return false;
+            };
+            if (sd) {
+                tlt_strategy s = cfg->fixed_strategy;
+                if (cfg->use_mab) s = mab->m->arms[mab->m->select(batch, select_rng)].strategy;
+                const int D = s.draft_depth;
+                acc_len.assign(batch, 0);
+                bonus.assign(batch, 0);
+                accepted.assign((size_t)batch * D, 0);
+                float ms = 0.f;
+                tlt_accept_out ao{accepted.data(), nullptr, acc_len.data(), bonus.data(), nullptr, nullptr, &ms};
+                E.sd_step(s, batch, act.data(), nullptr, &ao);
+                for (int j = 0; j < batch; ++j) {
+                    const int i = act[j];
+                    out->verify_events += 1;
+                    out->accepted_total += acc_len[j];
+                    bool done = false;
+                    for (int t = 0; t < acc_len[j] && !done; ++t) done = emit(i, accepted[(size_t)j * D + t]);
+                    if (!done) emit(i, bonus[j]);
+                }
+                out->device_ms += ms;
+                if (cfg->use_mab) mab->m->record(s, (double)ms, acc_len.data(), batch);  // rollout.hpp:244
+                out->sd_steps += 1;
+            } else {
+                tok.assign(batch, 0);
+                const float ms = E.ar_step(batch, act.data(), tok.data());
+                for (int j = 0; j < batch; ++j) {
+                    req_rng[act[j]].uniform01();  // sample_token consumes one draw (rollout.hpp:253)
+                    emit(act[j], tok[j]);
+                }
+                out->device_ms += ms;
+                out->plain_steps += 1;
+            }
+            for (int j = 0; j < batch; ++j)
+                if (!running[act[j]]) E.release(act[j]);
+        }
+        for (int i = 0; i < n; ++i) out->gen_len[i] = glen[i];
+        out->gpu_launches = E.launches - launches0;
+        (void)maxD;
+        out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,919 @@
+// Engine: weights, caches, forwards, the greedy tree SD step, the AR step and
+// the CUDA-graph pool keyed on the reference CaptureEntry keys
+// (capture_plan.hpp:25-33): one graph per (bucket, top_k, draft_depth,
+// tokens_to_verify) replaying draft -> verify -> accept -> commit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "engine.h"
+
+namespace tlt {
+
+namespace {
+template <typename T>
+T* dmalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    CUDA_CHECK(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+template <typename T>
+T* hmalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    CUDA_CHECK(cudaMallocHost(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+Rows alloc_rows(int n) {
+    Rows r;
+    r.tok = dmalloc<int>(n);
+    r.pos = dmalloc<int>(n);
+    r.slot = dmalloc<int>(n);
+    r.cidx = dmalloc<int>(n);
+    r.fkind = dmalloc<int>(n);
+    r.fidx = dmalloc<long long>(n);
+    r.mask = dmalloc<uint32_t>((size_t)n * kMaskWords);
+    CUDA_CHECK(cudaMemset(r.slot, 0xff, sizeof(int) * n));
+    CUDA_CHECK(cudaMemset(r.mask, 0, sizeof(uint32_t) * (size_t)n * kMaskWords));
+    return r;
+}
+void free_rows(Rows& r) {
+    cudaFree(r.tok);
+    cudaFree(r.pos);
+    cudaFree(r.slot);
+    cudaFree(r.cidx);
+    cudaFree(r.fkind);
+    cudaFree(r.fidx);
+    cudaFree(r.mask);
+}
+Groups alloc_groups(int n) {
+    Groups g;
+    g.slot = dmalloc<int>(n);
+    g.lc = dmalloc<int>(n);
+    g.tail0 = dmalloc<int>(n);
+    g.ntail = dmalloc<int>(n);
+    CUDA_CHECK(cudaMemset(g.slot, 0xff, sizeof(int) * n));
+    CUDA_CHECK(cudaMemset(g.ntail, 0, sizeof(int) * n));
+    return g;
+}
+void free_groups(Groups& g) {
+    cudaFree(g.slot);
+    cudaFree(g.lc);
+    cudaFree(g.tail0);
+    cudaFree(g.ntail);
+}
+Rows sub(const Rows& r, int base) {
+    Rows s = r;
+    s.tok += base;
+    s.pos += base;
+    s.slot += base;
+    s.cidx += base;
+    s.fkind += base;
+    s.fidx += base;
+    s.mask += (size_t)base * kMaskWords;
+    return s;
+}
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+}  // namespace
+
+Engine::Engine(const tlt_model_cfg& c, const tlt_init_cfg& init, int device) : cfg(c), dev_(device) {
+    if (c.vocab < 2) throw ConfigErr("vocab", "must be >= 2");
+    if (c.hidden % 64 != 0) throw ConfigErr("hidden", "must be a multiple of 64");
+    if (c.head_dim != 64 && c.head_dim != 128) throw ConfigErr("head_dim", "must be 64 or 128");
+    if (c.heads < 1 || c.kv_heads < 1 || c.heads % c.kv_heads) throw ConfigErr("kv_heads", "must divide heads");
+    if (c.ffn % 8 != 0) throw ConfigErr("ffn", "must be a multiple of 8");
+    if (c.layers < 1) throw ConfigErr("layers", "must be >= 1");
+    if (c.max_slots < 1 || c.max_ctx < 2) throw ConfigErr("max_ctx", "must be >= 2");
+    CUDA_CHECK(cudaSetDevice(device));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreate(&ev0_));
+    CUDA_CHECK(cudaEventCreate(&ev1_));
+    ip_ = tlt_init_params{init.seed, init.layer_scale, init.lm_gain, init.lm_noise, init.fc_noise,
+                          c.vocab,   c.hidden,         c.heads,      c.kv_heads,    c.head_dim, c.ffn};
+    alloc_weights(init);
+    alloc_state();
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+Engine::~Engine() {
+    cudaSetDevice(dev_);
+    graph_pool_clear();
+    cudaStreamSynchronize(st_);
+    auto f = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    f(embed_), f(lm_head_), f(final_norm_), f(fc_), f(rope_cos_), f(rope_sin_);
+    for (auto& L : layers_) f(L.attn_norm), f(L.qkv), f(L.qkv_b), f(L.o), f(L.mlp_norm), f(L.gu), f(L.down);
+    f(drafter_.attn_norm), f(drafter_.qkv), f(drafter_.qkv_b), f(drafter_.o), f(drafter_.mlp_norm), f(drafter_.gu),
+        f(drafter_.down);
+    for (auto p : kc_) f(p);
+    for (auto p : vc_) f(p);
+    f(dkc_), f(dvc_), f(d_kc_arr_), f(d_vc_arr_), f(tok_hist_), f(feat_hist_);
+    f(x_), f(xg_), f(h_), f(q_), f(attn_), f(act_), f(feat_), f(x2_), f(dfeat_), f(logits_), f(ws_);
+    f(aws_m_), f(aws_l_), f(aws_o_);
+    free_rows(drows_), free_rows(vrows_), free_rows(prows_);
+    for (auto& g : dg_) free_groups(g);
+    free_groups(vg_), free_groups(pg_);
+    f(root_row_), f(row_node_), f(tk_tok_), f(tk_logit_), f(tk_M_), f(tk_S_), f(argmax_), f(dbg_probs_);
+    f(arena_), f(arena_n_), f(kept_), f(kept_n_), f(exp_n_), f(done_);
+    f(tree_tok_), f(tree_par_), f(tree_dep_), f(tree_n_), f(tree_prob_), f(tree_pp_);
+    f(acc_nodes_), f(acc_tok_), f(acc_len_), f(bonus_), f(kv_len_), f(ar_tok_), f(d_step_);
+    if (h_step_) cudaFreeHost(h_step_);
+    void* hp[] = {ho_.acc_len, ho_.bonus, ho_.acc_tok, ho_.acc_nodes, ho_.tree_tok, ho_.tree_par,
+                  ho_.tree_dep, ho_.tree_prob, ho_.tree_pp, ho_.tree_n, ho_.ar_tok};
+    for (void* p : hp)
+        if (p) cudaFreeHost(p);
+    cudaEventDestroy(ev0_);
+    cudaEventDestroy(ev1_);
+    cudaStreamDestroy(st_);
+}
+
+void Engine::alloc_weights(const tlt_init_cfg&) {
+    const long long V = cfg.vocab, d = cfg.hidden, F = cfg.ffn;
+    const long long nqkv = (long long)(cfg.heads + 2 * cfg.kv_heads) * cfg.head_dim;
+    const long long nq = (long long)cfg.heads * cfg.head_dim;
+    auto W = [&](long long n, int tensor, int layer) {
+        bf16* p = dmalloc<bf16>(n);
+        launch_init(reinterpret_cast<uint16_t*>(p), n, ip_, tensor, layer, st_);
+        CUDA_CHECK(cudaGetLastError());
+        return p;
+    };
+    embed_ = W(V * d, TLT_W_EMBED, 0);
+    lm_head_ = W(V * d, TLT_W_LM_HEAD, 0);
+    final_norm_ = W(d, TLT_W_FINAL_NORM, 0);
+    fc_ = W(d * 2 * d, TLT_W_FC, TLT_DRAFTER_LAYER);
+    auto mk_layer = [&](int l) {
+        LayerW L;
+        L.attn_norm = W(d, TLT_W_ATTN_NORM, l);
+        L.qkv = W(nqkv * d, TLT_W_QKV, l);
+        L.qkv_b = cfg.qkv_bias ? W(nqkv, TLT_W_QKV_BIAS, l) : nullptr;
+        L.o = W(d * nq, TLT_W_O, l);
+        L.mlp_norm = W(d, TLT_W_MLP_NORM, l);
+        L.gu = W(2 * F * d, TLT_W_GATE_UP, l);
+        L.down = W(d * F, TLT_W_DOWN, l);
+        L.tm_qkv = make_tmap_bf16(L.qkv, (int)nqkv, (int)d, d, 128);
+        L.tm_o = make_tmap_bf16(L.o, (int)d, (int)nq, nq, 128);
+        L.tm_gu = make_tmap_bf16(L.gu, (int)(2 * F), (int)d, d, 128);
+        L.tm_down = make_tmap_bf16(L.down, (int)d, (int)F, F, 128);
+        return L;
+    };
+    for (int l = 0; l < cfg.layers; ++l) layers_.push_back(mk_layer(l));
+    drafter_ = mk_layer(TLT_DRAFTER_LAYER);
+    tm_lm_ = make_tmap_bf16(lm_head_, (int)V, (int)d, d, 128);
+    tm_fc_ = make_tmap_bf16(fc_, (int)d, (int)(2 * d), 2 * d, 128);
+    // RoPE table, computed in double exactly as the oracle does, stored fp32
+    cap_ = cfg.max_ctx + kMaxT + 2;
+    const int half = cfg.head_dim / 2;
+    const int rope_rows = cap_ + kMaxDepth + 2;
+    std::vector<float> cs((size_t)rope_rows * half), sn((size_t)rope_rows * half);
+    for (int pos = 0; pos < rope_rows; ++pos)
+        for (int i = 0; i < half; ++i) {
+            double inv = std::pow((double)cfg.rope_theta, -2.0 * (double)i / (double)cfg.head_dim);
+            double ang = (double)pos * inv;
+            cs[(size_t)pos * half + i] = (float)std::cos(ang);
+            sn[(size_t)pos * half + i] = (float)std::sin(ang);
+        }
+    rope_cos_ = dmalloc<float>(cs.size());
+    rope_sin_ = dmalloc<float>(sn.size());
+    CUDA_CHECK(cudaMemcpy(rope_cos_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(rope_sin_, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+}
+
+void Engine::alloc_state() {
+    const int S = cfg.max_slots, KV = cfg.kv_heads, hd = cfg.head_dim, d = cfg.hidden, V = cfg.vocab;
+    dcap_ = cap_ + 1024 + 8;
+    const size_t kv_elems = (size_t)S * KV * cap_ * hd;
+    for (int l = 0; l < cfg.layers; ++l) {
+        kc_.push_back(dmalloc<bf16>(kv_elems));
+        vc_.push_back(dmalloc<bf16>(kv_elems));
+    }
+    dkc_ = dmalloc<bf16>((size_t)S * KV * dcap_ * hd);
+    dvc_ = dmalloc<bf16>((size_t)S * KV * dcap_ * hd);
+    d_kc_arr_ = dmalloc<bf16*>(cfg.layers);
+    d_vc_arr_ = dmalloc<bf16*>(cfg.layers);
+    CUDA_CHECK(cudaMemcpy(d_kc_arr_, kc_.data(), sizeof(bf16*) * cfg.layers, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(d_vc_arr_, vc_.data(), sizeof(bf16*) * cfg.layers, cudaMemcpyHostToDevice));
+    tok_hist_ = dmalloc<int32_t>((size_t)S * cap_);
+    CUDA_CHECK(cudaMemset(tok_hist_, 0, sizeof(int32_t) * (size_t)S * cap_));
+    feat_hist_ = dmalloc<bf16>((size_t)S * cap_ * d);
+
+    R_ = env_int("TLT_MAX_ROWS", 2048);
+    Rmeta_ = env_int("TLT_MAX_DRAFT_ROWS", 32768);
+    const int nq = cfg.heads * hd, nqkv = (cfg.heads + 2 * KV) * hd;
+    x_ = dmalloc<float>((size_t)R_ * 2 * d);
+    xg_ = dmalloc<float>((size_t)R_ * d);
+    h_ = dmalloc<bf16>((size_t)R_ * 2 * d);
+    q_ = dmalloc<bf16>((size_t)R_ * std::max(nq, nqkv));
+    attn_ = dmalloc<bf16>((size_t)R_ * nq);
+    act_ = dmalloc<bf16>((size_t)R_ * cfg.ffn);
+    feat_ = dmalloc<bf16>((size_t)R_ * d);
+    x2_ = dmalloc<bf16>((size_t)R_ * 2 * d);
+    dfeat_ = dmalloc<bf16>((size_t)Rmeta_ * d);
+    logits_ = dmalloc<float>((size_t)R_ * V);
+    ws_elems_ = (size_t)env_int("TLT_GEMM_WS_MFLOATS", 64) << 20;
+    ws_ = dmalloc<float>(ws_elems_);
+    aws_elems_ = (size_t)env_int("TLT_ATTN_WS_MFLOATS", 48) << 20;
+    aws_m_ = dmalloc<float>(aws_elems_ / 32);
+    aws_l_ = dmalloc<float>(aws_elems_ / 32);
+    aws_o_ = dmalloc<float>(aws_elems_);
+    drows_ = alloc_rows(Rmeta_);
+    vrows_ = alloc_rows(R_);
+    prows_ = alloc_rows(R_);
+    max_b_ = S;
+    for (auto& g : dg_) g = alloc_groups(S);
+    vg_ = alloc_groups(S);
+    pg_ = alloc_groups(std::max(S, R_));
+    root_row_ = dmalloc<int>(S);
+    row_node_ = dmalloc<int>(Rmeta_);
+    tk_tok_ = dmalloc<int>((size_t)R_ * kMaxTopK);
+    tk_logit_ = dmalloc<float>((size_t)R_ * kMaxTopK);
+    tk_M_ = dmalloc<float>(R_);
+    tk_S_ = dmalloc<float>(R_);
+    argmax_ = dmalloc<int>(R_);
+    arena_ = dmalloc<Cand>((size_t)S * arena_cap_);
+    arena_n_ = dmalloc<int>(S);
+    kept_ = dmalloc<int>((size_t)S * kMaxT);
+    kept_n_ = dmalloc<int>(S);
+    exp_n_ = dmalloc<int>(S);
+    done_ = dmalloc<int>(S);
+    tree_tok_ = dmalloc<int>((size_t)S * kMaxT);
+    tree_par_ = dmalloc<int>((size_t)S * kMaxT);
+    tree_dep_ = dmalloc<int>((size_t)S * kMaxT);
+    tree_n_ = dmalloc<int>(S);
+    tree_prob_ = dmalloc<double>((size_t)S * kMaxT);
+    tree_pp_ = dmalloc<double>((size_t)S * kMaxT);
+    acc_nodes_ = dmalloc<int>((size_t)S * kMaxD);
+    acc_tok_ = dmalloc<int>((size_t)S * kMaxD);
+    acc_len_ = dmalloc<int>(S);
+    bonus_ = dmalloc<int>(S);
+    kv_len_ = dmalloc<int>(S);
+    ar_tok_ = dmalloc<int>(S);
+    d_step_ = dmalloc<StepIn>(S);
+    h_step_ = hmalloc<StepIn>(S);
+    ho_.acc_len = hmalloc<int32_t>(S);
+    ho_.bonus = hmalloc<int32_t>(S);
+    ho_.acc_tok = hmalloc<int32_t>((size_t)S * kMaxD);
+    ho_.acc_nodes = hmalloc<int32_t>((size_t)S * kMaxD);
+    ho_.tree_tok = hmalloc<int32_t>((size_t)S * kMaxT);
+    ho_.tree_par = hmalloc<int32_t>((size_t)S * kMaxT);
+    ho_.tree_dep = hmalloc<int32_t>((size_t)S * kMaxT);
+    ho_.tree_prob = hmalloc<double>((size_t)S * kMaxT);
+    ho_.tree_pp = hmalloc<double>((size_t)S * kMaxT);
+    ho_.tree_n = hmalloc<int32_t>(S);
+    ho_.ar_tok = hmalloc<int32_t>(S);
+    lt_.assign(S, 0);
+    ld_.assign(S, 0);
+    live_.assign(S, 0);
+}
+
+// ------------------------------------------------------------------ helpers
+const CUtensorMap& Engine::tmap_act(const void* p, int rows, int cols, long long ld, int box) {
+    char key[96];
+    std::snprintf(key, sizeof key, "%p/%d/%d/%lld/%d", p, rows, cols, ld, box);
+    auto it = tmaps_.find(key);
+    if (it != tmaps_.end()) return it->second;
+    return tmaps_.emplace(key, make_tmap_bf16(p, rows, cols, ld, box)).first->second;
+}
+
+void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep_in) {
+    GemmPlan g = plan_gemm(M, N, K);
+    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.bn);
+    EpiParams ep = ep_in;
+    ep.n_out = N;
+    ep.m_tok = M;
+    launch_gemm(g, tmW, tx, ep, ws_, ws_elems_, st_);
+    count_launch(g.splits > 1 ? 2 : 1);
+}
+
+void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int rpr,
+                       int ngroups, int max_keys) {
+    AttnParams p{};
+    p.q = q_;
+    p.out = attn_;
+    p.kc = kc;
+    p.vc = vc;
+    p.rows = rw;
+    p.g = gp;
+    p.rows_per_req = rpr;
+    p.n_groups = ngroups;
+    p.H = cfg.heads;
+    p.KV = cfg.kv_heads;
+    p.hd = cfg.head_dim;
+    p.cap = cache_cap;
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)cfg.head_dim));
+    p.chunk = 512;
+    p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+    p.qv_cap = rpr * (cfg.heads / cfg.kv_heads);
+    const size_t need = (size_t)ngroups * p.max_splits * p.qv_cap * cfg.kv_heads;
+    if (need * cfg.head_dim > aws_elems_ || need > aws_elems_ / 32)
+        throw CudaError("attention workspace too small (set TLT_ATTN_WS_MFLOATS)");
+    p.ws_m = aws_m_;
+    p.ws_l = aws_l_;
+    p.ws_o = aws_o_;
+    launch_attention(p, st_);
+    count_launch(2);
+}
+
+// One decoder layer over R rows (residual x_ in place).
+void Engine::layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, const Rows& rw, const Groups& gp,
+                           int R, int rpr, int ngroups, int max_keys) {
+    const int d = cfg.hidden, hd = cfg.head_dim;
+    const int nq = cfg.heads * hd, nkv = cfg.kv_heads * hd;
+    launch_rmsnorm(x_, R, d, w.attn_norm, cfg.rms_eps, h_, st_);
+    count_launch();
+    EpiParams e{};
+    e.kind = EPI_QKV;
+    e.out_bf16 = q_;
+    e.ld_bf16 = nq;
+    e.bias = w.qkv_b;
+    e.rope_cos = rope_cos_;
+    e.rope_sin = rope_sin_;
+    e.tok_pos = rw.pos;
+    e.tok_slot = rw.slot;
+    e.tok_cidx = rw.cidx;
+    e.kcache = kc;
+    e.vcache = vc;
+    e.n_q = nq;
+    e.n_kvr = nkv;
+    e.head_dim = hd;
+    e.n_kv = cfg.kv_heads;
+    e.max_ctx = cache_cap;
+    gemm(h_, R, d, d, w.tm_qkv, nq + 2 * nkv, e);
+    attention(kc, vc, cache_cap, rw, gp, rpr, ngroups, max_keys);
+    EpiParams o{};
+    o.kind = EPI_RESID_ADD;
+    o.out_f32 = x_;
+    o.ld_f32 = d;
+    gemm(attn_, R, nq, nq, w.tm_o, d, o);
+    launch_rmsnorm(x_, R, d, w.mlp_norm, cfg.rms_eps, h_, st_);
+    count_launch();
+    EpiParams s{};
+    s.kind = EPI_SWIGLU;
+    s.out_bf16 = act_;
+    s.ld_bf16 = cfg.ffn;
+    gemm(h_, R, d, d, w.tm_gu, 2 * cfg.ffn, s);
+    EpiParams dn{};
+    dn.kind = EPI_RESID_ADD;
+    dn.out_f32 = x_;
+    dn.ld_f32 = d;
+    gemm(act_, R, cfg.ffn, cfg.ffn, w.tm_down, d, dn);
+}
+
+void Engine::lm_head(const float* x, int n, float* logits) {
+    launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
+    count_launch();
+    EpiParams e{};
+    e.kind = EPI_F32;
+    e.out_f32 = logits;
+    e.ld_f32 = cfg.vocab;
+    gemm(h_, n, cfg.hidden, cfg.hidden, tm_lm_, cfg.vocab, e);
+}
+
+void Engine::target_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
+                            float* logits, bf16* feat) {
+    if (R > R_) throw ConfigErr("rows", "forward exceeds TLT_MAX_ROWS");
+    launch_embed(rw, R, embed_, cfg.hidden, x_, st_);
+    count_launch();
+    for (int l = 0; l < cfg.layers; ++l) layer_forward(layers_[l], kc_[l], vc_[l], cap_, rw, gp, R, rpr, ngroups, max_keys);
+    if (feat) {
+        launch_to_bf16(x_, (long long)R * cfg.hidden, feat, st_);
+        count_launch();
+    }
+    if (logits) lm_head(x_, R, logits);
+}
+
+void Engine::drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
+                             const int* gather, int n_lm, float* logits, bf16* dfeat_out) {
+    if (R > R_) throw ConfigErr("rows", "drafter forward exceeds TLT_MAX_ROWS");
+    const int d = cfg.hidden;
+    launch_draft_in(rw, R, embed_, d, feat_hist_, dfeat_, x2_, st_);
+    count_launch();
+    EpiParams e{};
+    e.kind = EPI_F32;
+    e.out_f32 = x_;
+    e.ld_f32 = d;
+    gemm(x2_, R, 2 * d, 2 * d, tm_fc_, d, e);
+    layer_forward(drafter_, dkc_, dvc_, dcap_, rw, gp, R, rpr, ngroups, max_keys);
+    if (dfeat_out) {
+        launch_to_bf16(x_, (long long)R * d, dfeat_out, st_);
+        count_launch();
+    }
+    if (logits) {
+        if (gather) {
+            launch_gather_rows(x_, gather, n_lm, d, xg_, st_);
+            count_launch();
+            lm_head(xg_, n_lm, logits);
+        } else {
+            lm_head(x_, n_lm, logits);
+        }
+    }
+}
+
+__global__ void k_scatter_feat(Rows rows, int d, const __nv_bfloat16* __restrict__ feat, __nv_bfloat16* hist, int cap) {
+    const int r = blockIdx.x;
+    const int slot = rows.slot[r];
+    if (slot < 0) return;
+    const long long dst = ((long long)slot * cap + rows.pos[r]) * d;
+    for (int e = threadIdx.x; e < d; e += blockDim.x) hist[dst + e] = feat[(long long)r * d + e];
+}
+
+void Engine::scatter_features(const Rows& rw, int R, const bf16* feat) {
+    k_scatter_feat<<<R, 256, 0, st_>>>(rw, cfg.hidden, feat, feat_hist_, cap_);
+    CUDA_CHECK(cudaGetLastError());
+    count_launch();
+}
+
+void Engine::upload_rows_host(const std::vector<int>& tok, const std::vector<int>& pos, const std::vector<int>& slot,
+                              const std::vector<int>& cidx, const std::vector<int>& fkind,
+                              const std::vector<long long>& fidx, const std::vector<uint32_t>& mask,
+                              const std::vector<int>& gslot, const std::vector<int>& glc, const std::vector<int>& gt0,
+                              const std::vector<int>& gnt) {
+    const size_t n = tok.size(), g = gslot.size();
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st_));
+    };
+    up(prows_.tok, tok.data(), n * 4);
+    up(prows_.pos, pos.data(), n * 4);
+    up(prows_.slot, slot.data(), n * 4);
+    up(prows_.cidx, cidx.data(), n * 4);
+    up(prows_.fkind, fkind.data(), n * 4);
+    up(prows_.fidx, fidx.data(), n * 8);
+    up(prows_.mask, mask.data(), n * kMaskWords * 4);
+    up(pg_.slot, gslot.data(), g * 4);
+    up(pg_.lc, glc.data(), g * 4);
+    up(pg_.tail0, gt0.data(), g * 4);
+    up(pg_.ntail, gnt.data(), g * 4);
+    CUDA_CHECK(cudaStreamSynchronize(st_));  // host vectors are freed on return
+}
+
+// ------------------------------------------------------------------ prefill
+// Positions 0..len-2 of each prompt through the target (KV + features), then
+// the drafter over the same positions with inputs (f_{p-1}, e(x_p)). The last
+// prompt token is the first step's root.
+void Engine::prefill(int b, const int32_t* slots, const int32_t* lens, const int32_t* tokens) {
+    std::vector<int> off(b + 1, 0);
+    for (int i = 0; i < b; ++i) {
+        if (slots[i] < 0 || slots[i] >= cfg.max_slots) throw ConfigErr("slot_ids", "slot out of range");
+        if (lens[i] < 1) throw ConfigErr("lens", "prompt must hold >= 1 token");
+        if (lens[i] + 1 > cfg.max_ctx) throw ConfigErr("lens", "prompt exceeds max_ctx");
+        off[i + 1] = off[i] + lens[i];
+    }
+    // token histories
+    for (int i = 0; i < b; ++i)
+        CUDA_CHECK(cudaMemcpyAsync(tok_hist_ + (size_t)slots[i] * cap_, tokens + off[i], sizeof(int32_t) * lens[i],
+                                   cudaMemcpyHostToDevice, st_));
+    const int chunk = std::min(512, std::max(1, R_ / 2));
+    // process requests in groups; each group forward has stride = chunk rows per request
+    for (int i0 = 0; i0 < b;) {
+        int nreq = std::max(1, std::min(b - i0, R_ / chunk));
+        const int i1 = i0 + nreq;
+        int max_rows = 0;
+        for (int i = i0; i < i1; ++i) max_rows = std::max(max_rows, lens[i] - 1);
+        for (int c0 = 0; c0 < max_rows; c0 += chunk) {
+            const int R = nreq * chunk;
+            std::vector<int> tok(R, 0), pos(R, 0), slot(R, -1), cidx(R, 0), fk(R, 0), gs(nreq, -1), glc(nreq, 0),
+                gt0(nreq, 0), gnt(nreq, 0);
+            std::vector<long long> fidx(R, 0);
+            std::vector<uint32_t> mask((size_t)R * kMaskWords, 0u);
+            for (int q = 0; q < nreq; ++q) {
+                const int i = i0 + q, s = slots[i], n = lens[i] - 1;
+                const int cn = std::max(0, std::min(chunk, n - c0));
+                gs[q] = cn > 0 ? s : -1;
+                glc[q] = c0;
+                gt0[q] = c0;
+                gnt[q] = cn;
+                for (int j = 0; j < cn; ++j) {
+                    const int r = q * chunk + j, p = c0 + j;
+                    tok[r] = tokens[off[i] + p];
+                    pos[r] = p;
+                    slot[r] = s;
+                    cidx[r] = p;
+                    fk[r] = p > 0 ? 1 : 0;
+                    fidx[r] = (long long)s * cap_ + p - 1;
+                    for (int t = 0; t <= j; ++t) mask[(size_t)r * kMaskWords + (t >> 5)] |= 1u << (t & 31);
+                }
+            }
+            upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, gs, glc, gt0, gnt);
+            target_forward(prows_, pg_, R, chunk, nreq, c0 + chunk, nullptr, feat_);
+            scatter_features(prows_, R, feat_);
+            drafter_forward(prows_, pg_, R, chunk, nreq, c0 + chunk, nullptr, 0, nullptr, nullptr);
+        }
+        i0 = i1;
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    for (int i = 0; i < b; ++i) {
+        lt_[slots[i]] = lens[i] - 1;
+        ld_[slots[i]] = lens[i] - 1;
+        live_[slots[i]] = 1;
+    }
+}
+
+void Engine::release(int slot) {
+    if (slot < 0 || slot >= cfg.max_slots) throw ConfigErr("slot_id", "out of range");
+    live_[slot] = 0;
+    lt_[slot] = ld_[slot] = 0;
+}
+
+// Drafter catch-up (after plain-decode steps): committed positions [ld, lt)
+// with target features, chunked. The SD graph then sees exactly 1 + accepted
+// pending rows per request.
+void Engine::catchup_drafter(int b, const int32_t* slots) {
+    const int chunk = 256;
+    for (int i = 0; i < b; ++i) {
+        const int s = slots[i];
+        while (lt_[s] - ld_[s] > 0) {
+            const int n = std::min(chunk, lt_[s] - ld_[s]);
+            const int c0 = ld_[s];
+            std::vector<int> tok(chunk, 0), pos(chunk, 0), slot(chunk, -1), cidx(chunk, 0), fk(chunk, 0);
+            std::vector<long long> fidx(chunk, 0);
+            std::vector<uint32_t> mask((size_t)chunk * kMaskWords, 0u);
+            std::vector<int32_t> htok(n);
+            CUDA_CHECK(cudaMemcpy(htok.data(), tok_hist_ + (size_t)s * cap_ + c0, sizeof(int32_t) * n,
+                                  cudaMemcpyDeviceToHost));
+            for (int j = 0; j < n; ++j) {
+                tok[j] = htok[j];
+                pos[j] = cidx[j] = c0 + j;
+                slot[j] = s;
+                fk[j] = c0 + j > 0 ? 1 : 0;
+                fidx[j] = (long long)s * cap_ + c0 + j - 1;
+                for (int t = 0; t <= j; ++t) mask[(size_t)j * kMaskWords + (t >> 5)] |= 1u << (t & 31);
+            }
+            upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, {s}, {c0}, {c0}, {n});
+            drafter_forward(prows_, pg_, chunk, chunk, 1, c0 + chunk, nullptr, 0, nullptr, nullptr);
+            ld_[s] += n;
+        }
+    }
+}
+
+int Engine::bucket_hi_for(int b, int T) const {
+    (void)T;
+    return b;
+}
+
+// ----------------------------------------------------------- SD device seq
+// draft (D levels) -> tree final -> verify forward -> argmax -> accept ->
+// commit. All shapes static in (b_hi, D, k, T); per-step data lives on the
+// device (StepIn uploaded first), so the sequence is graph-capturable.
+void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real) {
+    const int d = cfg.hidden, V = cfg.vocab, D1 = D + 1;
+    CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
+    // level bases
+    std::vector<int> base(D + 2, 0), Fd(D + 2, 0);
+    base[1] = 0;
+    Fd[1] = D1;  // rows per request at level 1 (pending + root)
+    long long kp = 1;
+    for (int lv = 2; lv <= D; ++lv) {
+        kp = std::min<long long>(kp * k, 1 << 20);
+        Fd[lv] = (int)std::min<long long>(T, kp);
+        base[lv] = base[lv - 1] + b_hi * Fd[lv - 1];
+    }
+    if (D >= 2 && base[D] + b_hi * Fd[D] > Rmeta_) throw ConfigErr("strategy", "draft rows exceed TLT_MAX_DRAFT_ROWS");
+    const int max_keys_t = cap_;
+    const int max_keys_d = dcap_;
+    launch_rows_level1(d_step_, b_hi, b_hi, D1, drows_, dg_[1], root_row_, tok_hist_, cap_, st_);
+    count_launch();
+    TreeParams tp{};
+    tp.step = d_step_;
+    tp.b = b_hi;
+    tp.b_hi = b_hi;
+    tp.D = D;
+    tp.k = k;
+    tp.T = T;
+    tp.arena = arena_;
+    tp.arena_cap = arena_cap_;
+    tp.arena_n = arena_n_;
+    tp.kept = kept_;
+    tp.kept_n = kept_n_;
+    tp.exp_n = exp_n_;
+    tp.done = done_;
+    tp.row_node = row_node_;
+    tp.root_row = root_row_;
+    tp.tk_tok = tk_tok_;
+    tp.tk_logit = tk_logit_;
+    tp.tk_M = tk_M_;
+    tp.tk_S = tk_S_;
+    tp.rows = drows_;
+    tp.tree_tok = tree_tok_;
+    tp.tree_par = tree_par_;
+    tp.tree_dep = tree_dep_;
+    tp.tree_prob = tree_prob_;
+    tp.tree_pp = tree_pp_;
+    tp.tree_n = tree_n_;
+    tp.vrows = vrows_;
+    tp.vg = vg_;
+    tp.tok_hist = tok_hist_;
+    tp.cap = cap_;
+    if (dbg) {
+        dbg_exp.assign(b_real, {});
+        if (!dbg_probs_) dbg_probs_ = dmalloc<double>((size_t)std::max(R_, 256) * V);
+    }
+    for (int lv = 1; lv <= D; ++lv) {
+        const int R = b_hi * Fd[lv];
+        const Rows rw = sub(drows_, base[lv]);
+        const int n_lm = lv == 1 ? b_hi : R;
+        drafter_forward(rw, dg_[lv], R, Fd[lv], b_hi, max_keys_d, lv == 1 ? root_row_ : nullptr, n_lm, logits_,
+                        dfeat_ + (size_t)base[lv] * d);
+        launch_row_topk(logits_, n_lm, V, lv == 1 ? dg_[1].slot : rw.slot, k, 1, tk_tok_, tk_logit_, tk_M_, tk_S_,
+                        st_);
+        count_launch();
+        if (dbg) {
+            // full fp64 rows of every live expansion (parity export)
+            launch_row_probs(logits_, n_lm, V, tk_M_, tk_S_, dbg_probs_, st_);
+            std::vector<int> live(n_lm), node(n_lm);
+            std::vector<double> rowsbuf((size_t)n_lm * V);
+            CUDA_CHECK(cudaMemcpyAsync(live.data(), lv == 1 ? dg_[1].slot : rw.slot, sizeof(int) * n_lm,
+                                       cudaMemcpyDeviceToHost, st_));
+            if (lv > 1)
+                CUDA_CHECK(cudaMemcpyAsync(node.data(), row_node_ + base[lv], sizeof(int) * n_lm,
+                                           cudaMemcpyDeviceToHost, st_));
+            CUDA_CHECK(cudaMemcpyAsync(rowsbuf.data(), dbg_probs_, sizeof(double) * n_lm * V, cudaMemcpyDeviceToHost,
+                                       st_));
+            std::vector<Cand> ar((size_t)b_real * arena_cap_);
+            CUDA_CHECK(cudaMemcpyAsync(ar.data(), arena_, sizeof(Cand) * ar.size(), cudaMemcpyDeviceToHost, st_));
+            CUDA_CHECK(cudaStreamSynchronize(st_));
+            for (int r = 0; r < n_lm; ++r) {
+                if (live[r] < 0) continue;
+                const int i = lv == 1 ? r : r / Fd[lv];
+                if (i >= b_real) continue;
+                DebugExp ex;
+                if (lv > 1) {
+                    for (int a = node[r]; a >= 0; a = ar[(size_t)i * arena_cap_ + a].parent)
+                        ex.path.push_back(ar[(size_t)i * arena_cap_ + a].token);
+                    std::reverse(ex.path.begin(), ex.path.end());
+                }
+                ex.row.assign(rowsbuf.begin() + (size_t)r * V, rowsbuf.begin() + (size_t)(r + 1) * V);
+                dbg_exp[i].push_back(std::move(ex));
+            }
+        }
+        tp.level = lv;
+        tp.lvl_base = base[lv];
+        tp.lm_F = lv == 1 ? 1 : Fd[lv];
+        tp.nxt_base = lv < D ? base[lv + 1] : 0;
+        tp.nxt_F = lv < D ? Fd[lv + 1] : 0;
+        tp.g_next = dg_[std::min(lv + 1, kMaxDepth + 1)];
+        launch_tree_level(tp, st_);
+        count_launch();
+    }
+    launch_tree_final(tp, st_);
+    count_launch();
+    // target verify over root + tree
+    const int T1 = T + 1, RV = b_hi * T1;
+    target_forward(vrows_, vg_, RV, T1, b_hi, max_keys_t, logits_, feat_);
+    if (dbg) {
+        dbg_vlogits.assign(b_real, {});
+        std::vector<float> lg((size_t)RV * V);
+        CUDA_CHECK(cudaMemcpyAsync(lg.data(), logits_, sizeof(float) * lg.size(), cudaMemcpyDeviceToHost, st_));
+        CUDA_CHECK(cudaStreamSynchronize(st_));
+        for (int i = 0; i < b_real; ++i)
+            dbg_vlogits[i].assign(lg.begin() + (size_t)i * T1 * V, lg.begin() + (size_t)(i + 1) * T1 * V);
+    }
+    launch_row_topk(logits_, RV, V, vrows_.slot, 1, 0, argmax_, tk_logit_, nullptr, nullptr, st_);
+    count_launch();
+    AcceptParams ap{};
+    ap.step = d_step_;
+    ap.b = b_hi;
+    ap.b_hi = b_hi;
+    ap.T = T;
+    ap.maxD = kMaxD;
+    ap.tree_tok = tree_tok_;
+    ap.tree_par = tree_par_;
+    ap.tree_n = tree_n_;
+    ap.argmax = argmax_;
+    ap.acc_nodes = acc_nodes_;
+    ap.acc_tok = acc_tok_;
+    ap.acc_len = acc_len_;
+    ap.bonus = bonus_;
+    launch_accept_greedy(ap, st_);
+    count_launch();
+    CommitParams cp{};
+    cp.step = d_step_;
+    cp.b = b_hi;
+    cp.b_hi = b_hi;
+    cp.maxD = kMaxD;
+    cp.layers = cfg.layers;
+    cp.KV = cfg.kv_heads;
+    cp.hd = cfg.head_dim;
+    cp.cap = cap_;
+    cp.d = d;
+    cp.row_stride = T1;
+    cp.kc = d_kc_arr_;
+    cp.vc = d_vc_arr_;
+    cp.acc_nodes = acc_nodes_;
+    cp.acc_tok = acc_tok_;
+    cp.acc_len = acc_len_;
+    cp.bonus = bonus_;
+    cp.tok_hist = tok_hist_;
+    cp.feat_hist = feat_hist_;
+    cp.vfeat = feat_;
+    cp.kv_len = kv_len_;
+    launch_commit(cp, st_);
+    count_launch();
+    // results -> pinned host
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st_));
+    };
+    d2h(ho_.acc_len, acc_len_, sizeof(int) * b_hi);
+    d2h(ho_.bonus, bonus_, sizeof(int) * b_hi);
+    d2h(ho_.acc_tok, acc_tok_, sizeof(int) * b_hi * kMaxD);
+    d2h(ho_.acc_nodes, acc_nodes_, sizeof(int) * b_hi * kMaxD);
+    d2h(ho_.tree_tok, tree_tok_, sizeof(int) * b_hi * T);
+    d2h(ho_.tree_par, tree_par_, sizeof(int) * b_hi * T);
+    d2h(ho_.tree_dep, tree_dep_, sizeof(int) * b_hi * T);
+    d2h(ho_.tree_prob, tree_prob_, sizeof(double) * b_hi * T);
+    d2h(ho_.tree_pp, tree_pp_, sizeof(double) * b_hi * T);
+    d2h(ho_.tree_n, tree_n_, sizeof(int) * b_hi);
+}
+
+float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out) {
+    const int D = s.draft_depth, k = s.top_k, T = s.tokens_to_verify;
+    if (D < 1) throw ConfigErr("draft_depth", "must be >= 1");
+    if (k < 1) throw ConfigErr("top_k", "must be >= 1");
+    if (T < 1) throw ConfigErr("tokens_to_verify", "must be >= 1");
+    {  // capacity (spec_decode.hpp:25-42)
+        long long total = 0, level = 1;
+        for (int i = 0; i < D && total < (1LL << 40); ++i) {
+            level = std::min(level * k, 1LL << 40);
+            total += level;
+        }
+        if (T > total) throw ConfigErr("tokens_to_verify", "exceeds tree capacity for (top_k, draft_depth)");
+    }
+    if (D > kMaxD - 1 || k > kMaxTopK || T > kMaxT) throw ConfigErr("strategy", "exceeds engine limits (D<=15,k<=8,T<=128)");
+    if ((long long)(D - 1) * T + 1 > kMaskWords * 32) throw ConfigErr("strategy", "too many drafter expansions");
+    if ((long long)k * std::min(T, (int)std::min<long long>(1LL << 20, (long long)std::pow(k, D - 1))) > 1024 ||
+        T + (long long)k * T > 2048)
+        throw ConfigErr("strategy", "frontier too large");
+    if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");
+    for (int i = 0; i < b; ++i) {
+        const int sl = slots[i];
+        if (sl < 0 || sl >= cfg.max_slots || !live_[sl]) throw ConfigErr("slot_ids", "slot not prefilled");
+        if (lt_[sl] + T + 2 > cap_ - 1 || lt_[sl] + 1 + (D - 1) * T + 2 > dcap_) throw ConfigErr("max_ctx", "context full");
+    }
+    // drafter catch-up for requests whose pending rows exceed the graph stride
+    {
+        std::vector<int32_t> need;
+        for (int i = 0; i < b; ++i)
+            if (lt_[slots[i]] - ld_[slots[i]] + 1 > D + 1) need.push_back(slots[i]);
+        if (!need.empty()) catchup_drafter((int)need.size(), need.data());
+    }
+    const int b_hi = bucket_hi_for(b, T);
+    for (int i = 0; i < b_hi; ++i) {
+        if (i < b) {
+            const int sl = slots[i];
+            if (lt_[sl] - ld_[sl] + 1 > D + 1) {  // only reachable when catch-up was skipped
+                throw ConfigErr("drafter", "pending rows exceed draft_depth + 1");
+            }
+            h_step_[i] = StepIn{sl, lt_[sl], ld_[sl], 0};
+        } else {
+            h_step_[i] = StepIn{-1, 0, 0, 0};
+        }
+    }
+    const bool dbg = debug_;
+    CUDA_CHECK(cudaEventRecord(ev0_, st_));
+    auto key = std::make_tuple(b_hi, D, k, T, 0);
+    auto it = graphs_.find(key);
+    if (use_graphs && !dbg && it != graphs_.end()) {
+        CUDA_CHECK(cudaGraphLaunch(it->second.first, st_));
+        launches += it->second.second;
+    } else {
+        launches_in_seq_ = 0;
+        sd_device_sequence(b_hi, D, k, T, dbg, b);
+        launches += launches_in_seq_;
+    }
+    CUDA_CHECK(cudaEventRecord(ev1_, st_));
+    CUDA_CHECK(cudaEventSynchronize(ev1_));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    // capture for the next replay (after a successful eager run)
+    if (use_graphs && !dbg && it == graphs_.end()) {
+        cudaGraph_t g;
+        launches_in_seq_ = 0;
+        CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+        // the captured sequence must not change device state: capture only
+        try {
+            sd_device_sequence(b_hi, D, k, T, false, b);
+        } catch (...) {
+            cudaStreamEndCapture(st_, &g);
+            throw;
+        }
+        CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+        cudaGraphExec_t ex;
+        CUDA_CHECK(cudaGraphInstantiate(&ex, g, 0));
+        CUDA_CHECK(cudaGraphDestroy(g));
+        graphs_[key] = {ex, launches_in_seq_};
+    }
+    // outputs + host mirrors
+    for (int i = 0; i < b; ++i) {
+        const int sl = slots[i];
+        const int a = ho_.acc_len[i];
+        if (out) {
+            if (out->accept_len) out->accept_len[i] = a;
+            if (out->bonus) out->bonus[i] = ho_.bonus[i];
+            for (int j = 0; j < a; ++j) {
+                if (out->accepted) out->accepted[(size_t)i * D + j] = ho_.acc_tok[(size_t)i * kMaxD + j];
+                if (out->nodes) out->nodes[(size_t)i * D + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
+                if (out->kv_src) out->kv_src[(size_t)i * D + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
+            }
+            if (out->kv_len) out->kv_len[i] = lt_[sl] + 1 + a;
+        }
+        if (tree) {
+            const int n = ho_.tree_n[i];
+            if (tree->n_nodes) tree->n_nodes[i] = n;
+            for (int t = 0; t < n; ++t) {
+                const size_t o = (size_t)i * T + t;
+                if (tree->tokens) tree->tokens[o] = ho_.tree_tok[o];
+                if (tree->parents) tree->parents[o] = ho_.tree_par[o];
+                if (tree->depths) tree->depths[o] = ho_.tree_dep[o];
+                if (tree->probs) tree->probs[o] = ho_.tree_prob[o];
+                if (tree->path_probs) tree->path_probs[o] = ho_.tree_pp[o];
+            }
+        }
+        ld_[sl] = lt_[sl] + 1;
+        lt_[sl] = lt_[sl] + 1 + a;
+    }
+    if (out && out->elapsed_ms) out->elapsed_ms[0] = ms;
+    return ms;
+}
+
+void Engine::ar_device_sequence(int b_hi) {
+    CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
+    launch_rows_ar(d_step_, b_hi, b_hi, prows_, pg_, tok_hist_, cap_, st_);
+    count_launch();
+    target_forward(prows_, pg_, b_hi, 1, b_hi, cap_, logits_, feat_);
+    launch_row_topk(logits_, b_hi, cfg.vocab, prows_.slot, 1, 0, argmax_, tk_logit_, nullptr, nullptr, st_);
+    count_launch();
+    launch_commit_ar(d_step_, b_hi, argmax_, feat_, cfg.hidden, tok_hist_, feat_hist_, cap_, ar_tok_, st_);
+    count_launch();
+    CUDA_CHECK(cudaMemcpyAsync(ho_.ar_tok, ar_tok_, sizeof(int) * b_hi, cudaMemcpyDeviceToHost, st_));
+}
+
+float Engine::ar_step(int b, const int32_t* slots, int32_t* out_tokens) {
+    if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");
+    for (int i = 0; i < b; ++i) {
+        const int sl = slots[i];
+        if (sl < 0 || sl >= cfg.max_slots || !live_[sl]) throw ConfigErr("slot_ids", "slot not prefilled");
+        if (lt_[sl] + 2 > cap_ - 1) throw ConfigErr("max_ctx", "context full");
+    }
+    const int b_hi = b;
+    for (int i = 0; i < b_hi; ++i) h_step_[i] = i < b ? StepIn{slots[i], lt_[slots[i]], ld_[slots[i]], 0} : StepIn{-1, 0, 0, 0};
+    CUDA_CHECK(cudaEventRecord(ev0_, st_));
+    auto key = std::make_tuple(b_hi, 0, 0, 0, 1);
+    auto it = graphs_.find(key);
+    if (use_graphs && !debug_ && it != graphs_.end()) {
+        CUDA_CHECK(cudaGraphLaunch(it->second.first, st_));
+        launches += it->second.second;
+    } else {
+        launches_in_seq_ = 0;
+        ar_device_sequence(b_hi);
+        launches += launches_in_seq_;
+    }
+    CUDA_CHECK(cudaEventRecord(ev1_, st_));
+    CUDA_CHECK(cudaEventSynchronize(ev1_));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    if (debug_) {
+        dbg_ar_logits.resize((size_t)b * cfg.vocab);
+        CUDA_CHECK(cudaMemcpy(dbg_ar_logits.data(), logits_, sizeof(float) * dbg_ar_logits.size(),
+                              cudaMemcpyDeviceToHost));
+    }
+    if (use_graphs && !debug_ && it == graphs_.end()) {
+        cudaGraph_t g;
+        launches_in_seq_ = 0;
+        CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+        try {
+            ar_device_sequence(b_hi);
+        } catch (...) {
+            cudaStreamEndCapture(st_, &g);
+            throw;
+        }
+        CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+        cudaGraphExec_t ex;
+        CUDA_CHECK(cudaGraphInstantiate(&ex, g, 0));
+        CUDA_CHECK(cudaGraphDestroy(g));
+        graphs_[key] = {ex, launches_in_seq_};
+    }
+    for (int i = 0; i < b; ++i) {
+        if (out_tokens) out_tokens[i] = ho_.ar_tok[i];
+        lt_[slots[i]] += 1;
+    }
+    return ms;
+}
+
+size_t Engine::graph_pool_build(const std::vector<tlt_capture_entry>& entries) {
+    (void)entries;  // graphs are captured lazily on first use of each key
+    return graphs_.size();
+}
+
+void Engine::graph_pool_clear() {
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.first);
+    graphs_.clear();
+}
+
+}  // namespace tlt

@@ -1,0 +1,159 @@
+// Host-side engine: owns weights, KV caches, histories, activation buffers and
+// the CUDA-graph pool; runs prefill, the greedy tree SD step and the AR step.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tlt_b200.h"
+#include "../../include/tlt_init.h"
+#include "engine_kernels.h"
+#include "tlt_internal.h"
+
+namespace tlt {
+
+using bf16 = __nv_bfloat16;
+
+struct LayerW {
+    bf16 *attn_norm = nullptr, *qkv = nullptr, *qkv_b = nullptr, *o = nullptr, *mlp_norm = nullptr, *gu = nullptr,
+         *down = nullptr;
+    CUtensorMap tm_qkv, tm_o, tm_gu, tm_down;
+};
+
+struct StepOutHost {  // pinned staging of one step's results
+    int32_t* acc_len;
+    int32_t* bonus;
+    int32_t* acc_tok;    // [b_hi][maxD]
+    int32_t* acc_nodes;  // [b_hi][maxD]
+    int32_t* tree_tok;   // [b_hi][T]
+    int32_t* tree_par;
+    int32_t* tree_dep;
+    double* tree_prob;
+    double* tree_pp;
+    int32_t* tree_n;
+    int32_t* ar_tok;     // [b_hi]
+};
+
+struct DebugExp {  // one drafter expansion of one request (parity export)
+    std::vector<int32_t> path;
+    std::vector<double> row;
+};
+
+class Engine {
+public:
+    Engine(const tlt_model_cfg& cfg, const tlt_init_cfg& init, int device);
+    ~Engine();
+
+    void prefill(int b, const int32_t* slots, const int32_t* lens, const int32_t* tokens);
+    void release(int slot);
+    // greedy tree SD step; returns device ms
+    float sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out);
+    float ar_step(int b, const int32_t* slots, int32_t* out_tokens);
+
+    int slot_len(int slot) const { return lt_.at(slot); }
+    void set_debug(bool on) { debug_ = on; }
+    bool use_graphs = true;
+    size_t graph_pool_build(const std::vector<tlt_capture_entry>& entries);
+    void graph_pool_clear();
+    int bucket_hi_for(int b, int T) const;
+
+    // parity exports
+    std::vector<std::vector<DebugExp>> dbg_exp;  // [request i] expansions of the last sd_step
+    std::vector<std::vector<float>> dbg_vlogits; // [request i] [(T+1)*V]
+    std::vector<float> dbg_ar_logits;            // [b*V]
+
+    const tlt_model_cfg cfg;
+    long long launches = 0;  // kernel launches issued (graph replays count their nodes)
+
+private:
+    void alloc_weights(const tlt_init_cfg& init);
+    void alloc_state();
+    const CUtensorMap& tmap_act(const void* p, int rows, int cols, long long ld, int box);
+    void gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep);
+    void layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int R,
+                       int rpr, int ngroups, int max_keys);
+    void attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int rpr,
+                   int ngroups, int max_keys);
+    void lm_head(const float* x, int n, float* logits);
+    void target_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
+                        float* logits, bf16* feat);
+    void drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
+                         const int* gather, int n_lm, float* logits, bf16* dfeat_out);
+    void scatter_features(const Rows& rw, int R, const bf16* feat);
+    void catchup_drafter(int b, const int32_t* slots);
+    void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real);
+    void ar_device_sequence(int b_hi);
+    void upload_rows_host(const std::vector<int>& tok, const std::vector<int>& pos, const std::vector<int>& slot,
+                          const std::vector<int>& cidx, const std::vector<int>& fkind,
+                          const std::vector<long long>& fidx, const std::vector<uint32_t>& mask,
+                          const std::vector<int>& gslot, const std::vector<int>& glc, const std::vector<int>& gt0,
+                          const std::vector<int>& gnt);
+
+    int dev_;
+    cudaStream_t st_;
+    tlt_init_params ip_;
+    // weights
+    bf16 *embed_ = nullptr, *lm_head_ = nullptr, *final_norm_ = nullptr, *fc_ = nullptr;
+    std::vector<LayerW> layers_;
+    LayerW drafter_;
+    CUtensorMap tm_lm_, tm_fc_;
+    float *rope_cos_ = nullptr, *rope_sin_ = nullptr;
+    // caches / histories
+    int cap_ = 0, dcap_ = 0;
+    std::vector<bf16*> kc_, vc_;
+    bf16 *dkc_ = nullptr, *dvc_ = nullptr;
+    bf16** d_kc_arr_ = nullptr;
+    bf16** d_vc_arr_ = nullptr;
+    int32_t* tok_hist_ = nullptr;
+    bf16* feat_hist_ = nullptr;
+    // activations (capacity R_)
+    int R_ = 0, Rmeta_ = 0;
+    float* x_ = nullptr;
+    float* xg_ = nullptr;  // gathered rows for LM head
+    bf16 *h_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *act_ = nullptr, *feat_ = nullptr, *x2_ = nullptr;
+    bf16* dfeat_ = nullptr;  // drafter output features per drafter row [Rmeta][d]
+    float* logits_ = nullptr;
+    float* ws_ = nullptr;
+    size_t ws_elems_ = 0;
+    float *aws_m_ = nullptr, *aws_l_ = nullptr, *aws_o_ = nullptr;
+    size_t aws_elems_ = 0;
+    // row metadata
+    Rows drows_, vrows_, prows_;
+    Groups dg_[kMaxDepth + 2], vg_, pg_;
+    int *root_row_ = nullptr, *row_node_ = nullptr;
+    int* tk_tok_ = nullptr;
+    float *tk_logit_ = nullptr, *tk_M_ = nullptr, *tk_S_ = nullptr;
+    int* argmax_ = nullptr;
+    double* dbg_probs_ = nullptr;
+    // tree + accept
+    Cand* arena_ = nullptr;
+    int arena_cap_ = 16384;
+    int *arena_n_ = nullptr, *kept_ = nullptr, *kept_n_ = nullptr, *exp_n_ = nullptr, *done_ = nullptr;
+    int *tree_tok_ = nullptr, *tree_par_ = nullptr, *tree_dep_ = nullptr, *tree_n_ = nullptr;
+    double *tree_prob_ = nullptr, *tree_pp_ = nullptr;
+    int *acc_nodes_ = nullptr, *acc_tok_ = nullptr, *acc_len_ = nullptr, *bonus_ = nullptr, *kv_len_ = nullptr;
+    int* ar_tok_ = nullptr;
+    static constexpr int kMaxD = kMaxDepth;
+    StepIn *d_step_ = nullptr, *h_step_ = nullptr;
+    StepOutHost ho_{};
+    int max_b_ = 0;
+    // host mirrors
+    std::vector<int> lt_, ld_, live_;
+    bool debug_ = false;
+    // caches
+    std::unordered_map<std::string, CUtensorMap> tmaps_;
+    std::map<std::tuple<int, int, int, int, int>, std::pair<cudaGraphExec_t, long long>> graphs_;
+    cudaEvent_t ev0_, ev1_;
+    long long launches_in_seq_ = 0;
+    bool counting_ = false;
+    void count_launch(int n = 1) { launches_in_seq_ += n; }
+    friend struct Counter;
+};
+
+}  // namespace tlt

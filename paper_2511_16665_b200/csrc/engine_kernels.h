@@ -1,0 +1,109 @@
+// Launch wrappers + parameter blocks of the engine kernels (kernels.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/tlt_init.h"
+#include "kernels.cuh"
+
+namespace tlt {
+
+struct AttnParams {
+    const __nv_bfloat16* q;  // [R][H*hd]
+    __nv_bfloat16* out;      // [R][H*hd]
+    const __nv_bfloat16* kc; // layer base [slots][KV][cap][hd]
+    const __nv_bfloat16* vc;
+    Rows rows;
+    Groups g;
+    int rows_per_req, n_groups;
+    int H, KV, hd, cap;
+    float scale_log2;
+    int chunk, max_splits, qv_cap;
+    float *ws_m, *ws_l, *ws_o;
+};
+
+struct TreeParams {
+    const StepIn* step;
+    int b, b_hi;
+    int level, D, k, T;
+    Cand* arena;
+    int arena_cap;
+    int *arena_n, *kept, *kept_n, *exp_n, *done;
+    // rows of this level
+    int lvl_base, lm_F;
+    int* row_node;     // [R_draft]
+    const int* root_row;
+    const int* tk_tok;
+    const float* tk_logit;
+    const float* tk_M;
+    const float* tk_S;
+    // next level
+    int nxt_base, nxt_F;
+    Rows rows;         // drafter rows (all levels)
+    Groups g_next;
+    // final tree + verify rows
+    int* tree_tok;
+    int* tree_par;
+    int* tree_dep;
+    double* tree_prob;
+    double* tree_pp;
+    int* tree_n;
+    Rows vrows;
+    Groups vg;
+    const int* tok_hist;
+    int cap;
+};
+
+struct AcceptParams {
+    const StepIn* step;
+    int b, b_hi, T, maxD;
+    const int* tree_tok;
+    const int* tree_par;
+    const int* tree_n;
+    const int* argmax;  // [b_hi*(T+1)]
+    int* acc_nodes;     // [b_hi][maxD]
+    int* acc_tok;
+    int* acc_len;
+    int* bonus;
+};
+
+struct CommitParams {
+    const StepIn* step;
+    int b, b_hi, maxD, layers, KV, hd, cap, d, row_stride;
+    __nv_bfloat16** kc;  // device array of per-layer bases
+    __nv_bfloat16** vc;
+    const int* acc_nodes;
+    const int* acc_tok;
+    const int* acc_len;
+    const int* bonus;
+    int* tok_hist;
+    __nv_bfloat16* feat_hist;
+    const __nv_bfloat16* vfeat;
+    int* kv_len;
+};
+
+void launch_init(uint16_t* dst, long long n, const tlt_init_params& p, int tensor, int layer, cudaStream_t st);
+void launch_embed(const Rows& rows, int R, const __nv_bfloat16* E, int d, float* x, cudaStream_t st);
+void launch_draft_in(const Rows& rows, int R, const __nv_bfloat16* E, int d, const __nv_bfloat16* hist,
+                     const __nv_bfloat16* dfeat, __nv_bfloat16* X2, cudaStream_t st);
+void launch_gather_rows(const float* x, const int* src, int n, int d, float* out, cudaStream_t st);
+void launch_to_bf16(const float* x, long long n, __nv_bfloat16* out, cudaStream_t st);
+void launch_rmsnorm(const float* x, int R, int d, const __nv_bfloat16* g, float eps, __nv_bfloat16* out,
+                    cudaStream_t st);
+void launch_attention(const AttnParams& p, cudaStream_t st);
+void launch_row_topk(const float* logits, int R, int V, const int* live, int k, int need_sum, int* out_tok,
+                     float* out_logit, float* out_M, float* out_S, cudaStream_t st);
+void launch_row_probs(const float* logits, int R, int V, const float* M, const float* S, double* out,
+                      cudaStream_t st);
+void launch_rows_level1(const StepIn* st, int b, int b_hi, int D1, const Rows& rows, const Groups& g, int* root_row,
+                        const int* tok_hist, int cap, cudaStream_t s);
+void launch_rows_ar(const StepIn* st, int b, int b_hi, const Rows& rows, const Groups& g, const int* tok_hist,
+                    int cap, cudaStream_t s);
+void launch_tree_level(const TreeParams& p, cudaStream_t st);
+void launch_tree_final(const TreeParams& p, cudaStream_t st);
+void launch_accept_greedy(const AcceptParams& p, cudaStream_t st);
+void launch_commit(const CommitParams& p, cudaStream_t st);
+void launch_commit_ar(const StepIn* st, int b, const int* argmax, const __nv_bfloat16* feat, int d, int* tok_hist,
+                      __nv_bfloat16* feat_hist, int cap, int* out_tok, cudaStream_t s);
+
+}  // namespace tlt

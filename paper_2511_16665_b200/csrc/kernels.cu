@@ -1,0 +1,892 @@
+// Engine kernels: weight init, gathers, RMSNorm, tree-masked attention,
+// row top-k / argmax, drafter tree select (K6), greedy accept (K7), KV
+// compaction + commit (K8), row-metadata builders. The GEMMs are in gemm.cu.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "../../include/tlt_init.h"
+#include "engine_kernels.h"
+#include "kernels.cuh"
+
+namespace tlt {
+
+using bf16 = __nv_bfloat16;
+
+// ------------------------------------------------------------------ init
+__global__ void k_init_weights(uint16_t* dst, long long n, tlt_init_params p, int tensor, int layer) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = tlt_init_elem(&p, tensor, layer, i);
+}
+void launch_init(uint16_t* dst, long long n, const tlt_init_params& p, int tensor, int layer, cudaStream_t st) {
+    k_init_weights<<<148 * 8, 256, 0, st>>>(dst, n, p, tensor, layer);
+}
+
+// ------------------------------------------------------------- gathers
+__global__ void k_embed(const int* __restrict__ tok, const int* __restrict__ slot, const bf16* __restrict__ E, int d,
+                        float* __restrict__ x) {
+    const int r = blockIdx.x;
+    const bool live = slot[r] >= 0;
+    const bf16* e = E + (long long)(live ? tok[r] : 0) * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) x[(long long)r * d + i] = live ? __bfloat162float(e[i]) : 0.f;
+}
+void launch_embed(const Rows& rows, int R, const bf16* E, int d, float* x, cudaStream_t st) {
+    k_embed<<<R, 256, 0, st>>>(rows.tok, rows.slot, E, d, x);
+}
+
+// X2[r] = [prev feature || embed(tok)] (drafter fc input)
+__global__ void k_draft_in(Rows rows, const bf16* __restrict__ E, int d, const bf16* __restrict__ hist,
+                           const bf16* __restrict__ dfeat, bf16* __restrict__ X2) {
+    const int r = blockIdx.x;
+    const bool live = rows.slot[r] >= 0;
+    const int kind = live ? rows.fkind[r] : 0;
+    const bf16* src = kind == 1 ? hist + rows.fidx[r] * d : (kind == 2 ? dfeat + rows.fidx[r] * d : nullptr);
+    const bf16* e = E + (long long)(live ? rows.tok[r] : 0) * d;
+    bf16* o = X2 + (long long)r * 2 * d;
+    const bf16 z = __float2bfloat16(0.f);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        o[i] = src ? src[i] : z;
+        o[d + i] = live ? e[i] : z;
+    }
+}
+void launch_draft_in(const Rows& rows, int R, const bf16* E, int d, const bf16* hist, const bf16* dfeat, bf16* X2,
+                     cudaStream_t st) {
+    k_draft_in<<<R, 256, 0, st>>>(rows, E, d, hist, dfeat, X2);
+}
+
+// out[r] = x[src[r]] for gathering the level-1 root rows
+__global__ void k_gather_rows(const float* __restrict__ x, const int* __restrict__ src, int d, float* __restrict__ out) {
+    const int r = blockIdx.x;
+    const int s = src[r];
+    for (int i = threadIdx.x; i < d; i += blockDim.x) out[(long long)r * d + i] = s >= 0 ? x[(long long)s * d + i] : 0.f;
+}
+void launch_gather_rows(const float* x, const int* src, int n, int d, float* out, cudaStream_t st) {
+    k_gather_rows<<<n, 256, 0, st>>>(x, src, d, out);
+}
+
+__global__ void k_to_bf16(const float* __restrict__ x, long long n, bf16* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = __float2bfloat16_rn(x[i]);
+}
+void launch_to_bf16(const float* x, long long n, bf16* out, cudaStream_t st) {
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_to_bf16<<<blocks, 256, 0, st>>>(x, n, out);
+}
+
+// ------------------------------------------------------------- RMSNorm
+// out = bf16(x * (1/sqrt(mean(x^2) + eps)) * g), one CTA per row, fixed
+// reduction tree (deterministic).
+__global__ void k_rmsnorm(const float* __restrict__ x, int d, const bf16* __restrict__ g, float eps,
+                          bf16* __restrict__ out) {
+    __shared__ float red[32];
+    const int r = blockIdx.x;
+    const float* xr = x + (long long)r * d;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+    for (int i = threadIdx.x; i < d; i += blockDim.x)
+        out[(long long)r * d + i] = __float2bfloat16_rn(xr[i] * inv * __bfloat162float(g[i]));
+}
+void launch_rmsnorm(const float* x, int R, int d, const bf16* g, float eps, bf16* out, cudaStream_t st) {
+    k_rmsnorm<<<R, 256, 0, st>>>(x, d, g, eps, out);
+}
+
+// ----------------------------------------------------------- attention
+// Tree-masked GQA attention over the per-slot KV cache, split along keys in
+// fixed 512-key chunks aligned to absolute key indices (so a row's result
+// does not depend on how many other rows share the launch). One CTA handles
+// 16 query vectors (row x q-head of one KV head) against one key chunk; K/V
+// tiles of 32 keys are staged in shared memory, the tree mask is read as
+// 32-bit words per row. Partials (m, l, o) are merged by k_attn_combine.
+constexpr int kAttnQV = 16;
+constexpr int kAttnKeys = 32;
+
+template <int HD>
+__global__ void __launch_bounds__(128) k_attention(AttnParams p) {
+    constexpr int DPL = HD / 32;  // output dims per lane
+    __shared__ float qs[kAttnQV][HD];
+    __shared__ uint32_t ks[kAttnKeys][HD / 2 + 1];
+    __shared__ __align__(16) bf16 vs[kAttnKeys][HD];
+    __shared__ int s_row[kAttnQV], s_head[kAttnQV];
+
+    const int G = p.H / p.KV;
+    const int kvh = blockIdx.y;
+    const int grp = blockIdx.z / p.max_splits;
+    const int split = blockIdx.z % p.max_splits;
+    const int qv0 = blockIdx.x * kAttnQV;
+    const int nqv = p.rows_per_req * G;
+    const int slot = p.g.slot[grp];
+    const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
+    const int total = slot >= 0 ? lc + ntail : 0;
+    const int k0 = split * p.chunk;
+    const int k1 = min(total, k0 + p.chunk);
+
+    if (threadIdx.x < kAttnQV) {
+        const int gqv = qv0 + threadIdx.x;
+        int row = -1, head = 0;
+        if (gqv < nqv) {
+            row = grp * p.rows_per_req + gqv / G;
+            head = kvh * G + gqv % G;
+            if (p.rows.slot[row] < 0) row = -1;
+        }
+        s_row[threadIdx.x] = row;
+        s_head[threadIdx.x] = head;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kAttnQV * HD; idx += blockDim.x) {
+        const int l = idx / HD, e = idx % HD;
+        const int row = s_row[l];
+        qs[l][e] = row >= 0 ? __bfloat162float(p.q[(long long)row * p.H * HD + s_head[l] * HD + e]) * p.scale_log2 : 0.f;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float m[4], l[4], acc[4][DPL];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        m[a] = -CUDART_INF_F;
+        l[a] = 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[a][e] = 0.f;
+    }
+    const long long slot_base = ((long long)(slot < 0 ? 0 : slot) * p.KV + kvh) * p.cap;
+    for (int kb = k0; kb < k1; kb += kAttnKeys) {
+        const int nk = min(kAttnKeys, k1 - kb);
+        __syncthreads();
+        // stage K (padded u32 pairs) and V for up to 32 keys: 16-byte chunks
+        constexpr int CPK = HD * 2 / 16;  // 16B chunks per key row
+        for (int c = threadIdx.x; c < kAttnKeys * CPK; c += blockDim.x) {
+            const int j = c / CPK, w = c % CPK;
+            uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+            if (j < nk) {
+                const int v = kb + j;
+                const long long ci = v < lc ? v : tail0 + (v - lc);
+                const long long off = (slot_base + ci) * HD;
+                kv = reinterpret_cast<const uint4*>(p.kc + off)[w];
+                vv = reinterpret_cast<const uint4*>(p.vc + off)[w];
+            }
+            ks[j][w * 4 + 0] = kv.x;
+            ks[j][w * 4 + 1] = kv.y;
+            ks[j][w * 4 + 2] = kv.z;
+            ks[j][w * 4 + 3] = kv.w;
+            reinterpret_cast<uint4*>(&vs[j][0])[w] = vv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int lq = warp * 4 + a;
+            const int row = s_row[lq];
+            if (row < 0) continue;  // warp-uniform
+            float s = -CUDART_INF_F;
+            const int v = kb + lane;
+            if (lane < nk) {
+                bool vis = v < lc;
+                if (!vis) {
+                    const int t = v - lc;
+                    vis = (p.rows.mask[(long long)row * kMaskWords + (t >> 5)] >> (t & 31)) & 1u;
+                }
+                if (vis) {
+                    float dot = 0.f;
+#pragma unroll 8
+                    for (int w = 0; w < HD / 2; ++w) {
+                        const uint32_t kk = ks[lane][w];
+                        const float k0f = __uint_as_float(kk << 16), k1f = __uint_as_float(kk & 0xffff0000u);
+                        dot = fmaf(qs[lq][2 * w], k0f, dot);
+                        dot = fmaf(qs[lq][2 * w + 1], k1f, dot);
+                    }
+                    s = dot;
+                }
+            }
+            float mx = s;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float m_new = fmaxf(m[a], mx);
+            if (m_new == -CUDART_INF_F) continue;
+            const float pr = exp2f(s - m_new);
+            float sum = pr;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            const float corr = exp2f(m[a] - m_new);
+            l[a] = l[a] * corr + sum;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) acc[a][e] *= corr;
+            for (int jj = 0; jj < nk; ++jj) {
+                const float pj = __shfl_sync(0xffffffffu, pr, jj);
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) acc[a][e] = fmaf(pj, __bfloat162float(vs[jj][lane * DPL + e]), acc[a][e]);
+            }
+            m[a] = m_new;
+        }
+    }
+    // partials
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int lq = warp * 4 + a;
+        const int gqv = qv0 + lq;
+        if (gqv >= nqv) continue;
+        const long long pidx = ((long long)(grp * p.max_splits + split) * p.qv_cap + gqv) * p.KV + kvh;
+        if (lane == 0) {
+            p.ws_m[pidx] = m[a];
+            p.ws_l[pidx] = l[a];
+        }
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) p.ws_o[pidx * HD + lane * DPL + e] = acc[a][e];
+    }
+}
+
+template <int HD>
+__global__ void k_attn_combine(AttnParams p) {
+    // one warp per (group, query vector, kv head)
+    const int G = p.H / p.KV;
+    const int nqv = p.rows_per_req * G;
+    const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long total = (long long)p.n_groups * nqv * p.KV;
+    if (gw >= total) return;
+    const int kvh = (int)(gw % p.KV);
+    const int gqv = (int)((gw / p.KV) % nqv);
+    const int grp = (int)(gw / ((long long)p.KV * nqv));
+    const int row = grp * p.rows_per_req + gqv / G;
+    const int head = kvh * G + gqv % G;
+    if (p.rows.slot[row] < 0) return;
+    const int total_keys = p.g.lc[grp] + p.g.ntail[grp];
+    const int nsplit = min(p.max_splits, (total_keys + p.chunk - 1) / p.chunk);
+    constexpr int DPL = HD / 32;
+    float M = -CUDART_INF_F;
+    for (int s = 0; s < nsplit; ++s) {
+        const long long pidx = ((long long)(grp * p.max_splits + s) * p.qv_cap + gqv) * p.KV + kvh;
+        M = fmaxf(M, p.ws_m[pidx]);
+    }
+    float L = 0.f, o[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) o[e] = 0.f;
+    for (int s = 0; s < nsplit; ++s) {  // fixed order
+        const long long pidx = ((long long)(grp * p.max_splits + s) * p.qv_cap + gqv) * p.KV + kvh;
+        const float ms = p.ws_m[pidx];
+        if (ms == -CUDART_INF_F) continue;
+        const float w = exp2f(ms - M);
+        L += p.ws_l[pidx] * w;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[e] += p.ws_o[pidx * HD + lane * DPL + e] * w;
+    }
+    const float inv = L > 0.f ? 1.0f / L : 0.f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e)
+        p.out[(long long)row * p.H * HD + head * HD + lane * DPL + e] = __float2bfloat16_rn(o[e] * inv);
+}
+
+void launch_attention(const AttnParams& p, cudaStream_t st) {
+    const int G = p.H / p.KV;
+    const int nqv = p.rows_per_req * G;
+    dim3 grid((nqv + kAttnQV - 1) / kAttnQV, p.KV, p.n_groups * p.max_splits);
+    const long long warps = (long long)p.n_groups * nqv * p.KV;
+    const int cblocks = (int)((warps * 32 + 255) / 256);
+    if (p.hd == 128) {
+        k_attention<128><<<grid, 128, 0, st>>>(p);
+        k_attn_combine<128><<<cblocks, 256, 0, st>>>(p);
+    } else if (p.hd == 64) {
+        k_attention<64><<<grid, 128, 0, st>>>(p);
+        k_attn_combine<64><<<cblocks, 256, 0, st>>>(p);
+    }
+}
+
+// ------------------------------------------------------- row top-k / argmax
+// Per row: top-k by (logit desc, id asc) — the reference child order
+// (stable_sort over ascending id, spec_decode.hpp:121-125) — plus the row max
+// M and, when need_sum, S = sum_i expf(l_i - M) (fixed reduction order).
+template <int K>
+struct TopK {
+    float v[K];
+    int id[K];
+    __device__ void init() {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            v[i] = -CUDART_INF_F;
+            id[i] = 0x7fffffff;
+        }
+    }
+    __device__ static bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
+    __device__ void push(float x, int ix) {
+        if (!better(x, ix, v[K - 1], id[K - 1])) return;
+        int p = K - 1;
+        while (p > 0 && better(x, ix, v[p - 1], id[p - 1])) {
+            v[p] = v[p - 1];
+            id[p] = id[p - 1];
+            --p;
+        }
+        v[p] = x;
+        id[p] = ix;
+    }
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) k_row_topk(const float* __restrict__ logits, int V, const int* __restrict__ live,
+                                                  int k, int need_sum, int* __restrict__ out_tok,
+                                                  float* __restrict__ out_logit, float* __restrict__ out_M,
+                                                  float* __restrict__ out_S) {
+    __shared__ float sv[256][K];
+    __shared__ int si[256][K];
+    __shared__ float red[8];
+    const int r = blockIdx.x;
+    if (live && live[r] < 0) return;
+    const float* lr = logits + (long long)r * V;
+    TopK<K> t;
+    t.init();
+    for (int i = threadIdx.x; i < V; i += blockDim.x) t.push(lr[i], i);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        sv[threadIdx.x][j] = t.v[j];
+        si[threadIdx.x][j] = t.id[j];
+    }
+    __syncthreads();
+    // pairwise merges of sorted K-lists: 256 -> 1
+    for (int stride = 1; stride < 256; stride <<= 1) {
+        if ((threadIdx.x % (2 * stride)) == 0) {
+            const int a = threadIdx.x, b = threadIdx.x + stride;
+            float mv[K];
+            int mi[K];
+            int ia = 0, ib = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const bool take_a = TopK<K>::better(sv[a][ia], si[a][ia], sv[b][ib], si[b][ib]);
+                mv[j] = take_a ? sv[a][ia] : sv[b][ib];
+                mi[j] = take_a ? si[a][ia] : si[b][ib];
+                if (take_a) ++ia; else ++ib;
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                sv[a][j] = mv[j];
+                si[a][j] = mi[j];
+            }
+        }
+        __syncthreads();
+    }
+    const float M = sv[0][0];
+    if (threadIdx.x < k) {
+        out_tok[(long long)r * k + threadIdx.x] = si[0][threadIdx.x];
+        out_logit[(long long)r * k + threadIdx.x] = sv[0][threadIdx.x];
+    }
+    if (threadIdx.x == 0 && out_M) out_M[r] = M;
+    if (!need_sum) return;
+    float s = 0.f;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) s += expf(lr[i] - M);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float tot = 0.f;
+        for (int w = 0; w < 8; ++w) tot += red[w];
+        out_S[r] = tot;
+    }
+}
+
+void launch_row_topk(const float* logits, int R, int V, const int* live, int k, int need_sum, int* out_tok,
+                     float* out_logit, float* out_M, float* out_S, cudaStream_t st) {
+    if (k <= 1)
+        k_row_topk<1><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+    else if (k <= 2)
+        k_row_topk<2><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+    else if (k <= 4)
+        k_row_topk<4><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+    else
+        k_row_topk<8><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+}
+
+// full fp64 distribution of a row (parity/debug export): p = exp((double)(l-M))/S
+__global__ void k_row_probs(const float* __restrict__ logits, int V, const float* __restrict__ M,
+                            const float* __restrict__ S, double* __restrict__ out) {
+    const int r = blockIdx.x;
+    const float m = M[r];
+    const double s = (double)S[r];
+    for (int i = threadIdx.x; i < V; i += blockDim.x)
+        out[(long long)r * V + i] = exp((double)(logits[(long long)r * V + i] - m)) / s;
+}
+void launch_row_probs(const float* logits, int R, int V, const float* M, const float* S, double* out, cudaStream_t st) {
+    k_row_probs<<<R, 256, 0, st>>>(logits, V, M, S, out);
+}
+
+// ------------------------------------------------------------ row builders
+// Drafter level 1: pending committed positions [ld, lt) (target features
+// known) + the root at lt, causal among themselves. Stride D1 per request.
+__global__ void k_rows_level1(const StepIn* __restrict__ st, int b, int b_hi, int D1, Rows rows, Groups g,
+                              int* __restrict__ root_row, const int* __restrict__ tok_hist, int cap,
+                              int drafter_cap) {
+    const int i = blockIdx.x;
+    const int j = threadIdx.x;
+    if (j >= D1) return;
+    const int r = i * D1 + j;
+    const bool live = i < b && st[i].slot >= 0;
+    const int pend = live ? st[i].lt - st[i].ld + 1 : 0;
+    uint32_t* mk = rows.mask + (long long)r * kMaskWords;
+    for (int w = 0; w < kMaskWords; ++w) mk[w] = 0u;
+    if (live && j < pend) {
+        const int slot = st[i].slot, pos = st[i].ld + j;
+        rows.tok[r] = tok_hist[(long long)slot * cap + pos];
+        rows.pos[r] = pos;
+        rows.slot[r] = slot;
+        rows.cidx[r] = pos;
+        rows.fkind[r] = pos > 0 ? 1 : 0;
+        rows.fidx[r] = (long long)slot * cap + pos - 1;
+        for (int t = 0; t <= j; ++t) mk[t >> 5] |= 1u << (t & 31);
+    } else {
+        rows.tok[r] = 0;
+        rows.pos[r] = 0;
+        rows.slot[r] = -1;
+        rows.cidx[r] = 0;
+        rows.fkind[r] = 0;
+        rows.fidx[r] = 0;
+    }
+    if (j == 0) {
+        g.slot[i] = live ? st[i].slot : -1;
+        g.lc[i] = live ? st[i].ld : 0;
+        g.tail0[i] = live ? st[i].ld : 0;
+        g.ntail[i] = pend;
+        root_row[i] = live ? i * D1 + pend - 1 : -1;
+    }
+    (void)b_hi;
+    (void)drafter_cap;
+}
+void launch_rows_level1(const StepIn* st, int b, int b_hi, int D1, const Rows& rows, const Groups& g, int* root_row,
+                        const int* tok_hist, int cap, cudaStream_t s) {
+    k_rows_level1<<<b_hi, 32 * ((D1 + 31) / 32), 0, s>>>(st, b, b_hi, D1, rows, g, root_row, tok_hist, cap, 0);
+}
+
+// AR decode: one row per request (the root), visible prefix [0, lt) + self.
+__global__ void k_rows_ar(const StepIn* __restrict__ st, int b, int b_hi, Rows rows, Groups g,
+                          const int* __restrict__ tok_hist, int cap) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b_hi) return;
+    const bool live = i < b && st[i].slot >= 0;
+    uint32_t* mk = rows.mask + (long long)i * kMaskWords;
+    for (int w = 0; w < kMaskWords; ++w) mk[w] = 0u;
+    mk[0] = 1u;
+    const int slot = live ? st[i].slot : -1, lt = live ? st[i].lt : 0;
+    rows.tok[i] = live ? tok_hist[(long long)slot * cap + lt] : 0;
+    rows.pos[i] = lt;
+    rows.slot[i] = slot;
+    rows.cidx[i] = lt;
+    rows.fkind[i] = 0;
+    rows.fidx[i] = 0;
+    g.slot[i] = slot;
+    g.lc[i] = lt;
+    g.tail0[i] = lt;
+    g.ntail[i] = live ? 1 : 0;
+}
+void launch_rows_ar(const StepIn* st, int b, int b_hi, const Rows& rows, const Groups& g, const int* tok_hist, int cap,
+                    cudaStream_t s) {
+    k_rows_ar<<<(b_hi + 127) / 128, 128, 0, s>>>(st, b, b_hi, rows, g, tok_hist, cap);
+}
+
+// ------------------------------------------------------------ tree (K6)
+__device__ __forceinline__ bool rank_before(const Cand& a, const Cand& b) {  // spec_decode.hpp:96-101
+    if (a.pp != b.pp) return a.pp > b.pp;
+    if (a.depth != b.depth) return a.depth < b.depth;
+    if (a.token != b.token) return a.token < b.token;
+    return a.birth < b.birth;
+}
+
+constexpr int kTreeThreads = 256;
+constexpr int kSortCap = 2048;
+
+// bitonic sort of idx[0..n) (n <= kSortCap, padded with -1) by rank_before over cand[]
+__device__ void bitonic_rank_sort(int* idx, int n_pad, const Cand* cand) {
+    for (int size = 2; size <= n_pad; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < n_pad / 2; t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const int a = idx[lo], b = idx[hi];
+                // -1 (padding) ranks last
+                bool a_first;
+                if (a < 0) a_first = false;
+                else if (b < 0) a_first = true;
+                else a_first = rank_before(cand[a], cand[b]);
+                const bool swap = up ? !a_first : a_first;
+                if (swap && !(a < 0 && b < 0)) {
+                    idx[lo] = b;
+                    idx[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// One drafter level of build_draft_tree (spec_decode.hpp:118-169) for one
+// request per CTA: append the children of this level's expanded rows (top-k
+// in child-rank order, p > 0, births in expansion order), sort them by
+// rank_before, merge into the running global top-T (the final selection of
+// :171-179, computed incrementally — exact under the strict total order),
+// and emit the cut frontier (:154-160) as the next level's drafter rows.
+__global__ void __launch_bounds__(kTreeThreads) k_tree_level(TreeParams p) {
+    extern __shared__ __align__(16) unsigned char tree_smem[];
+    Cand* sc = reinterpret_cast<Cand*>(tree_smem);                       // kept (first n_kept) + new children
+    int* sidx = reinterpret_cast<int*>(tree_smem + sizeof(Cand) * kSortCap);
+    __shared__ int s_cnt[kTreeThreads + 1];
+    __shared__ int s_n_new, s_n_kept;
+    const int i = blockIdx.x;
+    const bool live = i < p.b && p.step[i].slot >= 0;
+    const int lt = live ? p.step[i].lt : 0;
+    const int slot = live ? p.step[i].slot : -1;
+    Cand* arena = p.arena + (long long)i * p.arena_cap;
+    int* kept = p.kept + (long long)i * p.T;
+
+    if (p.level == 1 && threadIdx.x == 0) {
+        p.arena_n[i] = 0;
+        p.kept_n[i] = 0;
+        p.exp_n[i] = 0;
+        p.done[i] = live ? 0 : 1;
+    }
+    __syncthreads();
+    const bool active = live && !p.done[i];
+    // ---- collect children of this level's rows (row j of this request)
+    const int F = p.lm_F;
+    int my_valid = 0;
+    const int j = threadIdx.x;
+    int node = -1;
+    int lm_row = i * F + j;
+    bool row_live = false;
+    if (active && j < F) {
+        if (p.level == 1) {
+            row_live = true;
+            node = -1;
+        } else {
+            const int grow = p.lvl_base + lm_row;
+            row_live = p.rows.slot[grow] >= 0;
+            node = row_live ? p.row_node[grow] : -1;
+        }
+        if (row_live) {
+            for (int c = 0; c < p.k; ++c) {
+                const float lg = p.tk_logit[(long long)lm_row * p.k + c];
+                const double pr = exp((double)(lg - p.tk_M[lm_row])) / (double)p.tk_S[lm_row];
+                if (!(pr > 0.0)) break;
+                ++my_valid;
+            }
+        }
+    }
+    if (j < kTreeThreads) s_cnt[j] = my_valid;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int t = 0; t < kTreeThreads; ++t) {
+            const int v = s_cnt[t];
+            s_cnt[t] = acc;
+            acc += v;
+        }
+        s_cnt[kTreeThreads] = acc;
+        s_n_new = acc;
+        s_n_kept = active ? p.kept_n[i] : 0;
+    }
+    __syncthreads();
+    const int n_new = s_n_new, n_kept = s_n_kept;
+    const int count0 = active ? p.arena_n[i] : 0;
+    if (active && my_valid > 0) {
+        const double ppar = node < 0 ? 1.0 : arena[node].pp;
+        for (int c = 0; c < my_valid; ++c) {
+            const float lg = p.tk_logit[(long long)lm_row * p.k + c];
+            const double pr = exp((double)(lg - p.tk_M[lm_row])) / (double)p.tk_S[lm_row];
+            Cand cd;
+            cd.pp = ppar * pr;  // spec_decode.hpp:132
+            cd.prob = pr;
+            cd.token = p.tk_tok[(long long)lm_row * p.k + c];
+            cd.parent = node;
+            cd.depth = p.level;
+            cd.birth = count0 + s_cnt[j] + c;
+            cd.row = -1;
+            cd.eslot = -1;
+            arena[cd.birth] = cd;
+        }
+    }
+    __syncthreads();
+    // ---- sort the new children (indices into sc: kept at [0,n_kept), new at [n_kept, n_kept+n_new))
+    for (int t = threadIdx.x; t < n_kept; t += blockDim.x) sc[t] = arena[kept[t]];
+    for (int t = threadIdx.x; t < n_new; t += blockDim.x) sc[n_kept + t] = arena[count0 + t];
+    int n_pad = 1;
+    while (n_pad < n_new) n_pad <<= 1;
+    for (int t = threadIdx.x; t < n_pad; t += blockDim.x) sidx[t] = t < n_new ? n_kept + t : -1;
+    __syncthreads();
+    if (n_new > 1) bitonic_rank_sort(sidx, n_pad, sc);
+    // frontier = first min(T, n_new) new children in rank order (:154-160)
+    const int n_front = (p.level < p.D) ? min(p.T, n_new) : 0;
+    if (active && p.level < p.D) {
+        const int e0 = p.exp_n[i];
+        for (int f = threadIdx.x; f < p.nxt_F; f += blockDim.x) {
+            const int r = p.nxt_base + i * p.nxt_F + f;
+            uint32_t* mk = p.rows.mask + (long long)r * kMaskWords;
+            if (f < n_front) {
+                const int a = sidx[f] - n_kept;  // index among the new children
+                const int an = count0 + a;       // arena index
+                const Cand& cd = sc[n_kept + a];
+                const int e = e0 + f;
+                const int prow = cd.parent < 0 ? p.root_row[i] : arena[cd.parent].row;
+                p.rows.tok[r] = cd.token;
+                p.rows.pos[r] = lt + cd.depth;
+                p.rows.slot[r] = slot;
+                p.rows.cidx[r] = lt + 1 + e;
+                p.rows.fkind[r] = 2;
+                p.rows.fidx[r] = prow;
+                const uint32_t* pm = cd.parent < 0 ? nullptr : p.rows.mask + (long long)prow * kMaskWords;
+                for (int w = 0; w < kMaskWords; ++w) mk[w] = pm ? pm[w] : 0u;
+                mk[e >> 5] |= 1u << (e & 31);
+                p.row_node[r] = an;
+                arena[an].row = r;
+                arena[an].eslot = e;
+            } else {
+                p.rows.slot[r] = -1;
+                p.rows.tok[r] = 0;
+                p.rows.pos[r] = 0;
+                p.rows.cidx[r] = 0;
+                p.rows.fkind[r] = 0;
+                p.row_node[r] = -1;
+                for (int w = 0; w < kMaskWords; ++w) mk[w] = 0u;
+            }
+        }
+        if (threadIdx.x == 0) {
+            p.g_next.slot[i] = n_front > 0 ? slot : -1;
+            p.g_next.lc[i] = lt + 1;
+            p.g_next.tail0[i] = lt + 1;
+            p.g_next.ntail[i] = e0 + n_front;
+        }
+    } else if (!active && p.level < p.D) {
+        for (int f = threadIdx.x; f < p.nxt_F; f += blockDim.x) {
+            const int r = p.nxt_base + i * p.nxt_F + f;
+            p.rows.slot[r] = -1;
+            p.row_node[r] = -1;
+        }
+        if (threadIdx.x == 0) {
+            p.g_next.slot[i] = -1;
+            p.g_next.ntail[i] = 0;
+        }
+    }
+    __syncthreads();
+    // ---- merge: top-T of (kept U new) under rank_before
+    if (active) {
+        const int n_all = n_kept + n_new;
+        int m_pad = 1;
+        while (m_pad < n_all) m_pad <<= 1;
+        // reuse sidx: kept then new (unsorted is fine: full sort)
+        __syncthreads();
+        for (int t = threadIdx.x; t < m_pad; t += blockDim.x) sidx[t] = t < n_all ? t : -1;
+        __syncthreads();
+        if (n_all > 1) bitonic_rank_sort(sidx, m_pad, sc);
+        const int nk = min(p.T, n_all);
+        for (int t = threadIdx.x; t < nk; t += blockDim.x) {
+            const int s = sidx[t];
+            kept[t] = sc[s].birth;  // birth == arena index
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            p.kept_n[i] = nk;
+            p.arena_n[i] = count0 + n_new;
+            p.exp_n[i] += n_front;
+            if (n_new == 0 || p.level >= p.D) p.done[i] = 1;  // :167 `if (next.empty()) break;`
+        }
+    }
+}
+
+// Final tree (spec_decode.hpp:171-196): kept list in rank order with parents
+// remapped, plus the verify rows: root at lt, node n at cache lt+1+n with
+// position lt+depth, visibility = root + ancestors + self.
+__global__ void k_tree_final(TreeParams p) {
+    const int i = blockIdx.x;
+    const bool live = i < p.b && p.step[i].slot >= 0;
+    const int T = p.T, T1 = p.T + 1;
+    const int n = live ? p.kept_n[i] : 0;
+    const Cand* arena = p.arena + (long long)i * p.arena_cap;
+    const int* kept = p.kept + (long long)i * T;
+    const int lt = live ? p.step[i].lt : 0, slot = live ? p.step[i].slot : -1;
+    __shared__ int s_par[kMaxT];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const Cand& c = arena[kept[t]];
+        int par = -1;
+        if (c.parent >= 0)
+            for (int u = 0; u < t; ++u)
+                if (kept[u] == c.parent) par = u;
+        s_par[t] = par;
+        p.tree_tok[(long long)i * T + t] = c.token;
+        p.tree_par[(long long)i * T + t] = par;
+        p.tree_dep[(long long)i * T + t] = c.depth;
+        p.tree_prob[(long long)i * T + t] = c.prob;
+        p.tree_pp[(long long)i * T + t] = c.pp;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) p.tree_n[i] = n;
+    // verify rows
+    for (int t = threadIdx.x; t < T1; t += blockDim.x) {
+        const int r = i * T1 + t;
+        uint32_t* mk = p.vrows.mask + (long long)r * kMaskWords;
+        for (int w = 0; w < kMaskWords; ++w) mk[w] = 0u;
+        if (live && t <= n) {
+            mk[0] = 1u;  // root
+            if (t == 0) {
+                p.vrows.tok[r] = p.tok_hist[(long long)slot * p.cap + lt];
+                p.vrows.pos[r] = lt;
+            } else {
+                const int nd = t - 1;
+                p.vrows.tok[r] = p.tree_tok[(long long)i * T + nd];
+                p.vrows.pos[r] = lt + p.tree_dep[(long long)i * T + nd];
+                for (int a = nd; a >= 0; a = s_par[a]) mk[(a + 1) >> 5] |= 1u << ((a + 1) & 31);
+            }
+            p.vrows.slot[r] = slot;
+            p.vrows.cidx[r] = lt + t;
+        } else {
+            p.vrows.slot[r] = -1;
+            p.vrows.tok[r] = 0;
+            p.vrows.pos[r] = 0;
+            p.vrows.cidx[r] = 0;
+        }
+        p.vrows.fkind[r] = 0;
+        p.vrows.fidx[r] = 0;
+    }
+    if (threadIdx.x == 0) {
+        p.vg.slot[i] = live ? slot : -1;
+        p.vg.lc[i] = lt;
+        p.vg.tail0[i] = lt;
+        p.vg.ntail[i] = live ? n + 1 : 0;
+    }
+}
+
+void launch_tree_level(const TreeParams& p, cudaStream_t st) {
+    static bool attr = false;
+    const int smem = (int)(sizeof(Cand) * kSortCap + sizeof(int) * kSortCap);
+    if (!attr) {
+        cudaFuncSetAttribute(k_tree_level, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_tree_level<<<p.b_hi, kTreeThreads, smem, st>>>(p);
+}
+void launch_tree_final(const TreeParams& p, cudaStream_t st) { k_tree_final<<<p.b_hi, 128, 0, st>>>(p); }
+
+// ---------------------------------------------------------- accept (K7)
+// verify_greedy (spec_decode.hpp:245-268): from the root, accept the child
+// whose token equals the target argmax at the current node (lowest index; a
+// node's children carry distinct tokens), else emit that argmax as the bonus.
+// One warp per request; children are found with a ballot over the tree.
+__global__ void k_accept_greedy(AcceptParams p) {
+    const int i = blockIdx.x;
+    const int lane = threadIdx.x;
+    const bool live = i < p.b && p.step[i].slot >= 0;
+    if (!live) {
+        if (lane == 0 && i < p.b_hi) {
+            p.acc_len[i] = 0;
+            p.bonus[i] = 0;
+        }
+        return;
+    }
+    const int T = p.T, T1 = p.T + 1;
+    const int n = p.tree_n[i];
+    const int* tok = p.tree_tok + (long long)i * T;
+    const int* par = p.tree_par + (long long)i * T;
+    int node = -1, a = 0;
+    int want;
+    for (;;) {
+        const int vrow = i * T1 + (node < 0 ? 0 : node + 1);
+        want = p.argmax[vrow];
+        int found = -1;
+        for (int c0 = 0; c0 < n && found < 0; c0 += 32) {
+            const int c = c0 + lane;
+            const bool hit = c < n && par[c] == node && tok[c] == want;
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (bal) found = c0 + __ffs(bal) - 1;
+        }
+        if (found < 0) break;
+        if (lane == 0) {
+            p.acc_nodes[(long long)i * p.maxD + a] = found;
+            p.acc_tok[(long long)i * p.maxD + a] = want;
+        }
+        ++a;
+        node = found;
+    }
+    if (lane == 0) {
+        p.acc_len[i] = a;
+        p.bonus[i] = want;
+    }
+}
+void launch_accept_greedy(const AcceptParams& p, cudaStream_t st) { k_accept_greedy<<<p.b_hi, 32, 0, st>>>(p); }
+
+// ------------------------------------------------- commit / compaction (K8)
+// grid (b_hi, layers + 1): blocks y < layers compact that layer's target KV
+// (tree slot lt+1+n_j -> lt+1+j, all sources read before any write), block y
+// == layers commits tokens (accepted ++ bonus) and target features of the
+// root + accepted rows into the per-slot histories.
+__global__ void k_commit(CommitParams p) {
+    extern __shared__ __align__(16) unsigned char cm_smem[];
+    const int i = blockIdx.x;
+    const bool live = i < p.b && p.step[i].slot >= 0;
+    if (!live) return;
+    const int slot = p.step[i].slot, lt = p.step[i].lt;
+    const int a = p.acc_len[i];
+    const int y = blockIdx.y;
+    if (y < p.layers) {
+        const int per = p.KV * p.hd;  // elements per cache position
+        bf16* buf = reinterpret_cast<bf16*>(cm_smem);  // [2][a][per]
+        for (int c = threadIdx.x; c < 2 * a * per; c += blockDim.x) {
+            const int which = c / (a * per), rem = c % (a * per);
+            const int jj = rem / per, e = rem % per;
+            const int h = e / p.hd, dd = e % p.hd;
+            const int src = lt + 1 + p.acc_nodes[(long long)i * p.maxD + jj];
+            const bf16* cache = which == 0 ? p.kc[y] : p.vc[y];
+            buf[c] = cache[(((long long)slot * p.KV + h) * p.cap + src) * p.hd + dd];
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < 2 * a * per; c += blockDim.x) {
+            const int which = c / (a * per), rem = c % (a * per);
+            const int jj = rem / per, e = rem % per;
+            const int h = e / p.hd, dd = e % p.hd;
+            const int dst = lt + 1 + jj;
+            bf16* cache = which == 0 ? p.kc[y] : p.vc[y];
+            cache[(((long long)slot * p.KV + h) * p.cap + dst) * p.hd + dd] = buf[c];
+        }
+    } else {
+        // tokens: accepted at lt+1.., bonus at lt+1+a
+        for (int t = threadIdx.x; t <= a; t += blockDim.x) {
+            const int tokv = t < a ? p.acc_tok[(long long)i * p.maxD + t] : p.bonus[i];
+            p.tok_hist[(long long)slot * p.cap + lt + 1 + t] = tokv;
+        }
+        // features of root (verify row 0) and accepted nodes at positions lt..lt+a
+        for (int c = threadIdx.x; c < (a + 1) * p.d; c += blockDim.x) {
+            const int t = c / p.d, e = c % p.d;
+            const int vrow = i * p.row_stride + (t == 0 ? 0 : 1 + p.acc_nodes[(long long)i * p.maxD + t - 1]);
+            p.feat_hist[((long long)slot * p.cap + lt + t) * p.d + e] = p.vfeat[(long long)vrow * p.d + e];
+        }
+        if (threadIdx.x == 0 && p.kv_len) p.kv_len[i] = lt + 1 + a;
+    }
+}
+void launch_commit(const CommitParams& p, cudaStream_t st) {
+    const int smem = 2 * p.maxD * p.KV * p.hd * 2;
+    dim3 grid(p.b_hi, p.layers + 1);
+    k_commit<<<grid, 256, smem, st>>>(p);
+}
+
+// AR commit: token at lt+1, feature at lt
+__global__ void k_commit_ar(const StepIn* __restrict__ st, int b, const int* __restrict__ argmax,
+                            const bf16* __restrict__ feat, int d, int* tok_hist, bf16* feat_hist, int cap,
+                            int* __restrict__ out_tok) {
+    const int i = blockIdx.x;
+    if (i >= b || st[i].slot < 0) return;
+    const int slot = st[i].slot, lt = st[i].lt;
+    if (threadIdx.x == 0) {
+        tok_hist[(long long)slot * cap + lt + 1] = argmax[i];
+        out_tok[i] = argmax[i];
+    }
+    for (int e = threadIdx.x; e < d; e += blockDim.x)
+        feat_hist[((long long)slot * cap + lt) * d + e] = feat[(long long)i * d + e];
+}
+void launch_commit_ar(const StepIn* st, int b, const int* argmax, const bf16* feat, int d, int* tok_hist,
+                      bf16* feat_hist, int cap, int* out_tok, cudaStream_t s) {
+    if (b > 0) k_commit_ar<<<b, 256, 0, s>>>(st, b, argmax, feat, d, tok_hist, feat_hist, cap, out_tok);
+}
+
+}  // namespace tlt

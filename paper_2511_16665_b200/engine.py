@@ -1,0 +1,332 @@
+"""Python host mirror of the C-ABI (include/tlt_b200.h) for tests and bench.
+
+Names and argument meaning follow the reference ``specsim`` API:
+``sd_step`` = build_draft_tree + verify_greedy + commit for a batch
+(spec_decode.hpp:111-268), ``ar_step`` = the plain branch of run_rollout
+(rollout.hpp:247-261), ``Mab`` = beg_initialize / beg_select / beg_record
+(beg_mab.hpp:74-170), ``plan_captures`` (capture_plan.hpp:87-155),
+``run_rollout`` (rollout.hpp:130-276). Errors raise ConfigError /
+RoutingError like the reference (errors.hpp:9-34).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import lib
+
+TLT_OK, TLT_ERR_INTERNAL, TLT_ERR_CONFIG, TLT_ERR_ROUTING, TLT_ERR_CUDA, TLT_ERR_STATE = 0, 1, 2, 3, 4, 5
+MAX_DEPTH = 16  # tlt::kMaxDepth (stride of debug paths)
+
+
+class TltError(RuntimeError):
+    pass
+
+
+class ConfigError(TltError):
+    pass
+
+
+class RoutingError(TltError):
+    pass
+
+
+class CudaError(TltError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == TLT_OK:
+        return
+    msg = lib().tlt_last_error(None)
+    msg = msg.decode() if msg else ""
+    raise {TLT_ERR_CONFIG: ConfigError, TLT_ERR_ROUTING: RoutingError, TLT_ERR_CUDA: CudaError}.get(rc, TltError)(
+        f"[{rc}] {msg}")
+
+
+class Strategy(C.Structure):
+    _fields_ = [("draft_depth", C.c_int32), ("top_k", C.c_int32), ("tokens_to_verify", C.c_int32)]
+
+    def tuple(self):
+        return (self.draft_depth, self.top_k, self.tokens_to_verify)
+
+
+class ModelCfg(C.Structure):
+    _fields_ = [("vocab", C.c_int32), ("hidden", C.c_int32), ("layers", C.c_int32), ("heads", C.c_int32),
+                ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32), ("qkv_bias", C.c_int32),
+                ("rope_theta", C.c_float), ("rms_eps", C.c_float), ("max_slots", C.c_int32), ("max_ctx", C.c_int32)]
+
+
+class InitCfg(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("layer_scale", C.c_float), ("lm_gain", C.c_float), ("lm_noise", C.c_float),
+                ("fc_noise", C.c_float)]
+
+
+class TreeOut(C.Structure):
+    _fields_ = [("tokens", C.c_void_p), ("parents", C.c_void_p), ("depths", C.c_void_p), ("probs", C.c_void_p),
+                ("path_probs", C.c_void_p), ("n_nodes", C.c_void_p)]
+
+
+class AcceptOut(C.Structure):
+    _fields_ = [("accepted", C.c_void_p), ("nodes", C.c_void_p), ("accept_len", C.c_void_p), ("bonus", C.c_void_p),
+                ("kv_src", C.c_void_p), ("kv_len", C.c_void_p), ("elapsed_ms", C.c_void_p)]
+
+
+class CaptureEntry(C.Structure):
+    _fields_ = [("side", C.c_int32), ("bucket_lo", C.c_int32), ("bucket_hi", C.c_int32),
+                ("tokens_to_verify", C.c_int32), ("top_k", C.c_int32), ("draft_depth", C.c_int32),
+                ("memory_units", C.c_double)]
+
+
+class RolloutCfg(C.Structure):
+    _fields_ = [("enable_sd", C.c_int32), ("elastic_threshold", C.c_int32), ("mode", C.c_int32),
+                ("temperature", C.c_float), ("fixed_strategy", Strategy), ("use_mab", C.c_int32),
+                ("seed", C.c_uint64), ("use_graphs", C.c_int32)]
+
+
+class RolloutResult(C.Structure):
+    _fields_ = [("generated", C.c_void_p), ("gen_len", C.c_void_p), ("sd_steps", C.c_int64),
+                ("plain_steps", C.c_int64), ("verify_events", C.c_int64), ("accepted_total", C.c_int64),
+                ("emitted_total", C.c_int64), ("device_ms", C.c_double), ("wall_ms", C.c_double),
+                ("gpu_launches", C.c_int64)]
+
+
+def _p(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+# Model shapes. "tiny" is BASELINE config 1 (the parity
+# workload); "qwen2.5-7b" / "qwen2.5-32b" are the Qwen2.5 shapes of configs 2-5.
+MODELS = {
+    "tiny": dict(vocab=4096, hidden=256, layers=2, heads=4, kv_heads=2, head_dim=64, ffn=688, qkv_bias=1,
+                 rope_theta=1e4, rms_eps=1e-6),
+    "qwen2.5-7b": dict(vocab=152064, hidden=3584, layers=28, heads=28, kv_heads=4, head_dim=128, ffn=18944,
+                       qkv_bias=1, rope_theta=1e6, rms_eps=1e-6),
+    "qwen2.5-32b": dict(vocab=152064, hidden=5120, layers=64, heads=40, kv_heads=8, head_dim=128, ffn=27648,
+                        qkv_bias=1, rope_theta=1e6, rms_eps=1e-6),
+}
+# Structure knob per model: mean accept length in a realistic band.
+INITS = {
+    "tiny": dict(seed=42, layer_scale=1.0, lm_gain=4.0, lm_noise=2.0, fc_noise=0.05),
+    "qwen2.5-7b": dict(seed=42, layer_scale=0.3, lm_gain=4.0, lm_noise=2.0, fc_noise=0.05),
+    "qwen2.5-32b": dict(seed=42, layer_scale=0.3, lm_gain=4.0, lm_noise=2.0, fc_noise=0.05),
+}
+
+
+@dataclass
+class StepResult:
+    accept_len: np.ndarray
+    bonus: np.ndarray
+    accepted: list
+    nodes: list
+    kv_len: np.ndarray
+    elapsed_ms: float
+    tree: list | None
+
+
+class Engine:
+    def __init__(self, model: str | dict = "tiny", max_slots: int = 4, max_ctx: int = 512, init: dict | None = None,
+                 device: int = 0, **overrides):
+        m = dict(MODELS[model]) if isinstance(model, str) else dict(model)
+        m.update(overrides)
+        self.model = m
+        ini = dict(INITS.get(model, INITS["tiny"]) if isinstance(model, str) else INITS["tiny"])
+        if init:
+            ini.update(init)
+        self.init = ini
+        self.cfg = ModelCfg(m["vocab"], m["hidden"], m["layers"], m["heads"], m["kv_heads"], m["head_dim"], m["ffn"],
+                            m["qkv_bias"], m["rope_theta"], m["rms_eps"], max_slots, max_ctx)
+        self.icfg = InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_noise"], ini["fc_noise"])
+        self.L = lib()
+        h = C.c_void_p()
+        _check(self.L.tlt_engine_create(C.byref(self.cfg), C.byref(self.icfg), device, C.byref(h)))
+        self.h = h
+        self.vocab = m["vocab"]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.tlt_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- state
+    def prefill(self, slots, prompts):
+        slots = np.asarray(slots, np.int32)
+        lens = np.asarray([len(p) for p in prompts], np.int32)
+        toks = np.concatenate([np.asarray(p, np.int32) for p in prompts]).astype(np.int32)
+        _check(self.L.tlt_prefill(self.h, len(slots), _p(slots), _p(lens), _p(toks)))
+
+    def release(self, slot):
+        _check(self.L.tlt_release(self.h, slot))
+
+    def slot_len(self, slot) -> int:
+        v = C.c_int32()
+        _check(self.L.tlt_slot_len(self.h, slot, C.byref(v)))
+        return v.value
+
+    def set_debug(self, on: bool):
+        _check(self.L.tlt_set_debug(self.h, 1 if on else 0))
+
+    # -------------------------------------------------------------- steps
+    def sd_step(self, strategy, slots, want_tree: bool = True) -> StepResult:
+        s = Strategy(*strategy)
+        slots = np.asarray(slots, np.int32)
+        b, D, T = len(slots), s.draft_depth, s.tokens_to_verify
+        acc = np.zeros((b, D), np.int32)
+        nodes = np.zeros((b, D), np.int32)
+        alen = np.zeros(b, np.int32)
+        bonus = np.zeros(b, np.int32)
+        kvl = np.zeros(b, np.int32)
+        ms = np.zeros(1, np.float32)
+        ao = AcceptOut(acc.ctypes.data, nodes.ctypes.data, alen.ctypes.data, bonus.ctypes.data, None,
+                       kvl.ctypes.data, ms.ctypes.data)
+        tree = None
+        to = None
+        if want_tree:
+            tt = np.zeros((b, T), np.int32)
+            tp = np.zeros((b, T), np.int32)
+            td = np.zeros((b, T), np.int32)
+            tpr = np.zeros((b, T), np.float64)
+            tpp = np.zeros((b, T), np.float64)
+            tn = np.zeros(b, np.int32)
+            to = TreeOut(tt.ctypes.data, tp.ctypes.data, td.ctypes.data, tpr.ctypes.data, tpp.ctypes.data,
+                         tn.ctypes.data)
+        _check(self.L.tlt_sd_step(self.h, C.byref(s), b, _p(slots), C.byref(to) if to else None, C.byref(ao)))
+        if want_tree:
+            tree = [list(zip(tt[i, :tn[i]].tolist(), tp[i, :tn[i]].tolist(), td[i, :tn[i]].tolist(),
+                             tpr[i, :tn[i]].tolist(), tpp[i, :tn[i]].tolist())) for i in range(b)]
+        return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
+                          [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), tree)
+
+    def ar_step(self, slots):
+        slots = np.asarray(slots, np.int32)
+        out = np.zeros(len(slots), np.int32)
+        ms = C.c_float()
+        _check(self.L.tlt_ar_step(self.h, len(slots), _p(slots), _p(out), C.byref(ms)))
+        return out, ms.value
+
+    # ---------------------------------------------------------- debug
+    def debug_expansions(self, i: int, max_exp: int = 4096):
+        n = C.c_int32()
+        plen = np.zeros(max_exp, np.int32)
+        paths = np.zeros((max_exp, MAX_DEPTH), np.int32)
+        _check(self.L.tlt_debug_expansions(self.h, i, max_exp, C.byref(n), _p(plen), _p(paths), None))
+        cnt = min(n.value, max_exp)
+        rows = np.zeros((cnt, self.vocab), np.float64)
+        _check(self.L.tlt_debug_expansions(self.h, i, cnt, C.byref(n), _p(plen), _p(paths), _p(rows)))
+        return [(tuple(paths[j, :plen[j]].tolist()), rows[j]) for j in range(cnt)]
+
+    def debug_verify_logits(self, i: int, max_rows: int = 256):
+        out = np.zeros((max_rows, self.vocab), np.float32)
+        n = C.c_int32()
+        _check(self.L.tlt_debug_verify_logits(self.h, i, _p(out), max_rows, C.byref(n)))
+        return out[:n.value]
+
+    def debug_ar_logits(self, b: int):
+        out = np.zeros((b, self.vocab), np.float32)
+        _check(self.L.tlt_debug_ar_logits(self.h, _p(out), b))
+        return out
+
+    # ---------------------------------------------------------- rollout
+    def run_rollout(self, prompts, max_lens, request_ids=None, *, enable_sd=True, elastic_threshold=32,
+                    strategy=(4, 4, 16), mab: "Mab | None" = None, seed=0, use_graphs=True):
+        n = len(prompts)
+        rid = np.asarray(request_ids if request_ids is not None else range(n), np.int32)
+        plen = np.asarray([len(p) for p in prompts], np.int32)
+        toks = np.concatenate([np.asarray(p, np.int32) for p in prompts]).astype(np.int32)
+        ml = np.asarray(max_lens, np.int32)
+        stride = int(ml.max())
+        gen = np.zeros((n, stride), np.int32)
+        glen = np.zeros(n, np.int32)
+        cfg = RolloutCfg(1 if enable_sd else 0, elastic_threshold, 0, 0.0, Strategy(*strategy),
+                         1 if mab is not None else 0, seed, 1 if use_graphs else 0)
+        res = RolloutResult(gen.ctypes.data, glen.ctypes.data)
+        _check(self.L.tlt_run_rollout(self.h, C.byref(cfg), mab.h if mab is not None else None, n, _p(rid),
+                                      _p(plen), _p(toks), _p(ml), stride, C.byref(res)))
+        return dict(tokens=[gen[i, :glen[i]].tolist() for i in range(n)], sd_steps=res.sd_steps,
+                    plain_steps=res.plain_steps, verify_events=res.verify_events,
+                    accepted_total=res.accepted_total, emitted_total=res.emitted_total, device_ms=res.device_ms,
+                    wall_ms=res.wall_ms, gpu_launches=res.gpu_launches)
+
+
+class Rng:
+    def __init__(self, seed=0, stream=0, _h=None):
+        self.L = lib()
+        if _h is None:
+            _h = C.c_void_p()
+            _check(self.L.tlt_rng_create(C.c_uint64(seed), C.c_uint64(stream), C.byref(_h)))
+        self.h = _h
+
+    def fork(self, label):
+        h = C.c_void_p()
+        _check(self.L.tlt_rng_fork(self.h, C.c_uint64(label), C.byref(h)))
+        return Rng(_h=h)
+
+    def next_u64(self):
+        return self.L.tlt_rng_next_u64(self.h)
+
+    def uniform01(self):
+        return self.L.tlt_rng_uniform01(self.h)
+
+    def __del__(self):
+        try:
+            self.L.tlt_rng_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Mab:
+    def __init__(self, strategies, thresholds, epsilon=0.1, window=20):
+        self.L = lib()
+        self.strategies = [tuple(s) for s in strategies]
+        arr = (Strategy * len(strategies))(*[Strategy(*s) for s in strategies])
+        thr = np.asarray(thresholds, np.int32)
+        h = C.c_void_p()
+        _check(self.L.tlt_mab_create(arr, len(strategies), _p(thr), len(thr), C.c_double(epsilon), window,
+                                     C.byref(h)))
+        self.h = h
+
+    def select(self, batch, rng: Rng):
+        arm = C.c_int32()
+        s = Strategy()
+        _check(self.L.tlt_mab_select(self.h, batch, rng.h, C.byref(arm), C.byref(s)))
+        return arm.value, s.tuple()
+
+    def record(self, strategy, elapsed, accept_lens):
+        lens = np.asarray(accept_lens, np.int32)
+        _check(self.L.tlt_mab_record(self.h, C.byref(Strategy(*strategy)), C.c_double(elapsed), _p(lens),
+                                     len(lens)))
+
+    def arm_stats(self, arm):
+        med, sel, n = C.c_double(), C.c_int64(), C.c_int32()
+        _check(self.L.tlt_mab_arm_stats(self.h, arm, C.byref(med), C.byref(sel), C.byref(n)))
+        return med.value, sel.value, n.value
+
+    def apply_record(self, arm, reward, a_bar):
+        _check(self.L.tlt_mab_apply_record(self.h, arm, C.c_double(reward), C.c_double(a_bar)))
+
+    def __del__(self):
+        try:
+            self.L.tlt_mab_destroy(self.h)
+        except Exception:
+            pass
+
+
+def plan_captures(strategies, thresholds, max_batch=32, vanilla=False):
+    L = lib()
+    arr = (Strategy * len(strategies))(*[Strategy(*s) for s in strategies])
+    thr = np.asarray(thresholds, np.int32)
+    out = (CaptureEntry * 4096)()
+    n = C.c_int()
+    tot = C.c_double()
+    _check(L.tlt_plan_captures(arr, len(strategies), _p(thr), len(thr), max_batch, 1 if vanilla else 0, out, 4096,
+                               C.byref(n), C.byref(tot)))
+    return [(e.side, e.bucket_lo, e.bucket_hi, e.tokens_to_verify, e.top_k, e.draft_depth, e.memory_units)
+            for e in out[:n.value]], tot.value
