@@ -1,0 +1,363 @@
+"""bench.py — accepted tokens/s of the greedy tree-SD rollout (BASELINE config 2).
+
+One bench STEP = one rollout of the rank's request group (Qwen2.5-7B-shaped
+random-init target + 1-layer EAGLE drafter; 64 requests per GPU, long-tail
+response lengths, batch 64 -> 1) through the reference-facing C-ABI
+(tlt_run_rollout == reference run_rollout, rollout.hpp:130-276): prefill,
+elastic gate (SD when batch < 32), BEG-MAB strategy select per batch bucket
+(default 8 arms, thresholds {1,2,8,16}), greedy tree SD steps replaying the
+CUDA-graph pool, plain AR steps above the gate, emission with EOS / max_len.
+
+  value  = emitted tokens (all ranks) / device time of the timed rollouts
+           (CUDA events on the engine stream around every prefill/step, max
+           over ranks) — inputs already resident.
+  e2e    = same tokens / wall time of the timed tlt_run_rollout calls with
+           HOST prompts in and HOST generated tokens out (all H2D/D2H and
+           per-step host decisions inside), barrier + synchronize on both
+           sides, max over ranks.
+
+Under torchrun each rank runs an independent engine on its own GPU with its
+own 64 requests (request_id % world == rank, weak scaling); no collective is
+on the data path. --impl reference times the CPU path (oracle port of the
+reference spec_generate over the neural leaves) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "accepted tokens/s per GPU (tree-SD rollout) at 1/2/4/8 B200; mean accept len"
+DEFAULT_ARMS = [(10, 8, 64), (6, 8, 64), (10, 8, 48), (6, 8, 48), (10, 8, 32), (6, 8, 32), (10, 8, 16), (6, 8, 16)]
+THRESHOLDS = [1, 2, 8, 16]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def response_lengths(n, mu, sigma, max_len, seed):
+    """sample_response_length (rollout.hpp:42-50) with the RngStream normal (rng.hpp:64-69)."""
+    from paper_2511_16665_b200.engine import Rng
+    r = Rng(seed, 0x4C454E)
+    out = []
+    for _ in range(n):
+        u1, u2 = r.uniform01(), r.uniform01()
+        z = math.sqrt(-2.0 * math.log1p(-u1)) * math.cos(6.283185307179586477 * u2)
+        v = round(math.exp(mu + sigma * z))
+        out.append(int(min(max(v, 1), max_len)))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                o = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [x.strip() for x in o.stdout.strip().split(",")]
+                if len(f) >= 7:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return world, rank, local, pg
+
+
+def max_over_ranks(pg, vals, local):
+    if pg is None:
+        return vals
+    import torch
+    t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{local}")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return t.tolist()
+
+
+def sum_over_ranks(pg, vals, local):
+    if pg is None:
+        return vals
+    import torch
+    t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{local}")
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return t.tolist()
+
+
+def barrier(pg, local):
+    import torch
+    torch.cuda.synchronize(local)
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize(local)
+
+
+# ----------------------------------------------------------------- CPU arm
+def cpu_rollout_sample(model_name, n_threads, gen_tokens, prompt_len, strategy, seed=0):
+    """Oracle port of spec_generate (greedy tree) over the neural CPU leaves."""
+    import ctypes as C
+
+    import oracle as O
+    from paper_2511_16665_b200.engine import INITS, MODELS
+    m, ini = MODELS[model_name], INITS[model_name]
+    L = O.orc()
+    cfg = O.ModelCfg(m["vocab"], m["hidden"], m["layers"], m["heads"], m["kv_heads"], m["head_dim"], m["ffn"],
+                     m["qkv_bias"], m["rope_theta"], m["rms_eps"], prompt_len + gen_tokens + 64)
+    icfg = O.InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"],
+                     ini["fc_noise"])
+    t0 = time.time()
+    om = L.orc_model_create(C.byref(cfg), C.byref(icfg), n_threads)
+    init_s = time.time() - t0
+    L.orc_neural_spec_generate.argtypes = [C.c_void_p] * 11
+    rng = np.random.default_rng(seed)
+    prompt = (C.c_int32 * prompt_len)(*rng.integers(2, m["vocab"], prompt_len).tolist())
+    out = (C.c_int32 * 512)()
+    n = C.c_int()
+    acc = (C.c_int32 * 512)()
+    t0 = time.time()
+    steps = L.orc_neural_spec_generate(om, prompt, prompt_len, gen_tokens, C.byref(O.Strategy(*strategy)), out,
+                                       C.byref(n), acc, None, None, 512)
+    dt = time.time() - t0
+    L.orc_model_destroy(om)
+    return dict(tokens=n.value, seconds=dt, steps=steps, init_s=init_s,
+                mean_accept=float(np.mean(list(acc[:max(steps, 1)]))))
+
+
+def run_reference(a):
+    world, rank, local, pg = dist_setup(a.gpus)
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    strategy = (6, 8, 16)
+    vals = []
+    for i in range(a.warmup + a.steps):
+        r = cpu_rollout_sample(a.model, threads, a.cpu_gen, a.cpu_prompt, strategy, seed=i)
+        if i >= a.warmup:
+            vals.append(r)
+    toks = sum(v["tokens"] for v in vals)
+    secs = sum(v["seconds"] for v in vals)
+    value = toks / secs if secs > 0 else 0.0
+    sample = (f"{a.model} CPU oracle port, 1 request, prompt {a.cpu_prompt}, {a.cpu_gen} generated tokens per step, "
+              f"greedy tree SD {strategy}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(secs / max(1, len(vals)) * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16-weights/fp32",
+        "data": "synthetic", "config": {"workload": "config2-long-tail-sample", "model": a.model},
+        "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "mean_accept_len": round(float(np.mean([v["mean_accept"] for v in vals])), 3)}), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def gemm_roofline(model_name, m_tok, peak_gbs):
+    """Dominant kernel: gate_up GEMM (largest weight) at the long-tail verify
+    M, timed back to back with CUDA events on its own stream."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2511_16665_b200 import _lib
+    from paper_2511_16665_b200.engine import MODELS
+    mm = MODELS[model_name]
+    K, N = mm["hidden"], 2 * mm["ffn"]
+    L = _lib.lib()
+    x = torch.randn(m_tok, K, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    y = torch.empty(m_tok, N // 2, device="cuda", dtype=torch.bfloat16)
+    ws = torch.empty(64 << 20, device="cuda", dtype=torch.float32)
+    ms = C.c_float()
+    rc = L.tlt_dev_time_gemm(x.data_ptr(), m_tok, K, w.data_ptr(), N, 3, None, y.data_ptr(), ws.data_ptr(),
+                             ws.numel(), 50, C.byref(ms))
+    if rc < 0:
+        return None
+    byts = N * K * 2 + m_tok * K * 2 + m_tok * (N // 2) * 2
+    ach = byts / (ms.value * 1e-3) / 1e9
+    return {"kernel": f"gate_up tcgen05 GEMM+SwiGLU [M={m_tok}]x[{K}]x[{N}]", "bound": "hbm",
+            "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 3),
+            "traffic": None, "algorithmic_bytes": byts, "avg_launch_ms": round(ms.value, 4)}
+
+
+def run_ours(a):
+    world, rank, local, pg = dist_setup(a.gpus)
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2511_16665_b200.engine import Engine, Mab
+    peak_gbs, peak_tf, peak_kind = peaks()
+    n = a.requests
+    max_ctx = a.prompt + a.max_len + 8
+    eng = Engine(a.model, max_slots=n, max_ctx=max_ctx, device=local)
+    mab = Mab(DEFAULT_ARMS, THRESHOLDS, 0.1, 20)
+    V = eng.vocab
+
+    def workload(step):
+        # request ids of this rank: global id = rank + world * i (request_id % world == rank)
+        ids = [rank + world * i for i in range(n)]
+        rng = np.random.default_rng(1000 * step + rank)
+        prompts = [rng.integers(2, V, a.prompt).tolist() for _ in range(n)]
+        lens = response_lengths(n, math.log(a.len_median), a.len_sigma, a.max_len, seed=100 + step + 7919 * rank)
+        return ids, prompts, lens
+
+    def rollout(step, enable_sd=True):
+        ids, prompts, lens = workload(step)
+        return eng.run_rollout(prompts, lens, ids, enable_sd=enable_sd, elastic_threshold=a.elastic,
+                               mab=mab, seed=step, use_graphs=True)
+
+    for s in range(a.warmup):
+        rollout(s)
+    barrier(pg, local)
+    res = []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for s in range(a.steps):
+            res.append(rollout(a.warmup + s))
+        barrier(pg, local)
+        wall = time.perf_counter() - t0
+    emitted = sum(r["emitted_total"] for r in res)
+    dev_s = sum(r["device_ms"] for r in res) / 1e3
+    accepted = sum(r["accepted_total"] for r in res)
+    events = sum(r["verify_events"] for r in res)
+    launches = sum(r["gpu_launches"] for r in res)
+    sd_steps = sum(r["sd_steps"] for r in res)
+    plain_steps = sum(r["plain_steps"] for r in res)
+    h2d = sum(4 * (a.prompt + 3) * n for _ in range(1))
+    d2h = 4 * sum(len(t) for t in res[-1]["tokens"]) if res else 0
+    tot = sum_over_ranks(pg, [emitted, accepted, events], local)
+    mx = max_over_ranks(pg, [dev_s, wall], local)
+    value = tot[0] / mx[0] if mx[0] > 0 else 0.0
+    e2e = tot[0] / mx[1] if mx[1] > 0 else 0.0
+    # same engine, plain AR decode on the same workload (the 2x denominator)
+    ar = rollout(a.warmup, enable_sd=False) if a.ar_baseline else None
+    ar_tok_s = ar["emitted_total"] / (ar["device_ms"] / 1e3) if ar else None
+    sd_same = res[0] if res else None
+    out = None
+    if rank == 0:
+        roof = gemm_roofline(a.model, a.roof_m, peak_gbs)
+        if roof is not None:
+            roof["peak_kind"] = peak_kind
+        cpu = None
+        if a.cpu_gen > 0:
+            threads = os.cpu_count() or 1
+            c = cpu_rollout_sample(a.model, threads, a.cpu_gen, a.cpu_prompt, (6, 8, 16))
+            cpu = {"value": round(c["tokens"] / c["seconds"], 4), "unit": "tokens/s", "cores": threads, "kind": "port",
+                   "sample": f"{a.model} CPU oracle port (C restatement of spec_generate + neural leaves), 1 request, "
+                             f"prompt {a.cpu_prompt}, {a.cpu_gen} tokens, greedy tree SD (6,8,16); "
+                             f"{c['seconds']:.1f}s"}
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(mx[0] * 1e3 / max(1, a.steps), 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "config2: Qwen2.5-7B-shaped random-init target + 1-layer EAGLE drafter, "
+                                   "long-tail rollout batch 64->1, greedy tree SD, BEG-MAB",
+                       "model": a.model, "requests_per_gpu": n, "prompt_len": a.prompt,
+                       "len_lognormal": [round(math.log(a.len_median), 4), a.len_sigma, a.max_len],
+                       "elastic_threshold": a.elastic, "strategies": DEFAULT_ARMS, "thresholds": THRESHOLDS,
+                       "parallelism": f"dp{world} (independent rollout groups)",
+                       "l2": "KV + weights (15.2 GB) exceed the 126 MB L2 every step; no flush needed"},
+            "per_gpu": round(value / world, 2),
+            "mean_accept_len": round(tot[1] / tot[2], 3) if tot[2] else None,
+            "mean_accept_len_with_bonus": round(tot[1] / tot[2] + 1, 3) if tot[2] else None,
+            "sd_steps": sd_steps, "plain_steps": plain_steps,
+            "e2e": {"value": round(e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        if ar is not None:
+            out["ar_baseline"] = {"value": round(ar_tok_s, 2), "unit": "tokens/s (same engine, plain AR decode)",
+                                  "sd_rollout_same_workload": round(sd_same["emitted_total"] /
+                                                                    (sd_same["device_ms"] / 1e3), 2),
+                                  "speedup": round((sd_same["emitted_total"] / (sd_same["device_ms"] / 1e3)) /
+                                                   ar_tok_s, 3)}
+        print(json.dumps(out), flush=True)
+    eng.close()
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="qwen2.5-7b")
+    ap.add_argument("--requests", type=int, default=64)
+    ap.add_argument("--prompt", type=int, default=256)
+    ap.add_argument("--len-median", type=float, default=400.0)
+    ap.add_argument("--len-sigma", type=float, default=1.0)
+    ap.add_argument("--max-len", type=int, default=2048)
+    ap.add_argument("--elastic", type=int, default=32)
+    ap.add_argument("--roof-m", type=int, default=17)
+    ap.add_argument("--ar-baseline", type=int, default=1)
+    ap.add_argument("--cpu-gen", type=int, default=8)
+    ap.add_argument("--cpu-prompt", type=int, default=8)
+    a = ap.parse_args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

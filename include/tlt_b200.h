@@ -76,6 +76,7 @@ typedef struct {
     uint64_t seed;
     float layer_scale; /* std of attention/MLP weights ("structure" knob) */
     float lm_gain;     /* bigram structure of the LM head */
+    float lm_alt;      /* relative gain of the second (alternative) successor */
     float lm_noise;    /* unstructured part of the LM head */
     float fc_noise;    /* drafter fc deviation from the embedding passthrough */
 } tlt_init_cfg;
@@ -240,6 +241,10 @@ TLT_API int tlt_debug_ar_logits(tlt_engine* e, float* logits, int b);
  * 3 SwiGLU (W rows interleaved gate/up). Returns the split-K factor used. */
 TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32, void* y_bf16,
                          float* ws, long long ws_elems, int max_splits);
+/* Average device ms of one GEMM launch over `iters` back-to-back launches
+ * (CUDA events on a private stream). Returns the split-K factor. */
+TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
+                              void* y_bf16, float* ws, long long ws_elems, int iters, float* avg_ms);
 
 #ifdef __cplusplus
 }

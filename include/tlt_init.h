@@ -50,6 +50,8 @@ enum {
 /* LM-head backbone permutation: row y copies embedding row perm(y). */
 #define TLT_PERM_A 1000003ULL
 #define TLT_PERM_B 12345ULL
+#define TLT_PERM_A2 999983ULL
+#define TLT_PERM_B2 54321ULL
 
 TLT_HD uint64_t tlt_mix64(uint64_t z) {
     z ^= z >> 30;
@@ -99,7 +101,7 @@ TLT_HD float tlt_bf16_bits_to_f32(uint16_t b) {
 
 typedef struct {
     uint64_t seed;
-    float layer_scale, lm_gain, lm_noise, fc_noise;
+    float layer_scale, lm_gain, lm_alt, lm_noise, fc_noise;
     int vocab, hidden, heads, kv_heads, head_dim, ffn;
 } tlt_init_params;
 
@@ -119,12 +121,18 @@ TLT_HD uint16_t tlt_init_elem(const tlt_init_params* p, int tensor, int layer, i
                 v = 0.0f;
                 break;
             }
-            int64_t src = (int64_t)((TLT_PERM_A * (uint64_t)y + TLT_PERM_B) % (uint64_t)p->vocab);
-            float e = tlt_bf16_bits_to_f32(
-                tlt_f32_to_bf16_bits(TLT_FMUL(sqrt3, tlt_hash_unit(p->seed, TLT_W_EMBED, 0, src * d + i))));
+            /* two successors per token: y is the primary continuation of
+             * perm1(y) and the alternative continuation of perm2(y) */
+            int64_t s1 = (int64_t)((TLT_PERM_A * (uint64_t)y + TLT_PERM_B) % (uint64_t)p->vocab);
+            int64_t s2 = (int64_t)((TLT_PERM_A2 * (uint64_t)y + TLT_PERM_B2) % (uint64_t)p->vocab);
+            float e1 = tlt_bf16_bits_to_f32(
+                tlt_f32_to_bf16_bits(TLT_FMUL(sqrt3, tlt_hash_unit(p->seed, TLT_W_EMBED, 0, s1 * d + i))));
+            float e2 = tlt_bf16_bits_to_f32(
+                tlt_f32_to_bf16_bits(TLT_FMUL(sqrt3, tlt_hash_unit(p->seed, TLT_W_EMBED, 0, s2 * d + i))));
             float a = TLT_FMUL(p->lm_gain, 1.0f / (float)d);
+            float a2 = TLT_FMUL(a, p->lm_alt);
             float b = TLT_FMUL(p->lm_noise, 1.0f / (float)d);
-            v = TLT_FADD(TLT_FMUL(a, e), TLT_FMUL(TLT_FMUL(b, sqrt3), r));
+            v = TLT_FADD(TLT_FADD(TLT_FMUL(a, e1), TLT_FMUL(a2, e2)), TLT_FMUL(TLT_FMUL(b, sqrt3), r));
         } break;
         case TLT_W_FINAL_NORM:
         case TLT_W_ATTN_NORM:

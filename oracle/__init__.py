@@ -58,7 +58,7 @@ class ModelCfg(C.Structure):
 
 
 class InitCfg(C.Structure):
-    _fields_ = [("seed", C.c_uint64), ("layer_scale", C.c_float), ("lm_gain", C.c_float),
+    _fields_ = [("seed", C.c_uint64), ("layer_scale", C.c_float), ("lm_gain", C.c_float), ("lm_alt", C.c_float),
                 ("lm_noise", C.c_float), ("fc_noise", C.c_float)]
 
 

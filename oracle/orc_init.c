@@ -11,7 +11,7 @@ void orc_init_range(const tlt_init_params* p, uint16_t* dst, int tensor, int lay
 }
 
 uint16_t orc_init_value(const orc_init_cfg* init, const orc_model_cfg* c, int tensor, int layer, int64_t idx) {
-    tlt_init_params p = {init->seed, init->layer_scale, init->lm_gain, init->lm_noise, init->fc_noise,
+    tlt_init_params p = {init->seed, init->layer_scale, init->lm_gain, init->lm_alt, init->lm_noise, init->fc_noise,
                          c->vocab,   c->hidden,         c->heads,     c->kv_heads,    c->head_dim, c->ffn};
     return tlt_init_elem(&p, tensor, layer, idx);
 }

@@ -110,7 +110,7 @@ orc_model* orc_model_create(const orc_model_cfg* cfg, const orc_init_cfg* init, 
     if (!m) return NULL;
     m->c = *cfg;
     m->n_threads = n_threads < 1 ? 1 : (n_threads > 256 ? 256 : n_threads);
-    m->ip = (tlt_init_params){init->seed, init->layer_scale, init->lm_gain, init->lm_noise, init->fc_noise,
+    m->ip = (tlt_init_params){init->seed, init->layer_scale, init->lm_gain, init->lm_alt, init->lm_noise, init->fc_noise,
                               cfg->vocab, cfg->hidden,      cfg->heads,    cfg->kv_heads,  cfg->head_dim, cfg->ffn};
     int64_t V = cfg->vocab, d = cfg->hidden;
     m->embed = init_tensor(m, TLT_W_EMBED, 0, V * d);
@@ -207,8 +207,14 @@ static void* mm_worker(void* a) {
         for (int k = 0; k < j->K; ++k) wf[k] = bf(w[k]);
         for (int t = 0; t < j->n; ++t) {
             const float* xr = j->x + (size_t)t * (size_t)j->K;
+            /* 16 independent partial sums: vectorizable without reassociation */
+            float acc[16] = {0};
+            int k = 0;
+            for (; k + 16 <= j->K; k += 16)
+                for (int u = 0; u < 16; ++u) acc[u] += xr[k + u] * wf[k + u];
             float s = 0.f;
-            for (int k = 0; k < j->K; ++k) s += xr[k] * wf[k];
+            for (int u = 0; u < 16; ++u) s += acc[u];
+            for (; k < j->K; ++k) s += xr[k] * wf[k];
             if (j->accumulate)
                 j->y[(size_t)t * j->N + o] += s;
             else

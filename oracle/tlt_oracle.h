@@ -173,7 +173,7 @@ typedef struct {
 } orc_model_cfg;
 typedef struct {
     uint64_t seed;
-    float layer_scale, lm_gain, lm_noise, fc_noise;
+    float layer_scale, lm_gain, lm_alt, lm_noise, fc_noise;
 } orc_init_cfg;
 
 typedef struct orc_model orc_model;

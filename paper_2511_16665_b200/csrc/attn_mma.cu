@@ -1,0 +1,312 @@
+// Tree-masked GQA flash-decode attention on the tensor cores (mma.sync
+// m16n8k16 bf16 -> fp32, ldmatrix for V^T).
+//
+// Work unit (CTA): one request group x one KV head x 16 query vectors (the
+// (row, q-head) pairs of that KV head, GQA-packed) x one 256-key split aligned
+// to absolute key indices. Each of the 4 warps owns a 64-key quarter of the
+// split (keys across warps, so a single decode row still spreads over the SM),
+// stages 32 keys of K and V at a time in its own padded shared-memory slice
+// (cp.async 16B), runs S = Q K^T, applies the tree mask (bits per query row
+// staged in shared memory), an online exp2 softmax, O += P V, and the four
+// warps merge (m, l, O) in shared memory into one split partial for
+// k_attn_combine. Key layout per slot/head is contiguous [cap][hd] so every
+// 32-key tile is 8 KB of coalesced loads.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "engine_kernels.h"
+#include "kernels.cuh"
+
+namespace tlt {
+
+using bf16 = __nv_bfloat16;
+
+namespace {
+constexpr int kQV = 16;         // query vectors per CTA (one m16 tile)
+constexpr int kSplit = 256;     // keys per CTA split
+constexpr int kWarpKeys = 64;   // keys per warp per split
+constexpr int kTile = 32;       // keys per warp iteration
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                                              const void* p) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(a));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int sz = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+}  // namespace
+
+template <int kHD>
+__global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
+    constexpr int kStride = kHD + 8;  // padded smem row (elements): conflict-free fragments
+    constexpr int KS = kHD / 16;      // k-steps over head_dim
+    constexpr int NT = kHD / 8;       // n-tiles of the output
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    bf16* Qs = reinterpret_cast<bf16*>(sm_raw);                       // [16][kStride]
+    bf16* KVs = Qs + kQV * kStride;                                   // per warp: K[32][kStride], V[32][kStride]
+    uint32_t* Ms = reinterpret_cast<uint32_t*>(KVs + 4 * 2 * kTile * kStride);  // [16][kMaskWords]
+    float* red = reinterpret_cast<float*>(KVs);                       // merge scratch (aliases K/V after the loop)
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int G = p.H / p.KV;
+    const int kvh = blockIdx.y;
+    const int grp = blockIdx.z / p.max_splits;
+    const int split = blockIdx.z % p.max_splits;
+    const int qv0 = blockIdx.x * kQV;
+    const int nqv = p.rows_per_req * G;
+    const int slot = p.g.slot[grp];
+    const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
+    const int total = slot >= 0 ? lc + ntail : 0;
+    const int k0 = split * kSplit;
+
+    // ---- stage Q (bf16) and the query rows' tail masks
+    __shared__ int s_row[kQV];
+    if (threadIdx.x < kQV) {
+        const int gqv = qv0 + threadIdx.x;
+        int row = -1;
+        if (gqv < nqv) {
+            row = grp * p.rows_per_req + gqv / G;
+            if (p.rows.slot[row] < 0) row = -1;
+        }
+        s_row[threadIdx.x] = row;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kQV * (kHD / 8); c += blockDim.x) {
+        const int l = c / (kHD / 8), w = c % (kHD / 8);
+        const int row = s_row[l];
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row >= 0) {
+            const int head = kvh * G + (qv0 + l) % G;
+            v = reinterpret_cast<const uint4*>(p.q + (long long)row * p.H * kHD + head * kHD)[w];
+        }
+        *reinterpret_cast<uint4*>(Qs + l * kStride + w * 8) = v;
+    }
+    const int mw = (ntail + 31) >> 5;
+    for (int c = threadIdx.x; c < kQV * kMaskWords; c += blockDim.x) {
+        const int l = c / kMaskWords, w = c % kMaskWords;
+        const int row = s_row[l];
+        Ms[c] = (row >= 0 && w < mw) ? p.rows.mask[(long long)row * kMaskWords + w] : 0u;
+    }
+    __syncthreads();
+
+    // Q fragments (A operand), 8 k-steps over head_dim
+    uint32_t qa[KS][4];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        qa[kk][0] = *reinterpret_cast<const uint32_t*>(Qs + g * kStride + kk * 16 + 2 * t);
+        qa[kk][1] = *reinterpret_cast<const uint32_t*>(Qs + (g + 8) * kStride + kk * 16 + 2 * t);
+        qa[kk][2] = *reinterpret_cast<const uint32_t*>(Qs + g * kStride + kk * 16 + 8 + 2 * t);
+        qa[kk][3] = *reinterpret_cast<const uint32_t*>(Qs + (g + 8) * kStride + kk * 16 + 8 + 2 * t);
+    }
+    const bool live0 = s_row[g] >= 0, live1 = s_row[g + 8] >= 0;
+
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
+
+    bf16* Ks = KVs + warp * 2 * kTile * kStride;
+    bf16* Vs = Ks + kTile * kStride;
+    const long long slot_base = ((long long)(slot < 0 ? 0 : slot) * p.KV + kvh) * p.cap;
+    const int wk0 = k0 + warp * kWarpKeys;
+    const int wk1 = min(total, wk0 + kWarpKeys);
+    for (int kb = wk0; kb < wk1; kb += kTile) {
+        const int nk = min(kTile, wk1 - kb);
+        // ---- stage 32 keys of K and V (16B chunks), zero-fill past nk
+#pragma unroll 4
+        for (int c = lane; c < kTile * (kHD / 8); c += 32) {
+            const int j = c / (kHD / 8), w = c % (kHD / 8);
+            const bool ok = j < nk;
+            const int v = kb + j;
+            const long long ci = ok ? (v < lc ? v : tail0 + (v - lc)) : 0;
+            const long long off = (slot_base + ci) * kHD + w * 8;
+            cp_async16(Ks + j * kStride + w * 8, p.kc + off, ok);
+            cp_async16(Vs + j * kStride + w * 8, p.vc + off, ok);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        // ---- S = Q K^T  (16 x 32)
+        float s[4][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) {
+                const bf16* kr = Ks + (nt * 8 + g) * kStride + kk * 16 + 2 * t;
+                mma16816(s[nt], qa[kk], *reinterpret_cast<const uint32_t*>(kr),
+                         *reinterpret_cast<const uint32_t*>(kr + 8));
+            }
+        }
+        // ---- scale + visibility (prefix, or tree-mask bit of the query row)
+        float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int col = nt * 8 + 2 * t + (e & 1);
+                const int r = e < 2 ? g : g + 8;
+                const int v = kb + col;
+                bool vis = col < nk && (e < 2 ? live0 : live1);
+                if (vis && v >= lc) {
+                    const int tt = v - lc;
+                    vis = (Ms[r * kMaskWords + (tt >> 5)] >> (tt & 31)) & 1u;
+                }
+                const float x = vis ? s[nt][e] * p.scale_log2 : -CUDART_INF_F;
+                s[nt][e] = x;
+                if (e < 2) mx0 = fmaxf(mx0, x);
+                else mx1 = fmaxf(mx1, x);
+            }
+        }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
+        const float c0 = nm0 == -CUDART_INF_F ? 1.f : exp2f(m0 - nm0);
+        const float c1 = nm1 == -CUDART_INF_F ? 1.f : exp2f(m1 - nm1);
+        m0 = nm0;
+        m1 = nm1;
+        l0 *= c0;
+        l1 *= c1;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            o[n][0] *= c0;
+            o[n][1] *= c0;
+            o[n][2] *= c1;
+            o[n][3] *= c1;
+        }
+        uint32_t pa[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            const float p0 = m0 == -CUDART_INF_F ? 0.f : exp2f(s[nt][0] - m0);
+            const float p1 = m0 == -CUDART_INF_F ? 0.f : exp2f(s[nt][1] - m0);
+            const float p2 = m1 == -CUDART_INF_F ? 0.f : exp2f(s[nt][2] - m1);
+            const float p3 = m1 == -CUDART_INF_F ? 0.f : exp2f(s[nt][3] - m1);
+            l0 += p0 + p1;
+            l1 += p2 + p3;
+            const int j = nt >> 1;
+            if ((nt & 1) == 0) {
+                pa[j][0] = pack_bf16(p0, p1);
+                pa[j][1] = pack_bf16(p2, p3);
+            } else {
+                pa[j][2] = pack_bf16(p0, p1);
+                pa[j][3] = pack_bf16(p2, p3);
+            }
+        }
+        // ---- O += P V  (k = 32 keys in two k16 steps, 16 n-tiles of head dims)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int nd = 0; nd < NT; nd += 2) {
+                // matrices: (keys 16j..+7, dims nd*8), (keys 16j+8.., nd*8), (.., (nd+1)*8) x2
+                const int mi = lane >> 3, r = lane & 7;
+                const int key = 16 * j + (mi & 1) * 8 + r;
+                const int dim = (nd + (mi >> 1)) * 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_trans(b0, b1, b2, b3, Vs + key * kStride + dim);
+                mma16816(o[nd], pa[j], b0, b1);
+                mma16816(o[nd + 1], pa[j], b2, b3);
+            }
+        }
+        __syncwarp();
+    }
+    // quad-reduce l
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+
+    // ---- merge the 4 warps' partials (fixed order) in shared memory
+    __syncthreads();
+    float* wm = red;                      // [4][16]
+    float* wl = wm + 4 * kQV;             // [4][16]
+    float* wo = wl + 4 * kQV;             // [4][16][kHD]
+    if (t == 0) {
+        wm[warp * kQV + g] = m0;
+        wm[warp * kQV + g + 8] = m1;
+        wl[warp * kQV + g] = l0;
+        wl[warp * kQV + g + 8] = l1;
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        float* r0 = wo + (warp * kQV + g) * kHD + n * 8 + 2 * t;
+        float* r1 = wo + (warp * kQV + g + 8) * kHD + n * 8 + 2 * t;
+        r0[0] = o[n][0];
+        r0[1] = o[n][1];
+        r1[0] = o[n][2];
+        r1[1] = o[n][3];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kQV * kHD; c += blockDim.x) {
+        const int q = c / kHD, e = c % kHD;
+        const int gqv = qv0 + q;
+        if (gqv >= nqv) continue;
+        float M = -CUDART_INF_F;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w * kQV + q]);
+        float L = 0.f, O = 0.f;
+        if (M != -CUDART_INF_F)
+            for (int w = 0; w < 4; ++w) {
+                const float sc = exp2f(wm[w * kQV + q] - M);
+                L += wl[w * kQV + q] * sc;
+                O += wo[(w * kQV + q) * kHD + e] * sc;
+            }
+        const long long pidx = ((long long)(grp * p.max_splits + split) * p.qv_cap + gqv) * p.KV + kvh;
+        p.ws_o[pidx * kHD + e] = O;
+        if (e == 0) {
+            p.ws_m[pidx] = M;
+            p.ws_l[pidx] = L;
+        }
+    }
+}
+
+template <int kHD>
+size_t attention_mma_smem() {
+    constexpr int kStride = kHD + 8;
+    const size_t kv = sizeof(bf16) * 4 * 2 * kTile * kStride;
+    const size_t merge = sizeof(float) * (4 * kQV * 2 + 4 * kQV * kHD);
+    return sizeof(bf16) * kQV * kStride + (kv > merge ? kv : merge) + sizeof(uint32_t) * kQV * kMaskWords;
+}
+
+template <int kHD>
+void launch_attention_mma_t(const AttnParams& p, cudaStream_t st) {
+    static bool attr = false;
+    const size_t smem = attention_mma_smem<kHD>();
+    if (!attr) {
+        cudaFuncSetAttribute(k_attention_mma<kHD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int G = p.H / p.KV;
+    const int nqv = p.rows_per_req * G;
+    dim3 grid((nqv + kQV - 1) / kQV, p.KV, p.n_groups * p.max_splits);
+    k_attention_mma<kHD><<<grid, 128, smem, st>>>(p);
+}
+
+int attention_mma_split() { return kSplit; }
+
+void launch_attention_mma(const AttnParams& p, cudaStream_t st) {
+    if (p.hd == 128)
+        launch_attention_mma_t<128>(p, st);
+    else
+        launch_attention_mma_t<64>(p, st);
+}
+
+}  // namespace tlt

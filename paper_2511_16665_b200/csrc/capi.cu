@@ -269,7 +269,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         E.prefill(n, slots.data(), prompt_lens, prompts);
         std::vector<int> running(n, 1), glen(n, 0);
         out->sd_steps = out->plain_steps = out->verify_events = out->accepted_total = out->emitted_total = 0;
-        out->device_ms = 0.0;
+        out->device_ms = E.last_prefill_ms;
         const long long launches0 = E.launches;
         int maxD = 1;
         if (cfg->use_mab)

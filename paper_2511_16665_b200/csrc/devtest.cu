@@ -31,3 +31,42 @@ extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, 
         return -1;
     }
 }
+
+// Average device time of one GEMM launch (incl. its split-K reduce), `iters`
+// back-to-back launches on a private stream bracketed by CUDA events.
+extern "C" TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
+                                         void* y_bf16, float* ws, long long ws_elems, int iters, float* avg_ms) {
+    try {
+        GemmPlan g = plan_gemm(m, n, k);
+        CUtensorMap tw = make_tmap_bf16(w, n, k, k, 128);
+        CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.bn);
+        EpiParams ep{};
+        ep.kind = kind;
+        ep.n_out = n;
+        ep.m_tok = m;
+        ep.out_f32 = y_f32;
+        ep.ld_f32 = kind == EPI_SWIGLU ? n / 2 : n;
+        ep.out_bf16 = static_cast<__nv_bfloat16*>(y_bf16);
+        ep.ld_bf16 = kind == EPI_SWIGLU ? n / 2 : n;
+        cudaStream_t st;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        cudaEvent_t e0, e1;
+        CUDA_CHECK(cudaEventCreate(&e0));
+        CUDA_CHECK(cudaEventCreate(&e1));
+        for (int i = 0; i < 3; ++i) launch_gemm(g, tw, tx, ep, ws, static_cast<size_t>(ws_elems), st);
+        CUDA_CHECK(cudaEventRecord(e0, st));
+        for (int i = 0; i < iters; ++i) launch_gemm(g, tw, tx, ep, ws, static_cast<size_t>(ws_elems), st);
+        CUDA_CHECK(cudaEventRecord(e1, st));
+        CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        *avg_ms = ms / iters;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+        return g.splits;
+    } catch (const std::exception& e) {
+        tlt_set_last_error(e.what());
+        return -1;
+    }
+}

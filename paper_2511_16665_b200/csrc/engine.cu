@@ -96,10 +96,11 @@ Engine::Engine(const tlt_model_cfg& c, const tlt_init_cfg& init, int device) : c
     CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     CUDA_CHECK(cudaEventCreate(&ev0_));
     CUDA_CHECK(cudaEventCreate(&ev1_));
-    ip_ = tlt_init_params{init.seed, init.layer_scale, init.lm_gain, init.lm_noise, init.fc_noise,
+    ip_ = tlt_init_params{init.seed, init.layer_scale, init.lm_gain, init.lm_alt, init.lm_noise, init.fc_noise,
                           c.vocab,   c.hidden,         c.heads,      c.kv_heads,    c.head_dim, c.ffn};
     alloc_weights(init);
     alloc_state();
+    attn_impl_ = env_int("TLT_ATTN", 1);
     CUDA_CHECK(cudaStreamSynchronize(st_));
 }
 
@@ -309,7 +310,8 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
     p.hd = cfg.head_dim;
     p.cap = cache_cap;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)cfg.head_dim));
-    p.chunk = 512;
+    p.impl = attn_impl_;
+    p.chunk = p.impl == 1 ? attention_mma_split() : 512;
     p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
     p.qv_cap = rpr * (cfg.heads / cfg.kv_heads);
     const size_t need = (size_t)ngroups * p.max_splits * p.qv_cap * cfg.kv_heads;
@@ -466,6 +468,7 @@ void Engine::prefill(int b, const int32_t* slots, const int32_t* lens, const int
         if (lens[i] + 1 > cfg.max_ctx) throw ConfigErr("lens", "prompt exceeds max_ctx");
         off[i + 1] = off[i] + lens[i];
     }
+    CUDA_CHECK(cudaEventRecord(ev0_, st_));
     // token histories
     for (int i = 0; i < b; ++i)
         CUDA_CHECK(cudaMemcpyAsync(tok_hist_ + (size_t)slots[i] * cap_, tokens + off[i], sizeof(int32_t) * lens[i],
@@ -508,7 +511,9 @@ void Engine::prefill(int b, const int32_t* slots, const int32_t* lens, const int
         }
         i0 = i1;
     }
-    CUDA_CHECK(cudaStreamSynchronize(st_));
+    CUDA_CHECK(cudaEventRecord(ev1_, st_));
+    CUDA_CHECK(cudaEventSynchronize(ev1_));
+    CUDA_CHECK(cudaEventElapsedTime(&last_prefill_ms, ev0_, ev1_));
     for (int i = 0; i < b; ++i) {
         lt_[slots[i]] = lens[i] - 1;
         ld_[slots[i]] = lens[i] - 1;

@@ -69,7 +69,8 @@ public:
     std::vector<float> dbg_ar_logits;            // [b*V]
 
     const tlt_model_cfg cfg;
-    long long launches = 0;  // kernel launches issued (graph replays count their nodes)
+    long long launches = 0;
+    float last_prefill_ms = 0.f;  // device time of the last prefill (CUDA events)  // kernel launches issued (graph replays count their nodes)
 
 private:
     void alloc_weights(const tlt_init_cfg& init);
@@ -146,6 +147,7 @@ private:
     // host mirrors
     std::vector<int> lt_, ld_, live_;
     bool debug_ = false;
+    int attn_impl_ = 1;  // TLT_ATTN=0 selects the CUDA-core attention (cross-check)
     // caches
     std::unordered_map<std::string, CUtensorMap> tmaps_;
     std::map<std::tuple<int, int, int, int, int>, std::pair<cudaGraphExec_t, long long>> graphs_;

@@ -20,7 +20,10 @@ struct AttnParams {
     float scale_log2;
     int chunk, max_splits, qv_cap;
     float *ws_m, *ws_l, *ws_o;
+    int impl;  // 0: CUDA-core reference kernel, 1: tensor-core flash-decode (attn_mma.cu)
 };
+void launch_attention_mma(const AttnParams& p, cudaStream_t st);
+int attention_mma_split();
 
 struct TreeParams {
     const StepIn* step;

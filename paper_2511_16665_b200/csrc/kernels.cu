@@ -291,13 +291,17 @@ void launch_attention(const AttnParams& p, cudaStream_t st) {
     dim3 grid((nqv + kAttnQV - 1) / kAttnQV, p.KV, p.n_groups * p.max_splits);
     const long long warps = (long long)p.n_groups * nqv * p.KV;
     const int cblocks = (int)((warps * 32 + 255) / 256);
-    if (p.hd == 128) {
+    if (p.impl == 1) {
+        launch_attention_mma(p, st);  // tensor-core path (attn_mma.cu), chunk = 256 keys
+    } else if (p.hd == 128) {
         k_attention<128><<<grid, 128, 0, st>>>(p);
-        k_attn_combine<128><<<cblocks, 256, 0, st>>>(p);
-    } else if (p.hd == 64) {
+    } else {
         k_attention<64><<<grid, 128, 0, st>>>(p);
-        k_attn_combine<64><<<cblocks, 256, 0, st>>>(p);
     }
+    if (p.hd == 128)
+        k_attn_combine<128><<<cblocks, 256, 0, st>>>(p);
+    else
+        k_attn_combine<64><<<cblocks, 256, 0, st>>>(p);
 }
 
 // ------------------------------------------------------- row top-k / argmax

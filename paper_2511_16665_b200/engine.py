@@ -60,7 +60,7 @@ class ModelCfg(C.Structure):
 
 
 class InitCfg(C.Structure):
-    _fields_ = [("seed", C.c_uint64), ("layer_scale", C.c_float), ("lm_gain", C.c_float), ("lm_noise", C.c_float),
+    _fields_ = [("seed", C.c_uint64), ("layer_scale", C.c_float), ("lm_gain", C.c_float), ("lm_alt", C.c_float), ("lm_noise", C.c_float),
                 ("fc_noise", C.c_float)]
 
 
@@ -109,9 +109,9 @@ MODELS = {
 }
 # Structure knob per model: mean accept length in a realistic band.
 INITS = {
-    "tiny": dict(seed=42, layer_scale=1.0, lm_gain=4.0, lm_noise=2.0, fc_noise=0.05),
-    "qwen2.5-7b": dict(seed=42, layer_scale=0.3, lm_gain=4.0, lm_noise=2.0, fc_noise=0.05),
-    "qwen2.5-32b": dict(seed=42, layer_scale=0.3, lm_gain=4.0, lm_noise=2.0, fc_noise=0.05),
+    "tiny": dict(seed=42, layer_scale=1.0, lm_gain=10.0, lm_alt=0.9, lm_noise=1.0, fc_noise=0.05),
+    "qwen2.5-7b": dict(seed=42, layer_scale=1.0, lm_gain=13.0, lm_alt=0.9, lm_noise=1.0, fc_noise=0.05),
+    "qwen2.5-32b": dict(seed=42, layer_scale=0.3, lm_gain=13.0, lm_alt=0.9, lm_noise=1.0, fc_noise=0.05),
 }
 
 
@@ -138,7 +138,7 @@ class Engine:
         self.init = ini
         self.cfg = ModelCfg(m["vocab"], m["hidden"], m["layers"], m["heads"], m["kv_heads"], m["head_dim"], m["ffn"],
                             m["qkv_bias"], m["rope_theta"], m["rms_eps"], max_slots, max_ctx)
-        self.icfg = InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_noise"], ini["fc_noise"])
+        self.icfg = InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"], ini["fc_noise"])
         self.L = lib()
         h = C.c_void_p()
         _check(self.L.tlt_engine_create(C.byref(self.cfg), C.byref(self.icfg), device, C.byref(h)))
