@@ -221,7 +221,7 @@ void Engine::alloc_state() {
     logits_ = dmalloc<float>((size_t)R_ * V);
     ws_elems_ = (size_t)env_int("TLT_GEMM_WS_MFLOATS", 64) << 20;
     ws_ = dmalloc<float>(ws_elems_);
-    aws_elems_ = (size_t)env_int("TLT_ATTN_WS_MFLOATS", 48) << 20;
+    aws_elems_ = (size_t)env_int("TLT_ATTN_WS_MFLOATS", 192) << 20;
     aws_m_ = dmalloc<float>(aws_elems_ / 32);
     aws_l_ = dmalloc<float>(aws_elems_ / 32);
     aws_o_ = dmalloc<float>(aws_elems_);
@@ -239,6 +239,7 @@ void Engine::alloc_state() {
     tk_M_ = dmalloc<float>(R_);
     tk_S_ = dmalloc<float>(R_);
     argmax_ = dmalloc<int>(R_);
+    topk_part_ = dmalloc<float>((size_t)((V + 127) / 128) * R_ * (2 + 2 * kEpiTopkMax));
     arena_ = dmalloc<Cand>((size_t)S * arena_cap_);
     arena_n_ = dmalloc<int>(S);
     kept_ = dmalloc<int>((size_t)S * kMaxT);
@@ -286,12 +287,44 @@ const CUtensorMap& Engine::tmap_act(const void* p, int rows, int cols, long long
 
 void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep_in) {
     GemmPlan g = plan_gemm(M, N, K);
+    if (ep_in.kind == EPI_TOPK) {  // the fused top-k epilogue needs whole-K accumulators
+        g.kb_per_split = g.kb_total;
+        g.splits = 1;
+    }
     const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.bn);
     EpiParams ep = ep_in;
     ep.n_out = N;
     ep.m_tok = M;
     launch_gemm(g, tmW, tx, ep, ws_, ws_elems_, st_);
     count_launch(g.splits > 1 ? 2 : 1);
+}
+
+// x_ += X W^T, then h_ = bf16(rmsnorm(x_) * norm_w) when norm_w != null. At
+// split-K shapes (long-tail M) the reduce, residual add and the next RMSNorm
+// are one kernel (k_reduce_resid_norm).
+void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w) {
+    const int d = cfg.hidden;
+    GemmPlan g = plan_gemm(M, d, K);
+    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.bn);
+    EpiParams e{};
+    e.n_out = d;
+    e.m_tok = M;
+    if (g.splits > 1) {
+        e.kind = EPI_PARTIAL;
+        launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
+        launch_reduce_resid_norm(ws_, (long long)M * d, g.splits, M, d, x_, norm_w, cfg.rms_eps, h_, st_);
+        count_launch(2);
+    } else {
+        e.kind = EPI_RESID_ADD;
+        e.out_f32 = x_;
+        e.ld_f32 = d;
+        launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
+        count_launch();
+        if (norm_w) {
+            launch_rmsnorm(x_, M, d, norm_w, cfg.rms_eps, h_, st_);
+            count_launch();
+        }
+    }
 }
 
 void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int rpr,
@@ -326,11 +359,13 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
 
 // One decoder layer over R rows (residual x_ in place).
 void Engine::layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, const Rows& rw, const Groups& gp,
-                           int R, int rpr, int ngroups, int max_keys) {
+                           int R, int rpr, int ngroups, int max_keys, bool h_ready, const bf16* next_norm) {
     const int d = cfg.hidden, hd = cfg.head_dim;
     const int nq = cfg.heads * hd, nkv = cfg.kv_heads * hd;
-    launch_rmsnorm(x_, R, d, w.attn_norm, cfg.rms_eps, h_, st_);
-    count_launch();
+    if (!h_ready) {
+        launch_rmsnorm(x_, R, d, w.attn_norm, cfg.rms_eps, h_, st_);
+        count_launch();
+    }
     EpiParams e{};
     e.kind = EPI_QKV;
     e.out_bf16 = q_;
@@ -350,28 +385,20 @@ void Engine::layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, c
     e.max_ctx = cache_cap;
     gemm(h_, R, d, d, w.tm_qkv, nq + 2 * nkv, e);
     attention(kc, vc, cache_cap, rw, gp, rpr, ngroups, max_keys);
-    EpiParams o{};
-    o.kind = EPI_RESID_ADD;
-    o.out_f32 = x_;
-    o.ld_f32 = d;
-    gemm(attn_, R, nq, nq, w.tm_o, d, o);
-    launch_rmsnorm(x_, R, d, w.mlp_norm, cfg.rms_eps, h_, st_);
-    count_launch();
+    gemm_resid_norm(attn_, R, nq, nq, w.tm_o, w.mlp_norm);  // x += o W_o^T; h = norm(x)
     EpiParams s{};
     s.kind = EPI_SWIGLU;
     s.out_bf16 = act_;
     s.ld_bf16 = cfg.ffn;
     gemm(h_, R, d, d, w.tm_gu, 2 * cfg.ffn, s);
-    EpiParams dn{};
-    dn.kind = EPI_RESID_ADD;
-    dn.out_f32 = x_;
-    dn.ld_f32 = d;
-    gemm(act_, R, cfg.ffn, cfg.ffn, w.tm_down, d, dn);
+    gemm_resid_norm(act_, R, cfg.ffn, cfg.ffn, w.tm_down, next_norm);  // x += a W_down^T; h = next norm
 }
 
-void Engine::lm_head(const float* x, int n, float* logits) {
-    launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
-    count_launch();
+void Engine::lm_head(const float* x, int n, float* logits, bool h_ready) {
+    if (!h_ready) {
+        launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
+        count_launch();
+    }
     EpiParams e{};
     e.kind = EPI_F32;
     e.out_f32 = logits;
@@ -379,21 +406,50 @@ void Engine::lm_head(const float* x, int n, float* logits) {
     gemm(h_, n, cfg.hidden, cfg.hidden, tm_lm_, cfg.vocab, e);
 }
 
+// Final norm + LM head with the fused top-k epilogue (EPI_TOPK) and the
+// per-row merge: writes tk_tok_/tk_logit_ [n][k], tk_M_, tk_S_. The fp32
+// logits are only materialized for the parity exports (want_logits).
+void Engine::lm_topk(const float* x, int n, int k, const int* live, bool want_logits, bool h_ready) {
+    if (!h_ready) {
+        launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
+        count_launch();
+    }
+    EpiParams e{};
+    e.kind = EPI_TOPK;
+    e.out_f32 = topk_part_;
+    e.topk_k = k;
+    gemm(h_, n, cfg.hidden, cfg.hidden, tm_lm_, cfg.vocab, e);
+    const int n_tiles = (cfg.vocab + 127) / 128;
+    launch_topk_merge(topk_part_, n_tiles, n, k, live, tk_tok_, tk_logit_, tk_M_, tk_S_, st_);
+    count_launch();
+    if (want_logits) {
+        EpiParams f{};
+        f.kind = EPI_F32;
+        f.out_f32 = logits_;
+        f.ld_f32 = cfg.vocab;
+        gemm(h_, n, cfg.hidden, cfg.hidden, tm_lm_, cfg.vocab, f);
+    }
+}
+
 void Engine::target_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
                             float* logits, bf16* feat) {
     if (R > R_) throw ConfigErr("rows", "forward exceeds TLT_MAX_ROWS");
     launch_embed(rw, R, embed_, cfg.hidden, x_, st_);
     count_launch();
-    for (int l = 0; l < cfg.layers; ++l) layer_forward(layers_[l], kc_[l], vc_[l], cap_, rw, gp, R, rpr, ngroups, max_keys);
+    // each layer's down-proj epilogue normalizes for the next layer (the last
+    // one with the final norm, leaving h_ ready for the LM head)
+    for (int l = 0; l < cfg.layers; ++l)
+        layer_forward(layers_[l], kc_[l], vc_[l], cap_, rw, gp, R, rpr, ngroups, max_keys, l > 0,
+                      l + 1 < cfg.layers ? layers_[l + 1].attn_norm : final_norm_);
     if (feat) {
         launch_to_bf16(x_, (long long)R * cfg.hidden, feat, st_);
         count_launch();
     }
-    if (logits) lm_head(x_, R, logits);
+    if (logits) lm_head(x_, R, logits, true);
 }
 
 void Engine::drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
-                             const int* gather, int n_lm, float* logits, bf16* dfeat_out) {
+                             const int* gather, int n_lm, int k, const int* live, bool want_logits, bf16* dfeat_out) {
     if (R > R_) throw ConfigErr("rows", "drafter forward exceeds TLT_MAX_ROWS");
     const int d = cfg.hidden;
     launch_draft_in(rw, R, embed_, d, feat_hist_, dfeat_, x2_, st_);
@@ -403,18 +459,19 @@ void Engine::drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, i
     e.out_f32 = x_;
     e.ld_f32 = d;
     gemm(x2_, R, 2 * d, 2 * d, tm_fc_, d, e);
-    layer_forward(drafter_, dkc_, dvc_, dcap_, rw, gp, R, rpr, ngroups, max_keys);
+    layer_forward(drafter_, dkc_, dvc_, dcap_, rw, gp, R, rpr, ngroups, max_keys, false,
+                  (k > 0 && !gather) ? final_norm_ : nullptr);
     if (dfeat_out) {
         launch_to_bf16(x_, (long long)R * d, dfeat_out, st_);
         count_launch();
     }
-    if (logits) {
+    if (k > 0) {
         if (gather) {
             launch_gather_rows(x_, gather, n_lm, d, xg_, st_);
             count_launch();
-            lm_head(xg_, n_lm, logits);
+            lm_topk(xg_, n_lm, k, live, want_logits, false);
         } else {
-            lm_head(x_, n_lm, logits);
+            lm_topk(x_, n_lm, k, live, want_logits, true);
         }
     }
 }
@@ -507,7 +564,7 @@ void Engine::prefill(int b, const int32_t* slots, const int32_t* lens, const int
             upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, gs, glc, gt0, gnt);
             target_forward(prows_, pg_, R, chunk, nreq, c0 + chunk, nullptr, feat_);
             scatter_features(prows_, R, feat_);
-            drafter_forward(prows_, pg_, R, chunk, nreq, c0 + chunk, nullptr, 0, nullptr, nullptr);
+            drafter_forward(prows_, pg_, R, chunk, nreq, c0 + chunk, nullptr, 0, 0, nullptr, false, nullptr);
         }
         i0 = i1;
     }
@@ -552,7 +609,7 @@ void Engine::catchup_drafter(int b, const int32_t* slots) {
                 for (int t = 0; t <= j; ++t) mask[(size_t)j * kMaskWords + (t >> 5)] |= 1u << (t & 31);
             }
             upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, {s}, {c0}, {c0}, {n});
-            drafter_forward(prows_, pg_, chunk, chunk, 1, c0 + chunk, nullptr, 0, nullptr, nullptr);
+            drafter_forward(prows_, pg_, chunk, chunk, 1, c0 + chunk, nullptr, 0, 0, nullptr, false, nullptr);
             ld_[s] += n;
         }
     }
@@ -624,11 +681,8 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
         const int R = b_hi * Fd[lv];
         const Rows rw = sub(drows_, base[lv]);
         const int n_lm = lv == 1 ? b_hi : R;
-        drafter_forward(rw, dg_[lv], R, Fd[lv], b_hi, max_keys_d, lv == 1 ? root_row_ : nullptr, n_lm, logits_,
-                        dfeat_ + (size_t)base[lv] * d);
-        launch_row_topk(logits_, n_lm, V, lv == 1 ? dg_[1].slot : rw.slot, k, 1, tk_tok_, tk_logit_, tk_M_, tk_S_,
-                        st_);
-        count_launch();
+        drafter_forward(rw, dg_[lv], R, Fd[lv], b_hi, max_keys_d, lv == 1 ? root_row_ : nullptr, n_lm, k,
+                        lv == 1 ? dg_[1].slot : rw.slot, dbg, dfeat_ + (size_t)base[lv] * d);
         if (dbg) {
             // full fp64 rows of every live expansion (parity export)
             launch_row_probs(logits_, n_lm, V, tk_M_, tk_S_, dbg_probs_, st_);
@@ -671,7 +725,8 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
     count_launch();
     // target verify over root + tree
     const int T1 = T + 1, RV = b_hi * T1;
-    target_forward(vrows_, vg_, RV, T1, b_hi, max_keys_t, logits_, feat_);
+    target_forward(vrows_, vg_, RV, T1, b_hi, max_keys_t, nullptr, feat_);
+    lm_topk(x_, RV, 1, vrows_.slot, dbg, true);  // argmax per verify row (fused epilogue + merge)
     if (dbg) {
         dbg_vlogits.assign(b_real, {});
         std::vector<float> lg((size_t)RV * V);
@@ -680,8 +735,6 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
         for (int i = 0; i < b_real; ++i)
             dbg_vlogits[i].assign(lg.begin() + (size_t)i * T1 * V, lg.begin() + (size_t)(i + 1) * T1 * V);
     }
-    launch_row_topk(logits_, RV, V, vrows_.slot, 1, 0, argmax_, tk_logit_, nullptr, nullptr, st_);
-    count_launch();
     AcceptParams ap{};
     ap.step = d_step_;
     ap.b = b_hi;
@@ -691,7 +744,7 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
     ap.tree_tok = tree_tok_;
     ap.tree_par = tree_par_;
     ap.tree_n = tree_n_;
-    ap.argmax = argmax_;
+    ap.argmax = tk_tok_;  // top-1 of each verify row
     ap.acc_nodes = acc_nodes_;
     ap.acc_tok = acc_tok_;
     ap.acc_len = acc_len_;
@@ -851,10 +904,9 @@ void Engine::ar_device_sequence(int b_hi) {
     CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
     launch_rows_ar(d_step_, b_hi, b_hi, prows_, pg_, tok_hist_, cap_, st_);
     count_launch();
-    target_forward(prows_, pg_, b_hi, 1, b_hi, cap_, logits_, feat_);
-    launch_row_topk(logits_, b_hi, cfg.vocab, prows_.slot, 1, 0, argmax_, tk_logit_, nullptr, nullptr, st_);
-    count_launch();
-    launch_commit_ar(d_step_, b_hi, argmax_, feat_, cfg.hidden, tok_hist_, feat_hist_, cap_, ar_tok_, st_);
+    target_forward(prows_, pg_, b_hi, 1, b_hi, cap_, nullptr, feat_);
+    lm_topk(x_, b_hi, 1, prows_.slot, debug_, true);
+    launch_commit_ar(d_step_, b_hi, tk_tok_, feat_, cfg.hidden, tok_hist_, feat_hist_, cap_, ar_tok_, st_);
     count_launch();
     CUDA_CHECK(cudaMemcpyAsync(ho_.ar_tok, ar_tok_, sizeof(int) * b_hi, cudaMemcpyDeviceToHost, st_));
 }

@@ -78,14 +78,17 @@ private:
     const CUtensorMap& tmap_act(const void* p, int rows, int cols, long long ld, int box);
     void gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep);
     void layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int R,
-                       int rpr, int ngroups, int max_keys);
+                       int rpr, int ngroups, int max_keys, bool h_ready, const bf16* next_norm);
+    void gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w);
     void attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int rpr,
                    int ngroups, int max_keys);
-    void lm_head(const float* x, int n, float* logits);
+    void lm_head(const float* x, int n, float* logits, bool h_ready = false);
     void target_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
                         float* logits, bf16* feat);
     void drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
-                         const int* gather, int n_lm, float* logits, bf16* dfeat_out);
+                         const int* gather, int n_lm, int k, const int* live, bool want_logits, bf16* dfeat_out);
+    void lm_topk(const float* x, int n, int k, const int* live, bool want_logits, bool h_ready = false);
+    float* topk_part_ = nullptr;  // EPI_TOPK partials [vocab tiles][R][2 + 2k]
     void scatter_features(const Rows& rw, int R, const bf16* feat);
     void catchup_drafter(int b, const int32_t* slots);
     void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real);

@@ -93,9 +93,13 @@ void launch_gather_rows(const float* x, const int* src, int n, int d, float* out
 void launch_to_bf16(const float* x, long long n, __nv_bfloat16* out, cudaStream_t st);
 void launch_rmsnorm(const float* x, int R, int d, const __nv_bfloat16* g, float eps, __nv_bfloat16* out,
                     cudaStream_t st);
+void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int R, int d, float* x,
+                              const __nv_bfloat16* g, float eps, __nv_bfloat16* out, cudaStream_t st);
 void launch_attention(const AttnParams& p, cudaStream_t st);
 void launch_row_topk(const float* logits, int R, int V, const int* live, int k, int need_sum, int* out_tok,
                      float* out_logit, float* out_M, float* out_S, cudaStream_t st);
+void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,
+                       float* out_M, float* out_S, cudaStream_t st);
 void launch_row_probs(const float* logits, int R, int V, const float* M, const float* S, double* out,
                       cudaStream_t st);
 void launch_rows_level1(const StepIn* st, int b, int b_hi, int D1, const Rows& rows, const Groups& g, int* root_row,

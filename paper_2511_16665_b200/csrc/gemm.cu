@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <math_constants.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <mutex>
@@ -19,6 +21,97 @@ namespace tlt {
 constexpr int kBlockM = 128;  // weight rows per tile (MMA M)
 constexpr int kBlockK = 64;   // 64 bf16 = one 128-byte swizzle row
 constexpr int kABytes = kBlockM * kBlockK * 2;
+
+// LM-head epilogue (EPI_TOPK) for one 128-vocab x bn-token accumulator tile.
+// Per 16-token chunk the 4 epilogue warps transpose the accumulators through
+// shared memory; then 8 threads per token scan 16 vocab rows each (local max,
+// sum-exp, sorted top-K by (logit desc, id asc)) and merge with a 3-step
+// butterfly inside the warp. The merge is symmetric (commutative adds, strict
+// total order), so all 8 lanes hold identical results and the output is
+// deterministic. One partial (M, S, K values, K ids) per (tile, token).
+template <int KM>
+__device__ __forceinline__ void topk_insert(float (&v)[KM], int (&id)[KM], float x, int ix) {
+    if (!(x > v[KM - 1] || (x == v[KM - 1] && ix < id[KM - 1]))) return;
+    int p = KM - 1;
+#pragma unroll
+    for (int s = KM - 1; s > 0; --s) {
+        if (p == s && (x > v[s - 1] || (x == v[s - 1] && ix < id[s - 1]))) {
+            v[s] = v[s - 1];
+            id[s] = id[s - 1];
+            p = s - 1;
+        }
+    }
+    v[p] = x;
+    id[p] = ix;
+}
+
+template <int KM>
+__device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem, int q, int lane, int n0, int t0,
+                                              int bn, float* tr) {
+    const int K = ep.topk_k;
+    const int W = 2 + 2 * K;
+    const int ep_tid = threadIdx.x - 64;  // 0..127
+    const int col = ep_tid >> 3, part = ep_tid & 7;
+    for (int c = 0; c < bn; c += 16) {
+        if (t0 + c >= ep.m_tok) break;
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tr[j * 128 + q * 32 + lane] = v[j];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        float m = -CUDART_INF_F, s = 0.f;
+        float lv[KM];
+        int li[KM];
+#pragma unroll
+        for (int r = 0; r < KM; ++r) {
+            lv[r] = -CUDART_INF_F;
+            li[r] = 0x7fffffff;
+        }
+        const float* src = tr + col * 128 + part * 16;
+        float xs[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int id = n0 + part * 16 + i;
+            xs[i] = id < ep.n_out ? src[i] : -CUDART_INF_F;
+            m = fmaxf(m, xs[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (xs[i] != -CUDART_INF_F) s += __expf(xs[i] - m);
+            topk_insert<KM>(lv, li, xs[i], n0 + part * 16 + i);
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const float om = __shfl_xor_sync(0xffffffffu, m, o);
+            const float os = __shfl_xor_sync(0xffffffffu, s, o);
+            const float nm = fmaxf(m, om);
+            const float a = m == -CUDART_INF_F ? 0.f : s * __expf(m - nm);
+            const float b = om == -CUDART_INF_F ? 0.f : os * __expf(om - nm);
+            s = a + b;
+            m = nm;
+            float ov[KM];
+            int oi[KM];
+#pragma unroll
+            for (int r = 0; r < KM; ++r) {
+                ov[r] = __shfl_xor_sync(0xffffffffu, lv[r], o);
+                oi[r] = __shfl_xor_sync(0xffffffffu, li[r], o);
+            }
+#pragma unroll
+            for (int r = 0; r < KM; ++r) topk_insert<KM>(lv, li, ov[r], oi[r]);
+        }
+        const int tok = t0 + c + col;
+        if (part == 0 && tok < ep.m_tok) {
+            float* out = ep.out_f32 + ((long long)blockIdx.x * ep.m_tok + tok) * W;
+            out[0] = m;
+            out[1] = s;
+            for (int r = 0; r < K; ++r) {
+                out[2 + r] = lv[r];
+                out[2 + K + r] = __int_as_float(li[r]);
+            }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+}
 
 __global__ void __launch_bounds__(192, 1)
     k_gemm_swapab(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -106,6 +199,13 @@ __global__ void __launch_bounds__(192, 1)
         const int q = warp & 3;
         const int row = n0 + q * 32 + lane;
         const int n_even = row & ~1;
+        if (ep.kind == EPI_TOPK) {
+            float* tr = reinterpret_cast<float*>(tmem_holder + 4);  // [16 cols][128 vocab rows]
+            if (ep.topk_k <= 1)
+                epi_topk_tile<1>(ep, tmem, q, lane, n0, t0, bn, tr);
+            else
+                epi_topk_tile<kEpiTopkMax>(ep, tmem, q, lane, n0, t0, bn, tr);
+        } else
         for (int c = 0; c < bn; c += 16) {
             if (t0 + c >= ep.m_tok) break;
             float v[16];
@@ -196,9 +296,12 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     g.kb_total = (k + kBlockK - 1) / kBlockK;
     const int stage_bytes = kABytes + bn * kBlockK * 2;
     const int ctas_per_sm = bn <= 128 ? 2 : 1;
-    const int budget = ctas_per_sm == 2 ? 110 * 1024 : 200 * 1024;
+    // per-CTA budget incl. barriers, alignment slack and the EPI_TOPK merge
+    // scratch, so that 2 CTAs/SM really fit in the 228 KB SM carve-out
+    const int fixed = 1024 + 16 * 8 + 64 + 16 * 128 * 4;
+    const int budget = (ctas_per_sm == 2 ? 112 * 1024 : 220 * 1024) - fixed;
     g.stages = std::max(2, std::min(8, budget / stage_bytes));
-    g.smem = g.stages * stage_bytes + 2 * g.stages * 8 + 8 + 16 + 1024;
+    g.smem = g.stages * stage_bytes + fixed;
     g.tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
     const int tiles = g.n_wtiles * g.n_ttiles;
     const int slots = num_sms() * ctas_per_sm;
@@ -218,6 +321,16 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     }
     EpiParams ep = ep_in;
     dim3 grid(g.n_wtiles, g.n_ttiles, g.splits);
+    if (ep.kind == EPI_PARTIAL) {  // caller reduces (e.g. k_reduce_resid_norm)
+        ep.partial_stride = (long long)ep.m_tok * ep.n_out;
+        if ((size_t)(ep.partial_stride * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");
+        ep.out_f32 = workspace;
+        ep.ld_f32 = ep.n_out;
+        k_gemm_swapab<<<grid, 192, g.smem, st>>>(tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split, g.tmem_cols,
+                                                 ep);
+        CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     if (g.splits > 1) {
         const long long plane = (long long)ep.m_tok * ep.n_out;
         if ((size_t)(plane * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");

@@ -25,6 +25,7 @@ enum EpiKind : int {
     EPI_SWIGLU = 3,     // rows interleaved (gate, up): out_bf16[t][n/2] = bf16(silu(g) * u)
     EPI_QKV = 4,        // + bias, RoPE on q/k pairs, q -> out_bf16, k/v -> KV cache
     EPI_PARTIAL = 5,    // split-K partial: out_f32[z][t][n] = acc
+    EPI_TOPK = 6,       // LM head: per (128-vocab tile, token) max, sum-exp and top-k (logit desc, id asc)
 };
 
 struct EpiParams {
@@ -50,7 +51,10 @@ struct EpiParams {
     int head_dim;
     int n_kv;
     int max_ctx;
+    // EPI_TOPK: out_f32 = partials [n_wtiles][m_tok][2 + 2*topk_k] (m, s, vals[k], ids[k])
+    int topk_k;
 };
+constexpr int kEpiTopkMax = 8;
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
 

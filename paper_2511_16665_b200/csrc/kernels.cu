@@ -3,6 +3,7 @@
 // compaction + commit (K8), row-metadata builders. The GEMMs are in gemm.cu.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include "../../include/tlt_init.h"
@@ -101,6 +102,93 @@ __global__ void k_rmsnorm(const float* __restrict__ x, int d, const bf16* __rest
 }
 void launch_rmsnorm(const float* x, int R, int d, const bf16* g, float eps, bf16* out, cudaStream_t st) {
     k_rmsnorm<<<R, 256, 0, st>>>(x, d, g, eps, out);
+}
+
+// Split-K reduce + residual add + RMSNorm of the updated row, one CTA per
+// token row (the O-proj / down-proj epilogue at long-tail batch sizes):
+//   x[r] += sum_z ws[z][r]   (fixed z order);  h[r] = bf16(x[r] * inv_rms * g)
+// Replaces k_splitk_reduce + k_rmsnorm (one launch and one pass over x).
+// One 8-CTA thread-block cluster per token row: each CTA owns d/8 features
+// (so a single long-tail row still spreads over 8 SMs), the row's sum of
+// squares is combined through distributed shared memory in fixed rank order.
+constexpr int kNormCluster = 8;
+__global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
+    k_reduce_resid_norm(const float* __restrict__ ws, long long plane, int splits, int d, float* __restrict__ x,
+                        const bf16* __restrict__ g, float eps, bf16* __restrict__ out) {
+    __shared__ float red[32];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = (int)cluster.block_rank();
+    const int r = blockIdx.y;
+    const int per = (d + kNormCluster - 1) / kNormCluster;
+    const int i0 = crank * per, i1 = min(d, i0 + per);
+    float* xr = x + (long long)r * d;
+    const float* wr = ws + (long long)r * d;
+    float ss = 0.f;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        float v = 0.f;
+        for (int z = 0; z < splits; ++z) v += wr[z * plane + i];
+        const float nx = xr[i] + v;
+        xr[i] = nx;
+        ss += nx * nx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float v = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w];
+        red[16] = v;
+    }
+    cluster.sync();
+    if (threadIdx.x == 0) {
+        float tot = 0.f;
+        for (int c = 0; c < kNormCluster; ++c) tot += *cluster.map_shared_rank(&red[16], c);  // fixed order
+        red[17] = tot;
+    }
+    cluster.sync();  // remote reads done before any CTA of the cluster exits
+    if (!g) return;
+    const float inv = 1.0f / sqrtf(red[17] / (float)d + eps);
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+        out[(long long)r * d + i] = __float2bfloat16_rn(xr[i] * inv * __bfloat162float(g[i]));
+}
+
+// (single-CTA variant kept for reference / cross-checks)
+__global__ void k_reduce_resid_norm_1cta(const float* __restrict__ ws, long long plane, int splits, int d,
+                                         float* __restrict__ x, const bf16* __restrict__ g, float eps,
+                                         bf16* __restrict__ out) {
+    __shared__ float red[32];
+    const int r = blockIdx.x;
+    float* xr = x + (long long)r * d;
+    const float* wr = ws + (long long)r * d;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float v = 0.f;
+        for (int z = 0; z < splits; ++z) v += wr[z * plane + i];
+        const float nx = xr[i] + v;
+        xr[i] = nx;
+        ss += nx * nx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    if (!g) return;
+    const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+    for (int i = threadIdx.x; i < d; i += blockDim.x)
+        out[(long long)r * d + i] = __float2bfloat16_rn(xr[i] * inv * __bfloat162float(g[i]));
+}
+void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int R, int d, float* x, const bf16* g,
+                              float eps, bf16* out, cudaStream_t st) {
+    k_reduce_resid_norm<<<dim3(kNormCluster, R), 256, 0, st>>>(ws, plane, splits, d, x, g, eps, out);
 }
 
 // ----------------------------------------------------------- attention
@@ -405,6 +493,101 @@ void launch_row_topk(const float* logits, int R, int V, const int* live, int k, 
         k_row_topk<4><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
     else
         k_row_topk<8><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+}
+
+// Merge of the LM-head epilogue partials (EPI_TOPK): per token row, over the
+// 128-vocab tiles in fixed order: M = max m_t, S = sum s_t exp(m_t - M), and
+// top-k of the per-tile sorted candidate lists by (logit desc, id asc).
+template <int K>
+__global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ part, int n_tiles, int m_tok, int k,
+                                                    const int* __restrict__ live, int* __restrict__ out_tok,
+                                                    float* __restrict__ out_logit, float* __restrict__ out_M,
+                                                    float* __restrict__ out_S) {
+    __shared__ float sv[256][K];
+    __shared__ int si[256][K];
+    __shared__ float red[8];
+    __shared__ float sM;
+    const int r = blockIdx.x;
+    if (live && live[r] < 0) return;
+    const int W = 2 + 2 * k;
+    float m = -CUDART_INF_F;
+    TopK<K> t;
+    t.init();
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+        const float* pp = part + ((long long)i * m_tok + r) * W;
+        m = fmaxf(m, pp[0]);
+        for (int c = 0; c < k; ++c) t.push(pp[2 + c], __float_as_int(pp[2 + k + c]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = red[0];
+        for (int w = 1; w < 8; ++w) M = fmaxf(M, red[w]);
+        sM = M;
+    }
+    __syncthreads();
+    const float M = sM;
+    float s = 0.f;
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+        const float* pp = part + ((long long)i * m_tok + r) * W;
+        if (pp[0] != -CUDART_INF_F) s += pp[1] * __expf(pp[0] - M);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        sv[threadIdx.x][j] = t.v[j];
+        si[threadIdx.x][j] = t.id[j];
+    }
+    __syncthreads();
+    for (int stride = 1; stride < 256; stride <<= 1) {
+        if ((threadIdx.x % (2 * stride)) == 0) {
+            const int a = threadIdx.x, b = threadIdx.x + stride;
+            float mv[K];
+            int mi[K];
+            int ia = 0, ib = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const bool take_a = TopK<K>::better(sv[a][ia], si[a][ia], sv[b][ib], si[b][ib]);
+                mv[j] = take_a ? sv[a][ia] : sv[b][ib];
+                mi[j] = take_a ? si[a][ia] : si[b][ib];
+                if (take_a) ++ia; else ++ib;
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                sv[a][j] = mv[j];
+                si[a][j] = mi[j];
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < k) {
+        out_tok[(long long)r * k + threadIdx.x] = si[0][threadIdx.x];
+        out_logit[(long long)r * k + threadIdx.x] = sv[0][threadIdx.x];
+    }
+    if (threadIdx.x == 0) {
+        if (out_M) out_M[r] = M;
+        if (out_S) {
+            float tot = 0.f;
+            for (int w = 0; w < 8; ++w) tot += red[w];
+            out_S[r] = tot;
+        }
+    }
+}
+void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,
+                       float* out_M, float* out_S, cudaStream_t st) {
+    if (k <= 1)
+        k_topk_merge<1><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+    else if (k <= 2)
+        k_topk_merge<2><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+    else if (k <= 4)
+        k_topk_merge<4><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+    else
+        k_topk_merge<8><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
 }
 
 // full fp64 distribution of a row (parity/debug export): p = exp((double)(l-M))/S

@@ -1,0 +1,57 @@
+"""C1 on CPU: world_size-2 gloo all-gather of per-rank BEG-MAB records, applied
+in rank order to every replica. All replicas must end
+bit-identical; with one rank the merge reduces to the local beg_record
+sequence (beg_mab.hpp:111-134)."""
+import os
+import random
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ARMS = [(10, 8, 64), (6, 8, 64), (10, 8, 48), (6, 8, 48), (10, 8, 32), (6, 8, 32), (10, 8, 16), (6, 8, 16)]
+THR = [1, 2, 8, 16]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_16665_b200.engine import Mab, Rng
+    mab = Mab(ARMS, THR, 0.1, 20)
+    rng = Rng(1234, 0x53454C + rank)
+    g = random.Random(rank)
+    for step in range(40):
+        batch = g.choice([1, 3, 9, 20])
+        arm, s = mab.select(batch, rng)
+        lens = [g.randrange(0, s[0] + 1) for _ in range(batch)]
+        elapsed = 1.0 + g.random()
+        a_bar = sum(lens) / batch + 1.0
+        reward = a_bar * batch / elapsed
+        rec = torch.tensor([float(arm), reward, a_bar], dtype=torch.float64)
+        out = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, rec)
+        for r in range(world):  # rank order: every replica applies the same sequence
+            mab.apply_record(int(out[r][0].item()), out[r][1].item(), out[r][2].item())
+    # reward windows (median, fill) must agree; selection counts are local decisions
+    stats = torch.tensor([v for i in range(len(ARMS)) for v in (mab.arm_stats(i)[0], mab.arm_stats(i)[2])],
+                         dtype=torch.float64)
+    gathered = [torch.zeros_like(stats) for _ in range(world)]
+    dist.all_gather(gathered, stats)
+    q.put((rank, all(torch.equal(gathered[0], t) for t in gathered)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_allgather_merge_keeps_replicas_identical(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + random.randrange(1000)
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
