@@ -17,6 +17,7 @@
 
 #include "engine_kernels.h"
 #include "kernels.cuh"
+#include "pdl.cuh"
 
 namespace tlt {
 
@@ -56,6 +57,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 template <int kHD>
 __global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
+    pdl_wait();
     constexpr int kStride = kHD + 8;  // padded smem row (elements): conflict-free fragments
     constexpr int KS = kHD / 16;      // k-steps over head_dim
     constexpr int NT = kHD / 8;       // n-tiles of the output
@@ -297,7 +299,7 @@ void launch_attention_mma_t(const AttnParams& p, cudaStream_t st) {
     const int G = p.H / p.KV;
     const int nqv = p.rows_per_req * G;
     dim3 grid((nqv + kQV - 1) / kQV, p.KV, p.n_groups * p.max_splits);
-    k_attention_mma<kHD><<<grid, 128, smem, st>>>(p);
+    launch_pdl(k_attention_mma<kHD>, grid, 128, smem, st, p);
 }
 
 int attention_mma_split() { return kSplit; }

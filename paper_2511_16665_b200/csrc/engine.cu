@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "engine.h"
+#include "pdl.cuh"
 
 namespace tlt {
 
@@ -477,6 +478,7 @@ void Engine::drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, i
 }
 
 __global__ void k_scatter_feat(Rows rows, int d, const __nv_bfloat16* __restrict__ feat, __nv_bfloat16* hist, int cap) {
+    pdl_wait();
     const int r = blockIdx.x;
     const int slot = rows.slot[r];
     if (slot < 0) return;
@@ -485,7 +487,7 @@ __global__ void k_scatter_feat(Rows rows, int d, const __nv_bfloat16* __restrict
 }
 
 void Engine::scatter_features(const Rows& rw, int R, const bf16* feat) {
-    k_scatter_feat<<<R, 256, 0, st_>>>(rw, cfg.hidden, feat, feat_hist_, cap_);
+    launch_pdl(k_scatter_feat, R, 256, 0, st_, rw, cfg.hidden, feat, feat_hist_, cap_);
     CUDA_CHECK(cudaGetLastError());
     count_launch();
 }

@@ -14,6 +14,7 @@
 
 #include "gemm.cuh"
 #include "ptx.cuh"
+#include "pdl.cuh"
 #include "tlt_internal.h"
 
 namespace tlt {
@@ -32,17 +33,22 @@ constexpr int kABytes = kBlockM * kBlockK * 2;
 template <int KM>
 __device__ __forceinline__ void topk_insert(float (&v)[KM], int (&id)[KM], float x, int ix) {
     if (!(x > v[KM - 1] || (x == v[KM - 1] && ix < id[KM - 1]))) return;
-    int p = KM - 1;
+    // branch-free insertion with static indices only (keeps the list in registers)
+    bool placed = false;
 #pragma unroll
     for (int s = KM - 1; s > 0; --s) {
-        if (p == s && (x > v[s - 1] || (x == v[s - 1] && ix < id[s - 1]))) {
-            v[s] = v[s - 1];
-            id[s] = id[s - 1];
-            p = s - 1;
-        }
+        const bool shift = !placed && (x > v[s - 1] || (x == v[s - 1] && ix < id[s - 1]));
+        const bool put = !placed && !shift;
+        const float nv = shift ? v[s - 1] : (put ? x : v[s]);
+        const int ni = shift ? id[s - 1] : (put ? ix : id[s]);
+        v[s] = nv;
+        id[s] = ni;
+        placed = placed || put;
     }
-    v[p] = x;
-    id[p] = ix;
+    if (!placed) {
+        v[0] = x;
+        id[0] = ix;
+    }
 }
 
 template <int KM>
@@ -101,12 +107,15 @@ __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem
         }
         const int tok = t0 + c + col;
         if (part == 0 && tok < ep.m_tok) {
-            float* out = ep.out_f32 + ((long long)blockIdx.x * ep.m_tok + tok) * W;
+            float* out = ep.out_f32 + ((long long)blockIdx.y * ep.m_tok + tok) * W;
             out[0] = m;
             out[1] = s;
-            for (int r = 0; r < K; ++r) {
-                out[2 + r] = lv[r];
-                out[2 + K + r] = __int_as_float(li[r]);
+#pragma unroll
+            for (int r = 0; r < KM; ++r) {  // static indices: lv/li stay in registers
+                if (r < K) {
+                    out[2 + r] = lv[r];
+                    out[2 + K + r] = __int_as_float(li[r]);
+                }
             }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -128,8 +137,10 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * kBlockM;
-    const int t0 = blockIdx.y * bn;
+    // token tiles vary fastest: the CTAs sharing one weight tile run together,
+    // so the weight tile is fetched from HBM once and re-read from L2
+    const int n0 = blockIdx.y * kBlockM;
+    const int t0 = blockIdx.x * bn;
     const int z = blockIdx.z;
     const int kb0 = z * kb_per_split;
     const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
@@ -155,6 +166,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+    pdl_wait();  // setup above overlaps the previous kernel's tail (PDL)
 
     if (warp == 0) {
         // ---------------- TMA producer
@@ -227,6 +239,7 @@ __global__ void __launch_bounds__(192, 1)
 
 __global__ void k_splitk_reduce(const float* __restrict__ ws, long long stride, int splits, int ld,
                                 EpiParams ep) {
+    pdl_wait();
     const int npairs = (ep.n_out + 1) >> 1;
     const long long total = (long long)ep.m_tok * npairs;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -320,13 +333,13 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         attr_set = true;
     }
     EpiParams ep = ep_in;
-    dim3 grid(g.n_wtiles, g.n_ttiles, g.splits);
+    dim3 grid(g.n_ttiles, g.n_wtiles, g.splits);
     if (ep.kind == EPI_PARTIAL) {  // caller reduces (e.g. k_reduce_resid_norm)
         ep.partial_stride = (long long)ep.m_tok * ep.n_out;
         if ((size_t)(ep.partial_stride * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");
         ep.out_f32 = workspace;
         ep.ld_f32 = ep.n_out;
-        k_gemm_swapab<<<grid, 192, g.smem, st>>>(tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split, g.tmem_cols,
+        launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split, g.tmem_cols,
                                                  ep);
         CUDA_CHECK(cudaGetLastError());
         return;
@@ -339,15 +352,15 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         pp.out_f32 = workspace;
         pp.ld_f32 = ep.n_out;
         pp.partial_stride = plane;
-        k_gemm_swapab<<<grid, 192, g.smem, st>>>(tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
+        launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
                                                  g.tmem_cols, pp);
         CUDA_CHECK(cudaGetLastError());
         const long long pairs = (long long)ep.m_tok * ((ep.n_out + 1) / 2);
         const int threads = 256;
         const int blocks = static_cast<int>(std::min<long long>((pairs + threads - 1) / threads, 148LL * 16));
-        k_splitk_reduce<<<blocks, threads, 0, st>>>(workspace, plane, g.splits, ep.n_out, ep);
+        launch_pdl(k_splitk_reduce, blocks, threads, 0, st, workspace, plane, g.splits, ep.n_out, ep);
     } else {
-        k_gemm_swapab<<<grid, 192, g.smem, st>>>(tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
+        launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
                                                  g.tmem_cols, ep);
     }
     CUDA_CHECK(cudaGetLastError());

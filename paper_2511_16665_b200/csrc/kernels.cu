@@ -9,6 +9,7 @@
 #include "../../include/tlt_init.h"
 #include "engine_kernels.h"
 #include "kernels.cuh"
+#include "pdl.cuh"
 
 namespace tlt {
 
@@ -26,18 +27,20 @@ void launch_init(uint16_t* dst, long long n, const tlt_init_params& p, int tenso
 // ------------------------------------------------------------- gathers
 __global__ void k_embed(const int* __restrict__ tok, const int* __restrict__ slot, const bf16* __restrict__ E, int d,
                         float* __restrict__ x) {
+    pdl_wait();
     const int r = blockIdx.x;
     const bool live = slot[r] >= 0;
     const bf16* e = E + (long long)(live ? tok[r] : 0) * d;
     for (int i = threadIdx.x; i < d; i += blockDim.x) x[(long long)r * d + i] = live ? __bfloat162float(e[i]) : 0.f;
 }
 void launch_embed(const Rows& rows, int R, const bf16* E, int d, float* x, cudaStream_t st) {
-    k_embed<<<R, 256, 0, st>>>(rows.tok, rows.slot, E, d, x);
+    launch_pdl(k_embed, R, 256, 0, st, rows.tok, rows.slot, E, d, x);
 }
 
 // X2[r] = [prev feature || embed(tok)] (drafter fc input)
 __global__ void k_draft_in(Rows rows, const bf16* __restrict__ E, int d, const bf16* __restrict__ hist,
                            const bf16* __restrict__ dfeat, bf16* __restrict__ X2) {
+    pdl_wait();
     const int r = blockIdx.x;
     const bool live = rows.slot[r] >= 0;
     const int kind = live ? rows.fkind[r] : 0;
@@ -52,27 +55,29 @@ __global__ void k_draft_in(Rows rows, const bf16* __restrict__ E, int d, const b
 }
 void launch_draft_in(const Rows& rows, int R, const bf16* E, int d, const bf16* hist, const bf16* dfeat, bf16* X2,
                      cudaStream_t st) {
-    k_draft_in<<<R, 256, 0, st>>>(rows, E, d, hist, dfeat, X2);
+    launch_pdl(k_draft_in, R, 256, 0, st, rows, E, d, hist, dfeat, X2);
 }
 
 // out[r] = x[src[r]] for gathering the level-1 root rows
 __global__ void k_gather_rows(const float* __restrict__ x, const int* __restrict__ src, int d, float* __restrict__ out) {
+    pdl_wait();
     const int r = blockIdx.x;
     const int s = src[r];
     for (int i = threadIdx.x; i < d; i += blockDim.x) out[(long long)r * d + i] = s >= 0 ? x[(long long)s * d + i] : 0.f;
 }
 void launch_gather_rows(const float* x, const int* src, int n, int d, float* out, cudaStream_t st) {
-    k_gather_rows<<<n, 256, 0, st>>>(x, src, d, out);
+    launch_pdl(k_gather_rows, n, 256, 0, st, x, src, d, out);
 }
 
 __global__ void k_to_bf16(const float* __restrict__ x, long long n, bf16* __restrict__ out) {
+    pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         out[i] = __float2bfloat16_rn(x[i]);
 }
 void launch_to_bf16(const float* x, long long n, bf16* out, cudaStream_t st) {
     int blocks = (int)((n + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_to_bf16<<<blocks, 256, 0, st>>>(x, n, out);
+    launch_pdl(k_to_bf16, blocks, 256, 0, st, x, n, out);
 }
 
 // ------------------------------------------------------------- RMSNorm
@@ -80,6 +85,7 @@ void launch_to_bf16(const float* x, long long n, bf16* out, cudaStream_t st) {
 // reduction tree (deterministic).
 __global__ void k_rmsnorm(const float* __restrict__ x, int d, const bf16* __restrict__ g, float eps,
                           bf16* __restrict__ out) {
+    pdl_wait();
     __shared__ float red[32];
     const int r = blockIdx.x;
     const float* xr = x + (long long)r * d;
@@ -101,7 +107,7 @@ __global__ void k_rmsnorm(const float* __restrict__ x, int d, const bf16* __rest
         out[(long long)r * d + i] = __float2bfloat16_rn(xr[i] * inv * __bfloat162float(g[i]));
 }
 void launch_rmsnorm(const float* x, int R, int d, const bf16* g, float eps, bf16* out, cudaStream_t st) {
-    k_rmsnorm<<<R, 256, 0, st>>>(x, d, g, eps, out);
+    launch_pdl(k_rmsnorm, R, 256, 0, st, x, d, g, eps, out);
 }
 
 // Split-K reduce + residual add + RMSNorm of the updated row, one CTA per
@@ -115,6 +121,7 @@ constexpr int kNormCluster = 8;
 __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
     k_reduce_resid_norm(const float* __restrict__ ws, long long plane, int splits, int d, float* __restrict__ x,
                         const bf16* __restrict__ g, float eps, bf16* __restrict__ out) {
+    pdl_wait();
     __shared__ float red[32];
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -158,6 +165,7 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
 __global__ void k_reduce_resid_norm_1cta(const float* __restrict__ ws, long long plane, int splits, int d,
                                          float* __restrict__ x, const bf16* __restrict__ g, float eps,
                                          bf16* __restrict__ out) {
+    pdl_wait();
     __shared__ float red[32];
     const int r = blockIdx.x;
     float* xr = x + (long long)r * d;
@@ -188,7 +196,7 @@ __global__ void k_reduce_resid_norm_1cta(const float* __restrict__ ws, long long
 }
 void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int R, int d, float* x, const bf16* g,
                               float eps, bf16* out, cudaStream_t st) {
-    k_reduce_resid_norm<<<dim3(kNormCluster, R), 256, 0, st>>>(ws, plane, splits, d, x, g, eps, out);
+    launch_pdl(k_reduce_resid_norm, dim3(kNormCluster, R), dim3(256), 0, st, ws, plane, splits, d, x, g, eps, out);
 }
 
 // ----------------------------------------------------------- attention
@@ -203,6 +211,7 @@ constexpr int kAttnKeys = 32;
 
 template <int HD>
 __global__ void __launch_bounds__(128) k_attention(AttnParams p) {
+    pdl_wait();
     constexpr int DPL = HD / 32;  // output dims per lane
     __shared__ float qs[kAttnQV][HD];
     __shared__ uint32_t ks[kAttnKeys][HD / 2 + 1];
@@ -334,6 +343,7 @@ __global__ void __launch_bounds__(128) k_attention(AttnParams p) {
 
 template <int HD>
 __global__ void k_attn_combine(AttnParams p) {
+    pdl_wait();
     // one warp per (group, query vector, kv head)
     const int G = p.H / p.KV;
     const int nqv = p.rows_per_req * G;
@@ -382,14 +392,14 @@ void launch_attention(const AttnParams& p, cudaStream_t st) {
     if (p.impl == 1) {
         launch_attention_mma(p, st);  // tensor-core path (attn_mma.cu), chunk = 256 keys
     } else if (p.hd == 128) {
-        k_attention<128><<<grid, 128, 0, st>>>(p);
+        launch_pdl(k_attention<128>, grid, 128, 0, st, p);
     } else {
-        k_attention<64><<<grid, 128, 0, st>>>(p);
+        launch_pdl(k_attention<64>, grid, 128, 0, st, p);
     }
     if (p.hd == 128)
-        k_attn_combine<128><<<cblocks, 256, 0, st>>>(p);
+        launch_pdl(k_attn_combine<128>, cblocks, 256, 0, st, p);
     else
-        k_attn_combine<64><<<cblocks, 256, 0, st>>>(p);
+        launch_pdl(k_attn_combine<64>, cblocks, 256, 0, st, p);
 }
 
 // ------------------------------------------------------- row top-k / argmax
@@ -426,6 +436,7 @@ __global__ void __launch_bounds__(256) k_row_topk(const float* __restrict__ logi
                                                   int k, int need_sum, int* __restrict__ out_tok,
                                                   float* __restrict__ out_logit, float* __restrict__ out_M,
                                                   float* __restrict__ out_S) {
+    pdl_wait();
     __shared__ float sv[256][K];
     __shared__ int si[256][K];
     __shared__ float red[8];
@@ -486,13 +497,13 @@ __global__ void __launch_bounds__(256) k_row_topk(const float* __restrict__ logi
 void launch_row_topk(const float* logits, int R, int V, const int* live, int k, int need_sum, int* out_tok,
                      float* out_logit, float* out_M, float* out_S, cudaStream_t st) {
     if (k <= 1)
-        k_row_topk<1><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_row_topk<1>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
     else if (k <= 2)
-        k_row_topk<2><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_row_topk<2>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
     else if (k <= 4)
-        k_row_topk<4><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_row_topk<4>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
     else
-        k_row_topk<8><<<R, 256, 0, st>>>(logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_row_topk<8>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
 }
 
 // Merge of the LM-head epilogue partials (EPI_TOPK): per token row, over the
@@ -503,6 +514,7 @@ __global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ pa
                                                     const int* __restrict__ live, int* __restrict__ out_tok,
                                                     float* __restrict__ out_logit, float* __restrict__ out_M,
                                                     float* __restrict__ out_S) {
+    pdl_wait();
     __shared__ float sv[256][K];
     __shared__ int si[256][K];
     __shared__ float red[8];
@@ -581,18 +593,19 @@ __global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ pa
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,
                        float* out_M, float* out_S, cudaStream_t st) {
     if (k <= 1)
-        k_topk_merge<1><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<1>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
     else if (k <= 2)
-        k_topk_merge<2><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<2>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
     else if (k <= 4)
-        k_topk_merge<4><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<4>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
     else
-        k_topk_merge<8><<<R, 256, 0, st>>>(part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<8>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
 }
 
 // full fp64 distribution of a row (parity/debug export): p = exp((double)(l-M))/S
 __global__ void k_row_probs(const float* __restrict__ logits, int V, const float* __restrict__ M,
                             const float* __restrict__ S, double* __restrict__ out) {
+    pdl_wait();
     const int r = blockIdx.x;
     const float m = M[r];
     const double s = (double)S[r];
@@ -600,7 +613,7 @@ __global__ void k_row_probs(const float* __restrict__ logits, int V, const float
         out[(long long)r * V + i] = exp((double)(logits[(long long)r * V + i] - m)) / s;
 }
 void launch_row_probs(const float* logits, int R, int V, const float* M, const float* S, double* out, cudaStream_t st) {
-    k_row_probs<<<R, 256, 0, st>>>(logits, V, M, S, out);
+    launch_pdl(k_row_probs, R, 256, 0, st, logits, V, M, S, out);
 }
 
 // ------------------------------------------------------------ row builders
@@ -609,6 +622,7 @@ void launch_row_probs(const float* logits, int R, int V, const float* M, const f
 __global__ void k_rows_level1(const StepIn* __restrict__ st, int b, int b_hi, int D1, Rows rows, Groups g,
                               int* __restrict__ root_row, const int* __restrict__ tok_hist, int cap,
                               int drafter_cap) {
+    pdl_wait();
     const int i = blockIdx.x;
     const int j = threadIdx.x;
     if (j >= D1) return;
@@ -646,12 +660,13 @@ __global__ void k_rows_level1(const StepIn* __restrict__ st, int b, int b_hi, in
 }
 void launch_rows_level1(const StepIn* st, int b, int b_hi, int D1, const Rows& rows, const Groups& g, int* root_row,
                         const int* tok_hist, int cap, cudaStream_t s) {
-    k_rows_level1<<<b_hi, 32 * ((D1 + 31) / 32), 0, s>>>(st, b, b_hi, D1, rows, g, root_row, tok_hist, cap, 0);
+    launch_pdl(k_rows_level1, b_hi, 32 * ((D1 + 31) / 32), 0, s, st, b, b_hi, D1, rows, g, root_row, tok_hist, cap, 0);
 }
 
 // AR decode: one row per request (the root), visible prefix [0, lt) + self.
 __global__ void k_rows_ar(const StepIn* __restrict__ st, int b, int b_hi, Rows rows, Groups g,
                           const int* __restrict__ tok_hist, int cap) {
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= b_hi) return;
     const bool live = i < b && st[i].slot >= 0;
@@ -672,7 +687,7 @@ __global__ void k_rows_ar(const StepIn* __restrict__ st, int b, int b_hi, Rows r
 }
 void launch_rows_ar(const StepIn* st, int b, int b_hi, const Rows& rows, const Groups& g, const int* tok_hist, int cap,
                     cudaStream_t s) {
-    k_rows_ar<<<(b_hi + 127) / 128, 128, 0, s>>>(st, b, b_hi, rows, g, tok_hist, cap);
+    launch_pdl(k_rows_ar, (b_hi + 127) / 128, 128, 0, s, st, b, b_hi, rows, g, tok_hist, cap);
 }
 
 // ------------------------------------------------------------ tree (K6)
@@ -718,6 +733,7 @@ __device__ void bitonic_rank_sort(int* idx, int n_pad, const Cand* cand) {
 // :171-179, computed incrementally — exact under the strict total order),
 // and emit the cut frontier (:154-160) as the next level's drafter rows.
 __global__ void __launch_bounds__(kTreeThreads) k_tree_level(TreeParams p) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char tree_smem[];
     Cand* sc = reinterpret_cast<Cand*>(tree_smem);                       // kept (first n_kept) + new children
     int* sidx = reinterpret_cast<int*>(tree_smem + sizeof(Cand) * kSortCap);
@@ -887,6 +903,7 @@ __global__ void __launch_bounds__(kTreeThreads) k_tree_level(TreeParams p) {
 // remapped, plus the verify rows: root at lt, node n at cache lt+1+n with
 // position lt+depth, visibility = root + ancestors + self.
 __global__ void k_tree_final(TreeParams p) {
+    pdl_wait();
     const int i = blockIdx.x;
     const bool live = i < p.b && p.step[i].slot >= 0;
     const int T = p.T, T1 = p.T + 1;
@@ -952,9 +969,9 @@ void launch_tree_level(const TreeParams& p, cudaStream_t st) {
         cudaFuncSetAttribute(k_tree_level, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_tree_level<<<p.b_hi, kTreeThreads, smem, st>>>(p);
+    launch_pdl(k_tree_level, p.b_hi, kTreeThreads, smem, st, p);
 }
-void launch_tree_final(const TreeParams& p, cudaStream_t st) { k_tree_final<<<p.b_hi, 128, 0, st>>>(p); }
+void launch_tree_final(const TreeParams& p, cudaStream_t st) { launch_pdl(k_tree_final, p.b_hi, 128, 0, st, p); }
 
 // ---------------------------------------------------------- accept (K7)
 // verify_greedy (spec_decode.hpp:245-268): from the root, accept the child
@@ -962,6 +979,7 @@ void launch_tree_final(const TreeParams& p, cudaStream_t st) { k_tree_final<<<p.
 // node's children carry distinct tokens), else emit that argmax as the bonus.
 // One warp per request; children are found with a ballot over the tree.
 __global__ void k_accept_greedy(AcceptParams p) {
+    pdl_wait();
     const int i = blockIdx.x;
     const int lane = threadIdx.x;
     const bool live = i < p.b && p.step[i].slot >= 0;
@@ -1001,7 +1019,7 @@ __global__ void k_accept_greedy(AcceptParams p) {
         p.bonus[i] = want;
     }
 }
-void launch_accept_greedy(const AcceptParams& p, cudaStream_t st) { k_accept_greedy<<<p.b_hi, 32, 0, st>>>(p); }
+void launch_accept_greedy(const AcceptParams& p, cudaStream_t st) { launch_pdl(k_accept_greedy, p.b_hi, 32, 0, st, p); }
 
 // ------------------------------------------------- commit / compaction (K8)
 // grid (b_hi, layers + 1): blocks y < layers compact that layer's target KV
@@ -1009,6 +1027,7 @@ void launch_accept_greedy(const AcceptParams& p, cudaStream_t st) { k_accept_gre
 // == layers commits tokens (accepted ++ bonus) and target features of the
 // root + accepted rows into the per-slot histories.
 __global__ void k_commit(CommitParams p) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char cm_smem[];
     const int i = blockIdx.x;
     const bool live = i < p.b && p.step[i].slot >= 0;
@@ -1054,13 +1073,14 @@ __global__ void k_commit(CommitParams p) {
 void launch_commit(const CommitParams& p, cudaStream_t st) {
     const int smem = 2 * p.maxD * p.KV * p.hd * 2;
     dim3 grid(p.b_hi, p.layers + 1);
-    k_commit<<<grid, 256, smem, st>>>(p);
+    launch_pdl(k_commit, grid, 256, smem, st, p);
 }
 
 // AR commit: token at lt+1, feature at lt
 __global__ void k_commit_ar(const StepIn* __restrict__ st, int b, const int* __restrict__ argmax,
                             const bf16* __restrict__ feat, int d, int* tok_hist, bf16* feat_hist, int cap,
                             int* __restrict__ out_tok) {
+    pdl_wait();
     const int i = blockIdx.x;
     if (i >= b || st[i].slot < 0) return;
     const int slot = st[i].slot, lt = st[i].lt;
@@ -1073,7 +1093,7 @@ __global__ void k_commit_ar(const StepIn* __restrict__ st, int b, const int* __r
 }
 void launch_commit_ar(const StepIn* st, int b, const int* argmax, const bf16* feat, int d, int* tok_hist,
                       bf16* feat_hist, int cap, int* out_tok, cudaStream_t s) {
-    if (b > 0) k_commit_ar<<<b, 256, 0, s>>>(st, b, argmax, feat, d, tok_hist, feat_hist, cap, out_tok);
+    if (b > 0) launch_pdl(k_commit_ar, b, 256, 0, s, st, b, argmax, feat, d, tok_hist, feat_hist, cap, out_tok);
 }
 
 }  // namespace tlt

@@ -1,0 +1,21 @@
+"""Launch one GEMM shape a few times (for ncu --set full captures)."""
+import sys
+
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+from paper_2511_16665_b200 import _lib  # noqa: E402
+
+m, k, n, kind = (int(a) for a in sys.argv[1:5])
+L = _lib.lib()
+x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
+w = (torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16)
+y32 = torch.empty(m, n, device="cuda", dtype=torch.float32)
+y16 = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+ws = torch.empty(64 << 20, device="cuda", dtype=torch.float32)
+for _ in range(3):
+    rc = L.tlt_dev_gemm(x.data_ptr(), m, k, w.data_ptr(), n, kind, y32.data_ptr(), y16.data_ptr(), ws.data_ptr(),
+                        ws.numel(), 0)
+    assert rc >= 1, _lib.last_error()
+torch.cuda.synchronize()
+print("ok splits", rc)
