@@ -233,6 +233,12 @@ TLT_API int tlt_debug_expansions(tlt_engine* e, int i, int max_exp, int32_t* n_e
                                  int32_t* paths /* [max_exp][depth] */, double* rows /* [max_exp][V] */);
 /* Target logits (fp32) of the verify rows of request i: [T+1][V], row 0 = root. */
 TLT_API int tlt_debug_verify_logits(tlt_engine* e, int i, float* logits, int max_rows, int32_t* n_rows);
+/* Drafted chain of request i in the last tlt_sd_step_stochastic and the
+ * number of uniforms it consumed (draft_depth + examined positions + 1). */
+TLT_API int tlt_debug_chain(tlt_engine* e, int i, int32_t* chain, int32_t* n, int32_t* consumed);
+/* Raw (untempered) target rows, fp64, of the root + chain of request i in the
+ * last stochastic step: [D+1][V], computed by the accept kernel's code. */
+TLT_API int tlt_debug_target_rows(tlt_engine* e, int i, double* rows, int max_rows, int32_t* n_rows);
 /* Target logits of the last tlt_ar_step: [b][V]. */
 TLT_API int tlt_debug_ar_logits(tlt_engine* e, float* logits, int b);
 

@@ -574,6 +574,75 @@ int orc_neural_spec_generate(orc_model* m, const int32_t* prompt, int prompt_len
     return rc ? rc : steps;
 }
 
+/* Stochastic-path rows: same as softmax64 but the normalizer is a double sum
+ * (rows sum to 1 within 1e-15, matching the GPU stochastic kernels). */
+static void softmax64d(const float* l, int v, double* p) {
+    float M = l[0];
+    for (int i = 1; i < v; ++i)
+        if (l[i] > M) M = l[i];
+    double S = 0.0;
+    for (int i = 0; i < v; ++i) {
+        p[i] = exp((double)(l[i] - M));
+        S += p[i];
+    }
+    for (int i = 0; i < v; ++i) p[i] /= S;
+}
+static int drafter_d_cb(void* user, const int32_t* path, int n, double* out) {
+    orc_seq* s = (orc_seq*)user;
+    if (orc_drafter_row(s, path, n, NULL, s->logits)) return -1;
+    softmax64d(s->logits, s->m->c.vocab, out);
+    return 0;
+}
+static int target_raw_cb(void* user, const int32_t* path, int n, double* out) {
+    orc_seq* s = (orc_seq*)user;
+    if (orc_target_logits_path(s, path, n, s->logits)) return -1;
+    softmax64d(s->logits, s->m->c.vocab, out);
+    return 0;
+}
+
+/* Rejection-sampling SD generate (spec_generate in StochasticLinear mode,
+ * spec_decode.hpp:351-380): build_sampled_chain over the EAGLE drafter,
+ * verify_stochastic over the neural target, uniforms from
+ * RngStream(seed, stream). Returns #steps. */
+int orc_neural_spec_generate_stochastic(orc_model* m, const int32_t* prompt, int prompt_len, int max_len, int depth,
+                                        double temperature, uint64_t seed, uint64_t stream, int32_t* out_tokens,
+                                        int* out_len, int32_t* accept_lens, int max_steps) {
+    orc_seq* s = orc_seq_create(m);
+    if (!s || orc_seq_append(s, prompt, prompt_len)) return -1;
+    orc_rng r;
+    orc_rng_init(&r, seed, stream);
+    orc_usrc u = {&r, NULL, 0, 0};
+    const int V = m->c.vocab;
+    orc_node* chain = (orc_node*)malloc(sizeof(orc_node) * (size_t)depth);
+    double* dd = (double*)malloc(sizeof(double) * (size_t)depth * (size_t)V);
+    int gen = 0, steps = 0, rc = 0;
+    while (gen < max_len && steps < max_steps) {
+        if (orc_build_sampled_chain(drafter_d_cb, s, V, depth, &u, chain, dd) != depth) {
+            rc = -1;
+            break;
+        }
+        orc_accept res;
+        if (orc_verify_stochastic(target_raw_cb, s, V, temperature, chain, depth, dd, &u, &res)) {
+            rc = -1;
+            break;
+        }
+        accept_lens[steps++] = res.accept_length;
+        int done = 0;
+        for (int i = 0; i <= res.accept_length && !done; ++i) {
+            int32_t t = i < res.accept_length ? res.accepted[i] : res.bonus;
+            out_tokens[gen++] = t;
+            orc_seq_append(s, &t, 1);
+            if (t == TLT_EOS_TOKEN_ORC || gen >= max_len) done = 1;
+        }
+        if (done) break;
+    }
+    *out_len = gen;
+    free(chain);
+    free(dd);
+    orc_seq_destroy(s);
+    return rc ? rc : steps;
+}
+
 int orc_neural_generate_ar(orc_model* m, const int32_t* prompt, int prompt_len, int max_len, int32_t* out_tokens) {
     orc_seq* s = orc_seq_create(m);
     if (!s || orc_seq_append(s, prompt, prompt_len)) return -1;

@@ -211,6 +211,11 @@ int orc_seq_truncate(orc_seq* s, int len);
 int orc_neural_spec_generate(orc_model* m, const int32_t* prompt, int prompt_len, int max_len,
                              const orc_strategy* s, int32_t* out_tokens, int* out_len, int32_t* accept_lens,
                              orc_node* trees, int32_t* tree_sizes, int max_steps);
+/* Rejection-sampling SD generate (StochasticLinear), uniforms from
+ * RngStream(seed, stream) in reference consumption order. */
+int orc_neural_spec_generate_stochastic(orc_model* m, const int32_t* prompt, int prompt_len, int max_len, int depth,
+                                        double temperature, uint64_t seed, uint64_t stream, int32_t* out_tokens,
+                                        int* out_len, int32_t* accept_lens, int max_steps);
 /* Greedy AR decode (generate_autoregressive at temperature 0). */
 int orc_neural_generate_ar(orc_model* m, const int32_t* prompt, int prompt_len, int max_len, int32_t* out_tokens);
 

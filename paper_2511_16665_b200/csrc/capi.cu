@@ -2,6 +2,7 @@
 // engine lifecycle, steps, graph pool, BEG-MAB / RNG / capture plan, and the
 // rollout loop (reference run_rollout, rollout.hpp:130-276).
 #include <chrono>
+#include <deque>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -87,9 +88,32 @@ TLT_API int tlt_sd_step(tlt_engine* e, const tlt_strategy* s, int b, const int32
 
 TLT_API int tlt_sd_step_stochastic(tlt_engine* e, int draft_depth, float temperature, int b, const int32_t* slot_ids,
                                    const double* uniforms, tlt_accept_out* out) {
-    (void)draft_depth, (void)temperature, (void)b, (void)slot_ids, (void)uniforms, (void)out;
+    if (!e || !slot_ids) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { e->e->sd_step_stochastic(draft_depth, temperature, b, slot_ids, uniforms, out); });
+}
+
+TLT_API int tlt_debug_target_rows(tlt_engine* e, int i, double* rows, int max_rows, int32_t* n_rows) {
     if (!e) return fail(TLT_ERR_STATE, "null engine");
-    return fail(TLT_ERR_CONFIG, "mode: stochastic linear-chain verify is not implemented in this build");
+    return guard([&] {
+        auto& E = *e->e;
+        if (i < 0 || i >= (int)E.dbg_praw.size()) throw tlt::ConfigErr("i", "no debug data for request");
+        const auto& v = E.dbg_praw[i];
+        const int V = E.cfg.vocab;
+        const int n = (int)(v.size() / V);
+        *n_rows = n;
+        std::memcpy(rows, v.data(), sizeof(double) * (size_t)std::min(n, max_rows) * V);
+    });
+}
+
+TLT_API int tlt_debug_chain(tlt_engine* e, int i, int32_t* chain, int32_t* n, int32_t* consumed) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] {
+        auto& E = *e->e;
+        if (i < 0 || i >= (int)E.last_chain.size()) throw tlt::ConfigErr("i", "no stochastic step recorded");
+        *n = (int32_t)E.last_chain[i].size();
+        for (size_t j = 0; j < E.last_chain[i].size(); ++j) chain[j] = E.last_chain[i][j];
+        *consumed = E.last_consumed[i];
+    });
 }
 
 TLT_API int tlt_ar_step(tlt_engine* e, int b, const int32_t* slot_ids, int32_t* out_tokens, float* elapsed_ms) {
@@ -252,7 +276,11 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         const auto t0 = std::chrono::steady_clock::now();
         if (n < 1 || n > E.cfg.max_slots) throw tlt::ConfigErr("requests", "count exceeds max_slots");
         if (cfg->elastic_threshold < 1) throw tlt::ConfigErr("threshold", "must be >= 1");
-        if (cfg->mode != TLT_MODE_GREEDY_TREE) throw tlt::ConfigErr("mode", "only greedy tree SD in this build");
+        const bool stoch = cfg->mode == TLT_MODE_STOCHASTIC_LINEAR;
+        if (cfg->mode != TLT_MODE_GREEDY_TREE && !stoch) throw tlt::ConfigErr("mode", "unknown decode mode");
+        // experiment.hpp:136-137: stochastic_linear requires temperature > 0
+        if (stoch && !(cfg->temperature > 0.0f)) throw tlt::ConfigErr("temperature", "stochastic_linear requires t > 0");
+        if (cfg->temperature < 0.0f) throw tlt::ConfigErr("temperature", "must be >= 0");
         if (cfg->use_mab && !mab) throw tlt::ConfigErr("mab", "use_mab requires a bandit state");
         if (!cfg->use_mab && cfg->enable_sd) tlt::validate(cfg->fixed_strategy);
         E.use_graphs = cfg->use_graphs != 0;
@@ -277,6 +305,17 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         else
             maxD = std::max(1, cfg->fixed_strategy.draft_depth);
         std::vector<int32_t> act, acc_len, bonus, accepted, tok;
+        // per-request queue of RngStream draws: the device consumes them in
+        // reference order, the host pops exactly what was consumed
+        std::vector<std::deque<double>> uq(n);
+        std::vector<double> ubuf;
+        auto take = [&](int i, int cnt, double* dst) {
+            while ((int)uq[i].size() < cnt) uq[i].push_back(req_rng[i].uniform01());
+            for (int c = 0; c < cnt; ++c) dst[c] = uq[i][c];
+        };
+        auto pop = [&](int i, int cnt) {
+            for (int c = 0; c < cnt; ++c) uq[i].pop_front();
+        };
         for (;;) {
             act.clear();
             for (int i = 0; i < n; ++i)
@@ -303,7 +342,15 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 accepted.assign((size_t)batch * D, 0);
                 float ms = 0.f;
                 tlt_accept_out ao{accepted.data(), nullptr, acc_len.data(), bonus.data(), nullptr, nullptr, &ms};
-                E.sd_step(s, batch, act.data(), nullptr, &ao);
+                if (stoch) {
+                    const int U = 2 * D + 1;
+                    ubuf.assign((size_t)batch * U, 0.0);
+                    for (int j = 0; j < batch; ++j) take(act[j], U, ubuf.data() + (size_t)j * U);
+                    E.sd_step_stochastic(D, cfg->temperature, batch, act.data(), ubuf.data(), &ao);
+                    for (int j = 0; j < batch; ++j) pop(act[j], E.last_consumed[j]);
+                } else {
+                    E.sd_step(s, batch, act.data(), nullptr, &ao);
+                }
                 for (int j = 0; j < batch; ++j) {
                     const int i = act[j];
                     out->verify_events += 1;
@@ -317,9 +364,14 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 out->sd_steps += 1;
             } else {
                 tok.assign(batch, 0);
-                const float ms = E.ar_step(batch, act.data(), tok.data());
+                ubuf.assign(batch, 0.0);
+                // sample_token consumes one draw per request (rollout.hpp:252-253)
+                for (int j = 0; j < batch; ++j) take(act[j], 1, ubuf.data() + j);
+                const float ms = cfg->temperature > 0.0f
+                                     ? E.ar_step_sampled(batch, act.data(), cfg->temperature, ubuf.data(), tok.data())
+                                     : E.ar_step(batch, act.data(), tok.data());
                 for (int j = 0; j < batch; ++j) {
-                    req_rng[act[j]].uniform01();  // sample_token consumes one draw (rollout.hpp:253)
+                    pop(act[j], 1);
                     emit(act[j], tok[j]);
                 }
                 out->device_ms += ms;

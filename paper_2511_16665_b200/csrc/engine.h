@@ -55,6 +55,13 @@ public:
     // greedy tree SD step; returns device ms
     float sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out);
     float ar_step(int b, const int32_t* slots, int32_t* out_tokens);
+    // rejection-sampling SD over a drafter-sampled chain (stochastic.cu);
+    // uniforms [b][2D+1] in RngStream consumption order
+    float sd_step_stochastic(int D, float temperature, int b, const int32_t* slots, const double* uniforms,
+                             tlt_accept_out* out);
+    std::vector<std::vector<double>> dbg_praw;   // [request i] [(D+1)*V] raw target rows examined (stochastic)
+    std::vector<int> last_consumed;              // uniforms consumed per request by the last stochastic step
+    std::vector<std::vector<int>> last_chain;    // drafted chain per request of the last stochastic step
 
     int slot_len(int slot) const { return lt_.at(slot); }
     void set_debug(bool on) { debug_ = on; }
@@ -93,6 +100,22 @@ private:
     void catchup_drafter(int b, const int32_t* slots);
     void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real);
     void ar_device_sequence(int b_hi);
+    void stoch_device_sequence(int b_hi, int D, double temperature, bool dbg, int b_real);
+    void ar_sample_sequence(int b_hi, double temperature);
+    void ensure_stoch_buffers();
+
+public:
+    float ar_step_sampled(int b, const int32_t* slots, float temperature, const double* uniforms,
+                          int32_t* out_tokens);
+
+private:
+    // stochastic-path buffers
+    double* qrows_ = nullptr;   // drafter chain rows [S][kMaxDepth][V]
+    double* pbuf_ = nullptr;    // target row scratch [S][V]
+    double* d_uni_ = nullptr;   // uploaded uniforms [S][2*kMaxDepth+1]
+    double* h_uni_ = nullptr;   // pinned staging
+    int* consumed_ = nullptr;
+    int* h_consumed_ = nullptr;
     void upload_rows_host(const std::vector<int>& tok, const std::vector<int>& pos, const std::vector<int>& slot,
                           const std::vector<int>& cidx, const std::vector<int>& fkind,
                           const std::vector<long long>& fidx, const std::vector<uint32_t>& mask,

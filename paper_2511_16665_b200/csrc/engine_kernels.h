@@ -93,6 +93,16 @@ void launch_gather_rows(const float* x, const int* src, int n, int d, float* out
 void launch_to_bf16(const float* x, long long n, __nv_bfloat16* out, cudaStream_t st);
 void launch_rmsnorm(const float* x, int R, int d, const __nv_bfloat16* g, float eps, __nv_bfloat16* out,
                     cudaStream_t st);
+void launch_raw_rows(const float* logits, int R, int V, double* out, cudaStream_t st);
+void launch_sample_rows(const float* logits, int R, int V, const int* live, double temperature, const double* uni,
+                        double* pbuf, int* out_tok, cudaStream_t st);
+void launch_chain_sample(const float* logits, int R, int V, const int* live, double* q, int level, int D,
+                         const double* uni, int uni_stride, int* out_tok, float* out_logit, float* out_M, float* out_S,
+                         cudaStream_t st);
+void launch_accept_stochastic(const StepIn* step, int b, int D, int V, double temperature, const float* vlogits,
+                              const double* q, const int* chain, const int* chain_n, const double* uni,
+                              int uni_stride, double* pbuf, int* acc_nodes, int* acc_tok, int* acc_len, int* bonus,
+                              int* consumed, int maxD, int chain_stride, cudaStream_t st);
 void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int R, int d, float* x,
                               const __nv_bfloat16* g, float eps, __nv_bfloat16* out, cudaStream_t st);
 void launch_attention(const AttnParams& p, cudaStream_t st);

@@ -53,7 +53,7 @@ __device__ __forceinline__ void topk_insert(float (&v)[KM], int (&id)[KM], float
 
 template <int KM>
 __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem, int q, int lane, int n0, int t0,
-                                              int bn, float* tr) {
+                                              int bn, float* tr, int tile) {
     const int K = ep.topk_k;
     const int W = 2 + 2 * K;
     const int ep_tid = threadIdx.x - 64;  // 0..127
@@ -107,7 +107,7 @@ __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem
         }
         const int tok = t0 + c + col;
         if (part == 0 && tok < ep.m_tok) {
-            float* out = ep.out_f32 + ((long long)blockIdx.y * ep.m_tok + tok) * W;
+            float* out = ep.out_f32 + ((long long)tile * ep.m_tok + tok) * W;
             out[0] = m;
             out[1] = s;
 #pragma unroll
@@ -124,12 +124,13 @@ __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem
 
 __global__ void __launch_bounds__(192, 1)
     k_gemm_swapab(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                  int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, EpiParams ep) {
+                  int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, int wm, EpiParams ep) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int b_bytes = bn * kBlockK * 2;
+    const int a_bytes = wm * kABytes;  // wm weight sub-tiles of 128 rows share every token tile
     uint8_t* sA = smem;
-    uint8_t* sB = smem + stages * kABytes;
+    uint8_t* sB = smem + stages * a_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + stages * b_bytes);
     uint64_t* empty = full + stages;
     uint64_t* tfull = empty + stages;
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(192, 1)
     const int lane = threadIdx.x & 31;
     // token tiles vary fastest: the CTAs sharing one weight tile run together,
     // so the weight tile is fetched from HBM once and re-read from L2
-    const int n0 = blockIdx.y * kBlockM;
+    const int n0 = blockIdx.y * kBlockM * wm;
     const int t0 = blockIdx.x * bn;
     const int z = blockIdx.z;
     const int kb0 = z * kb_per_split;
@@ -177,9 +178,10 @@ __global__ void __launch_bounds__(192, 1)
                 const int s = i % stages;
                 const uint32_t ph = (i / stages) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&full[s], kABytes + b_bytes);
+                mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
                 const int kc = (kb0 + i) * kBlockK;
-                tma_load_2d(sA + s * kABytes, &tmW, &full[s], kc, n0, pol_w);
+                for (int a = 0; a < wm; ++a)
+                    tma_load_2d(sA + s * a_bytes + a * kABytes, &tmW, &full[s], kc, n0 + a * kBlockM, pol_w);
                 tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
             }
         }
@@ -192,12 +194,14 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&full[s], ph);
             tc_fence_after();
             if (elect_one()) {
-                const uint64_t da = sdesc_kmajor_sw128(sA + s * kABytes);
                 const uint64_t db = sdesc_kmajor_sw128(sB + s * b_bytes);
+                for (int a = 0; a < wm; ++a) {
+                    const uint64_t da = sdesc_kmajor_sw128(sA + s * a_bytes + a * kABytes);
 #pragma unroll
-                for (int kk = 0; kk < kBlockK / 16; ++kk) {
-                    // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
-                    tc_mma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                    for (int kk = 0; kk < kBlockK / 16; ++kk) {
+                        // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
+                        tc_mma_bf16(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                    }
                 }
                 tc_commit(&empty[s]);
                 if (i == nkb - 1) tc_commit(tfull);
@@ -209,25 +213,31 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(tfull, 0);
         tc_fence_after();
         const int q = warp & 3;
-        const int row = n0 + q * 32 + lane;
+        for (int a = 0; a < wm; ++a) {
+        const int na = n0 + a * kBlockM;
+        if (na >= ep.n_out) break;  // second sub-tile entirely out of range
+        const uint32_t tm_a = tmem + a * bn;
+        const int row = na + q * 32 + lane;
         const int n_even = row & ~1;
         if (ep.kind == EPI_TOPK) {
             float* tr = reinterpret_cast<float*>(tmem_holder + 4);  // [16 cols][128 vocab rows]
+            const int tile = blockIdx.y * wm + a;
             if (ep.topk_k <= 1)
-                epi_topk_tile<1>(ep, tmem, q, lane, n0, t0, bn, tr);
+                epi_topk_tile<1>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
             else
-                epi_topk_tile<kEpiTopkMax>(ep, tmem, q, lane, n0, t0, bn, tr);
+                epi_topk_tile<kEpiTopkMax>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
         } else
         for (int c = 0; c < bn; c += 16) {
             if (t0 + c >= ep.m_tok) break;
             float v[16];
-            tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+            tmem_ld16(tm_a + (static_cast<uint32_t>(q * 32) << 16) + c, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
                 if ((lane & 1) == 0) epi_pair(ep, t0 + c + j, n_even, v[j], other, z);
             }
         }
+        }  // a
     }
     tc_fence_before();
     __syncthreads();
@@ -298,24 +308,44 @@ int num_sms() {
     return g_num_sms;
 }
 
+static int env_knob(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
 GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     GemmPlan g;
-    const int n_ttiles = (m_tok + 255) / 256;
+    // Measured on B200 (tools/gemm_sweep.sh, profiles/): two co-resident CTAs
+    // per SM (one's epilogue/prologue overlapping the other's mainloop) beat
+    // deeper pipelines and larger tiles: token tiles <= 128, <= ~110 KB smem.
+    static const int bn_max = env_knob("TLT_GEMM_BN_MAX", 128);
+    static const int force_wm = env_knob("TLT_GEMM_WM", 0);
+    static const int force_stages = env_knob("TLT_GEMM_STAGES", 0);
+    const int n_ttiles = (m_tok + bn_max - 1) / bn_max;
     int bn = (m_tok + n_ttiles - 1) / n_ttiles;
     bn = std::max(16, (bn + 15) / 16 * 16);
     g.bn = bn;
     g.n_ttiles = (m_tok + bn - 1) / bn;
-    g.n_wtiles = (n_out + kBlockM - 1) / kBlockM;
     g.kb_total = (k + kBlockK - 1) / kBlockK;
-    const int stage_bytes = kABytes + bn * kBlockK * 2;
-    const int ctas_per_sm = bn <= 128 ? 2 : 1;
+    // Tensor-bound regime (many tokens): two 128-row weight sub-tiles per CTA
+    // share each staged token tile (halves the L2->SMEM re-reads of the
+    // activations), as long as there are still >= one CTA per SM.
+    const int wtiles2 = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
+    g.wm = 1;  // 2 measured slower at every shape (fewer co-resident CTAs); kept behind TLT_GEMM_WM
+    (void)wtiles2;
+    if (force_wm) g.wm = force_wm;
+    g.n_wtiles = (n_out + kBlockM * g.wm - 1) / (kBlockM * g.wm);
+    const int stage_bytes = g.wm * kABytes + bn * kBlockK * 2;
+    const int ctas_per_sm = (bn <= 128 && g.wm == 1) ? 2 : 1;
     // per-CTA budget incl. barriers, alignment slack and the EPI_TOPK merge
     // scratch, so that 2 CTAs/SM really fit in the 228 KB SM carve-out
     const int fixed = 1024 + 16 * 8 + 64 + 16 * 128 * 4;
     const int budget = (ctas_per_sm == 2 ? 112 * 1024 : 220 * 1024) - fixed;
     g.stages = std::max(2, std::min(8, budget / stage_bytes));
+    if (force_stages) g.stages = std::min(force_stages, std::max(2, (220 * 1024 - fixed) / stage_bytes));
     g.smem = g.stages * stage_bytes + fixed;
-    g.tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+    const int cols = g.wm * bn;
+    g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
     const int tiles = g.n_wtiles * g.n_ttiles;
     const int slots = num_sms() * ctas_per_sm;
     int splits = 1;
@@ -340,7 +370,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         ep.out_f32 = workspace;
         ep.ld_f32 = ep.n_out;
         launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split, g.tmem_cols,
-                                                 ep);
+                   g.wm, ep);
         CUDA_CHECK(cudaGetLastError());
         return;
     }
@@ -353,7 +383,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         pp.ld_f32 = ep.n_out;
         pp.partial_stride = plane;
         launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                                                 g.tmem_cols, pp);
+                                                 g.tmem_cols, g.wm, pp);
         CUDA_CHECK(cudaGetLastError());
         const long long pairs = (long long)ep.m_tok * ((ep.n_out + 1) / 2);
         const int threads = 256;
@@ -361,7 +391,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         launch_pdl(k_splitk_reduce, blocks, threads, 0, st, workspace, plane, g.splits, ep.n_out, ep);
     } else {
         launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                                                 g.tmem_cols, ep);
+                                                 g.tmem_cols, g.wm, ep);
     }
     CUDA_CHECK(cudaGetLastError());
 }

@@ -37,6 +37,7 @@ struct GemmPlan {
     int bn = 16, n_ttiles = 1, n_wtiles = 1, kb_total = 1, kb_per_split = 1, splits = 1, stages = 4;
     int smem = 0;
     unsigned tmem_cols = 32;
+    int wm = 1;  // 128-row weight sub-tiles per CTA (1 or 2)
 };
 
 int num_sms();

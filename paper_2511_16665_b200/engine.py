@@ -212,6 +212,39 @@ class Engine:
         _check(self.L.tlt_ar_step(self.h, len(slots), _p(slots), _p(out), C.byref(ms)))
         return out, ms.value
 
+    def sd_step_stochastic(self, draft_depth, temperature, slots, uniforms):
+        """Rejection-sampling SD over drafter-sampled chains. uniforms: [b][2D+1]
+        RngStream draws in consumption order; returns (StepResult, chains, consumed)."""
+        slots = np.asarray(slots, np.int32)
+        b, D = len(slots), draft_depth
+        uni = np.ascontiguousarray(np.asarray(uniforms, np.float64).reshape(b, 2 * D + 1))
+        acc = np.zeros((b, D), np.int32)
+        nodes = np.zeros((b, D), np.int32)
+        alen = np.zeros(b, np.int32)
+        bonus = np.zeros(b, np.int32)
+        kvl = np.zeros(b, np.int32)
+        ms = np.zeros(1, np.float32)
+        ao = AcceptOut(acc.ctypes.data, nodes.ctypes.data, alen.ctypes.data, bonus.ctypes.data, None,
+                       kvl.ctypes.data, ms.ctypes.data)
+        _check(self.L.tlt_sd_step_stochastic(self.h, D, C.c_float(temperature), b, _p(slots), _p(uni),
+                                             C.byref(ao)))
+        chains, consumed = [], []
+        for i in range(b):
+            ch = np.zeros(D, np.int32)
+            n, cons = C.c_int32(), C.c_int32()
+            _check(self.L.tlt_debug_chain(self.h, i, _p(ch), C.byref(n), C.byref(cons)))
+            chains.append(ch[:n.value].tolist())
+            consumed.append(cons.value)
+        res = StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
+                         [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
+        return res, chains, consumed
+
+    def debug_target_rows(self, i: int, max_rows: int = 32):
+        out = np.zeros((max_rows, self.vocab), np.float64)
+        n = C.c_int32()
+        _check(self.L.tlt_debug_target_rows(self.h, i, _p(out), max_rows, C.byref(n)))
+        return out[:n.value]
+
     # ---------------------------------------------------------- debug
     def debug_expansions(self, i: int, max_exp: int = 4096):
         n = C.c_int32()
@@ -236,7 +269,8 @@ class Engine:
 
     # ---------------------------------------------------------- rollout
     def run_rollout(self, prompts, max_lens, request_ids=None, *, enable_sd=True, elastic_threshold=32,
-                    strategy=(4, 4, 16), mab: "Mab | None" = None, seed=0, use_graphs=True):
+                    strategy=(4, 4, 16), mab: "Mab | None" = None, seed=0, use_graphs=True, mode="greedy",
+                    temperature=0.0):
         n = len(prompts)
         rid = np.asarray(request_ids if request_ids is not None else range(n), np.int32)
         plen = np.asarray([len(p) for p in prompts], np.int32)
@@ -245,7 +279,8 @@ class Engine:
         stride = int(ml.max())
         gen = np.zeros((n, stride), np.int32)
         glen = np.zeros(n, np.int32)
-        cfg = RolloutCfg(1 if enable_sd else 0, elastic_threshold, 0, 0.0, Strategy(*strategy),
+        cfg = RolloutCfg(1 if enable_sd else 0, elastic_threshold, 1 if mode == "stochastic" else 0,
+                         float(temperature), Strategy(*strategy),
                          1 if mab is not None else 0, seed, 1 if use_graphs else 0)
         res = RolloutResult(gen.ctypes.data, glen.ctypes.data)
         _check(self.L.tlt_run_rollout(self.h, C.byref(cfg), mab.h if mab is not None else None, n, _p(rid),
