@@ -297,7 +297,7 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
     ep.n_out = N;
     ep.m_tok = M;
     launch_gemm(g, tmW, tx, ep, ws_, ws_elems_, st_);
-    count_launch(g.splits > 1 ? 2 : 1);
+    count_launch(1);  // split-K reduction is fused into the same launch
 }
 
 // x_ += X W^T, then h_ = bf16(rmsnorm(x_) * norm_w) when norm_w != null. At

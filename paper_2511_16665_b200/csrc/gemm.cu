@@ -238,6 +238,38 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
         }  // a
+        if (ep.counters) {
+            // fused split-K finish: the last CTA of this tile reduces all
+            // partials in fixed z order (deterministic) and applies final_kind
+            __shared__ int s_last;
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (threadIdx.x == 64) {
+                const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+                const int old = atomicAdd(&ep.counters[tile], 1);
+                s_last = old == (int)gridDim.z - 1;
+                if (s_last) ep.counters[tile] = 0;  // ready for the next launch / graph replay
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (s_last) {
+                __threadfence();
+                EpiParams fe = ep;
+                fe.kind = ep.final_kind;
+                const int t1 = min(ep.m_tok, t0 + bn);
+                for (int a = 0; a < wm; ++a) {
+                    const int row = n0 + a * kBlockM + q * 32 + lane;
+                    const int n_even = row & ~1;
+                    for (int t = t0; t < t1; ++t) {
+                        float v = 0.f;
+                        if (row < ep.n_out)
+                            for (int zz = 0; zz < (int)gridDim.z; ++zz)
+                                v += ep.ws[zz * ep.partial_stride + (long long)t * ep.ws_ld + row];
+                        const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+                        if ((lane & 1) == 0) epi_pair(fe, t, n_even, v, other, 0);
+                    }
+                }
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -355,6 +387,20 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     return g;
 }
 
+constexpr long long kSplitCounters = 1 << 16;
+// per-device zeroed tile counters for the fused split-K finish (each last CTA
+// resets its counter, so the buffer stays zero between launches / replays)
+static int* split_counters() {
+    static int* ptrs[64] = {nullptr};
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    if (!ptrs[dev]) {
+        CUDA_CHECK(cudaMalloc(&ptrs[dev], sizeof(int) * kSplitCounters));
+        CUDA_CHECK(cudaMemset(ptrs[dev], 0, sizeof(int) * kSplitCounters));
+    }
+    return ptrs[dev];
+}
+
 void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep_in,
                  float* workspace, size_t workspace_elems, cudaStream_t st) {
     static bool attr_set = false;
@@ -367,31 +413,32 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     if (ep.kind == EPI_PARTIAL) {  // caller reduces (e.g. k_reduce_resid_norm)
         ep.partial_stride = (long long)ep.m_tok * ep.n_out;
         if ((size_t)(ep.partial_stride * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");
-        ep.out_f32 = workspace;
-        ep.ld_f32 = ep.n_out;
+        ep.ws = workspace;
+        ep.ws_ld = ep.n_out;
+        ep.counters = nullptr;
         launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split, g.tmem_cols,
                    g.wm, ep);
         CUDA_CHECK(cudaGetLastError());
         return;
     }
     if (g.splits > 1) {
+        // fused split-K: partials + last-CTA reduction inside the same launch
         const long long plane = (long long)ep.m_tok * ep.n_out;
         if ((size_t)(plane * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");
+        if ((long long)g.n_ttiles * g.n_wtiles > kSplitCounters) throw CudaError("too many split-K tiles");
         EpiParams pp = ep;
         pp.kind = EPI_PARTIAL;
-        pp.out_f32 = workspace;
-        pp.ld_f32 = ep.n_out;
+        pp.final_kind = ep.kind;
+        pp.ws = workspace;
+        pp.ws_ld = ep.n_out;
         pp.partial_stride = plane;
+        pp.counters = split_counters();
         launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                                                 g.tmem_cols, g.wm, pp);
-        CUDA_CHECK(cudaGetLastError());
-        const long long pairs = (long long)ep.m_tok * ((ep.n_out + 1) / 2);
-        const int threads = 256;
-        const int blocks = static_cast<int>(std::min<long long>((pairs + threads - 1) / threads, 148LL * 16));
-        launch_pdl(k_splitk_reduce, blocks, threads, 0, st, workspace, plane, g.splits, ep.n_out, ep);
+                   g.tmem_cols, g.wm, pp);
     } else {
+        ep.counters = nullptr;
         launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                                                 g.tmem_cols, g.wm, ep);
+                   g.tmem_cols, g.wm, ep);
     }
     CUDA_CHECK(cudaGetLastError());
 }

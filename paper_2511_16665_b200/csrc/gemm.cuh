@@ -53,6 +53,13 @@ struct EpiParams {
     int max_ctx;
     // EPI_TOPK: out_f32 = partials [n_wtiles][m_tok][2 + 2*topk_k] (m, s, vals[k], ids[k])
     int topk_k;
+    // fused split-K: partials are written with EPI_PARTIAL, the last-arriving
+    // CTA of each tile (per-tile counter) reduces them in z order and applies
+    // final_kind — no separate reduce launch
+    int final_kind;
+    int* counters;
+    float* ws;  // EPI_PARTIAL destination: ws[split][t][n], row stride ws_ld
+    int ws_ld;
 };
 constexpr int kEpiTopkMax = 8;
 
@@ -69,7 +76,7 @@ __device__ __forceinline__ void epi_pair(const EpiParams& p, int t, int n, float
             if (has1) o[1] = v1;
         } break;
         case EPI_PARTIAL: {
-            float* o = p.out_f32 + split * p.partial_stride + (long long)t * p.ld_f32 + n;
+            float* o = p.ws + split * p.partial_stride + (long long)t * p.ws_ld + n;
             o[0] = v0;
             if (has1) o[1] = v1;
         } break;
