@@ -415,6 +415,19 @@ void Engine::lm_topk(const float* x, int n, int k, const int* live, bool want_lo
         launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
         count_launch();
     }
+    if (k > 1) {
+        // top-k > 1 (drafter children): fp32 logits + multi-CTA chunked top-k
+        // (the per-column k-selection is too branchy for the MMA epilogue)
+        EpiParams f{};
+        f.kind = EPI_F32;
+        f.out_f32 = logits_;
+        f.ld_f32 = cfg.vocab;
+        gemm(h_, n, cfg.hidden, cfg.hidden, tm_lm_, cfg.vocab, f);
+        const int nch = launch_row_topk_chunked(logits_, n, cfg.vocab, live, k, topk_part_, st_);
+        launch_topk_merge(topk_part_, nch, n, k, live, tk_tok_, tk_logit_, tk_M_, tk_S_, st_);
+        count_launch(2);
+        return;  // logits_ already materialized for the parity exports
+    }
     EpiParams e{};
     e.kind = EPI_TOPK;
     e.out_f32 = topk_part_;

@@ -108,6 +108,7 @@ void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int 
 void launch_attention(const AttnParams& p, cudaStream_t st);
 void launch_row_topk(const float* logits, int R, int V, const int* live, int k, int need_sum, int* out_tok,
                      float* out_logit, float* out_M, float* out_S, cudaStream_t st);
+int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, int k, float* part, cudaStream_t st);
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,
                        float* out_M, float* out_S, cudaStream_t st);
 void launch_row_probs(const float* logits, int R, int V, const float* M, const float* S, double* out,

@@ -256,16 +256,27 @@ __global__ void __launch_bounds__(192, 1)
                 EpiParams fe = ep;
                 fe.kind = ep.final_kind;
                 const int t1 = min(ep.m_tok, t0 + bn);
+                const int nz = (int)gridDim.z;
                 for (int a = 0; a < wm; ++a) {
                     const int row = n0 + a * kBlockM + q * 32 + lane;
                     const int n_even = row & ~1;
-                    for (int t = t0; t < t1; ++t) {
-                        float v = 0.f;
-                        if (row < ep.n_out)
-                            for (int zz = 0; zz < (int)gridDim.z; ++zz)
-                                v += ep.ws[zz * ep.partial_stride + (long long)t * ep.ws_ld + row];
-                        const float other = __shfl_xor_sync(0xffffffffu, v, 1);
-                        if ((lane & 1) == 0) epi_pair(fe, t, n_even, v, other, 0);
+                    const bool rv = row < ep.n_out;
+                    // 8 tokens per batch: all partial loads issued before use (ILP)
+                    for (int tb = t0; tb < t1; tb += 8) {
+                        float v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) v[u] = 0.f;
+                        for (int zz = 0; zz < nz; ++zz) {
+                            const float* src = ep.ws + zz * ep.partial_stride + row;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (rv && tb + u < t1) v[u] += src[(long long)(tb + u) * ep.ws_ld];
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const float other = __shfl_xor_sync(0xffffffffu, v[u], 1);
+                            if ((lane & 1) == 0 && tb + u < t1) epi_pair(fe, tb + u, n_even, v[u], other, 0);
+                        }
                     }
                 }
             }
@@ -405,7 +416,8 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
                  float* workspace, size_t workspace_elems, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        // 226 KB: leaves room for the kernel's few static shared words
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         attr_set = true;
     }
     EpiParams ep = ep_in;

@@ -506,6 +506,100 @@ void launch_row_topk(const float* logits, int R, int V, const int* live, int k, 
         launch_pdl(k_row_topk<8>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
 }
 
+// Stage 1 of the multi-CTA row top-k (k > 1) over materialized logits: CTA
+// (chunk c, row r) reduces a 4096-entry chunk to the same partial record the
+// EPI_TOPK epilogue writes (chunk max m, sum exp(l - m), sorted top-k), so
+// k_topk_merge finishes both. Chunk order is fixed -> deterministic.
+constexpr int kTopkChunk = 4096;
+template <int K>
+__global__ void __launch_bounds__(256) k_row_topk_chunk(const float* __restrict__ logits, int V, const int* live,
+                                                        int k, float* __restrict__ part, int R) {
+    pdl_wait();
+    __shared__ float sv[256][K];
+    __shared__ int si[256][K];
+    __shared__ float red[8];
+    __shared__ float sM;
+    const int c = blockIdx.x, r = blockIdx.y;
+    if (live && live[r] < 0) return;
+    const float* lr = logits + (long long)r * V;
+    const int i0 = c * kTopkChunk, i1 = min(V, i0 + kTopkChunk);
+    TopK<K> t;
+    t.init();
+    float m = -CUDART_INF_F;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const float x = lr[i];
+        m = fmaxf(m, x);
+        t.push(x, i);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = red[0];
+        for (int w = 1; w < 8; ++w) M = fmaxf(M, red[w]);
+        sM = M;
+    }
+    __syncthreads();
+    const float M = sM;
+    float s = 0.f;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) s += __expf(lr[i] - M);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        sv[threadIdx.x][j] = t.v[j];
+        si[threadIdx.x][j] = t.id[j];
+    }
+    __syncthreads();
+    for (int stride = 1; stride < 256; stride <<= 1) {
+        if ((threadIdx.x % (2 * stride)) == 0) {
+            const int a = threadIdx.x, b = threadIdx.x + stride;
+            float mv[K];
+            int mi[K];
+            int ia = 0, ib = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const bool take_a = TopK<K>::better(sv[a][ia], si[a][ia], sv[b][ib], si[b][ib]);
+                mv[j] = take_a ? sv[a][ia] : sv[b][ib];
+                mi[j] = take_a ? si[a][ia] : si[b][ib];
+                if (take_a) ++ia; else ++ib;
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                sv[a][j] = mv[j];
+                si[a][j] = mi[j];
+            }
+        }
+        __syncthreads();
+    }
+    const int W = 2 + 2 * k;
+    float* out = part + ((long long)c * R + r) * W;
+    if (threadIdx.x == 0) {
+        float tot = 0.f;
+        for (int w = 0; w < 8; ++w) tot += red[w];
+        out[0] = M;
+        out[1] = tot;
+    }
+    if (threadIdx.x < k) {
+        out[2 + threadIdx.x] = sv[0][threadIdx.x];
+        out[2 + k + threadIdx.x] = __int_as_float(si[0][threadIdx.x]);
+    }
+}
+int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, int k, float* part, cudaStream_t st) {
+    const int nch = (V + kTopkChunk - 1) / kTopkChunk;
+    const dim3 grid(nch, R);
+    if (k <= 2)
+        launch_pdl(k_row_topk_chunk<2>, grid, dim3(256), 0, st, logits, V, live, k, part, R);
+    else if (k <= 4)
+        launch_pdl(k_row_topk_chunk<4>, grid, dim3(256), 0, st, logits, V, live, k, part, R);
+    else
+        launch_pdl(k_row_topk_chunk<8>, grid, dim3(256), 0, st, logits, V, live, k, part, R);
+    return nch;
+}
+
 // Merge of the LM-head epilogue partials (EPI_TOPK): per token row, over the
 // 128-vocab tiles in fixed order: M = max m_t, S = sum s_t exp(m_t - M), and
 // top-k of the per-tile sorted candidate lists by (logit desc, id asc).
