@@ -220,7 +220,7 @@ void Engine::alloc_state() {
     x2_ = dmalloc<bf16>((size_t)R_ * 2 * d);
     dfeat_ = dmalloc<bf16>((size_t)Rmeta_ * d);
     logits_ = dmalloc<float>((size_t)R_ * V);
-    ws_elems_ = (size_t)env_int("TLT_GEMM_WS_MFLOATS", 64) << 20;
+    ws_elems_ = (size_t)env_int("TLT_GEMM_WS_MFLOATS", 1) << 20;
     ws_ = dmalloc<float>(ws_elems_);
     aws_elems_ = (size_t)env_int("TLT_ATTN_WS_MFLOATS", 192) << 20;
     aws_m_ = dmalloc<float>(aws_elems_ / 32);
@@ -297,12 +297,12 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
     ep.n_out = N;
     ep.m_tok = M;
     launch_gemm(g, tmW, tx, ep, ws_, ws_elems_, st_);
-    count_launch(1);  // split-K reduction is fused into the same launch
+    count_launch(1);  // split-K reduction happens inside the same launch (cluster DSMEM)
 }
 
-// x_ += X W^T, then h_ = bf16(rmsnorm(x_) * norm_w) when norm_w != null. At
-// split-K shapes (long-tail M) the reduce, residual add and the next RMSNorm
-// are one kernel (k_reduce_resid_norm).
+// x_ += X W^T, then h_ = bf16(rmsnorm(x_) * norm_w) when norm_w != null. The
+// residual add is the GEMM epilogue (after the in-cluster split-K reduction at
+// long-tail M); the norm of few rows spreads each row over an 8-CTA cluster.
 void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w) {
     const int d = cfg.hidden;
     GemmPlan g = plan_gemm(M, d, K);
@@ -310,21 +310,17 @@ void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const C
     EpiParams e{};
     e.n_out = d;
     e.m_tok = M;
-    if (g.splits > 1) {
-        e.kind = EPI_PARTIAL;
-        launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
-        launch_reduce_resid_norm(ws_, (long long)M * d, g.splits, M, d, x_, norm_w, cfg.rms_eps, h_, st_);
-        count_launch(2);
-    } else {
-        e.kind = EPI_RESID_ADD;
-        e.out_f32 = x_;
-        e.ld_f32 = d;
-        launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
-        count_launch();
-        if (norm_w) {
+    e.kind = EPI_RESID_ADD;
+    e.out_f32 = x_;
+    e.ld_f32 = d;
+    launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
+    count_launch();
+    if (norm_w) {
+        if (M <= 256)
+            launch_reduce_resid_norm(nullptr, 0, 0, M, d, x_, norm_w, cfg.rms_eps, h_, st_);
+        else
             launch_rmsnorm(x_, M, d, norm_w, cfg.rms_eps, h_, st_);
-            count_launch();
-        }
+        count_launch();
     }
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cooperative_groups.h>
 #include <math_constants.h>
 
 #include <algorithm>
@@ -22,6 +23,7 @@ namespace tlt {
 constexpr int kBlockM = 128;  // weight rows per tile (MMA M)
 constexpr int kBlockK = 64;   // 64 bf16 = one 128-byte swizzle row
 constexpr int kABytes = kBlockM * kBlockK * 2;
+constexpr int kMaxSplits = 8;  // portable thread-block cluster size
 
 // LM-head epilogue (EPI_TOPK) for one 128-vocab x bn-token accumulator tile.
 // Per 16-token chunk the 4 epilogue warps transpose the accumulators through
@@ -213,6 +215,18 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(tfull, 0);
         tc_fence_after();
         const int q = warp & 3;
+        if (gridDim.z > 1) {
+            // split-K: stage this CTA's fp32 partial in the (now idle) pipeline
+            // smem, [token][128 weight rows]; the cluster reduces it below
+            float* P = reinterpret_cast<float*>(smem);
+            for (int c = 0; c < bn; c += 16) {
+                if (t0 + c >= ep.m_tok) break;
+                float v[16];
+                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) P[(c + j) * kBlockM + q * 32 + lane] = v[j];
+            }
+        } else {
         for (int a = 0; a < wm; ++a) {
         const int na = n0 + a * kBlockM;
         if (na >= ep.n_out) break;  // second sub-tile entirely out of range
@@ -238,75 +252,41 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
         }  // a
-        if (ep.counters) {
-            // fused split-K finish: the last CTA of this tile reduces all
-            // partials in fixed z order (deterministic) and applies final_kind
-            __shared__ int s_last;
-            __threadfence();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (threadIdx.x == 64) {
-                const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-                const int old = atomicAdd(&ep.counters[tile], 1);
-                s_last = old == (int)gridDim.z - 1;
-                if (s_last) ep.counters[tile] = 0;  // ready for the next launch / graph replay
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (s_last) {
-                __threadfence();
-                EpiParams fe = ep;
-                fe.kind = ep.final_kind;
-                const int t1 = min(ep.m_tok, t0 + bn);
-                const int nz = (int)gridDim.z;
-                for (int a = 0; a < wm; ++a) {
-                    const int row = n0 + a * kBlockM + q * 32 + lane;
-                    const int n_even = row & ~1;
-                    const bool rv = row < ep.n_out;
-                    // 8 tokens per batch: all partial loads issued before use (ILP)
-                    for (int tb = t0; tb < t1; tb += 8) {
-                        float v[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) v[u] = 0.f;
-                        for (int zz = 0; zz < nz; ++zz) {
-                            const float* src = ep.ws + zz * ep.partial_stride + row;
-#pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                if (rv && tb + u < t1) v[u] += src[(long long)(tb + u) * ep.ws_ld];
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const float other = __shfl_xor_sync(0xffffffffu, v[u], 1);
-                            if ((lane & 1) == 0 && tb + u < t1) epi_pair(fe, tb + u, n_even, v[u], other, 0);
-                        }
-                    }
-                }
-            }
         }
+    }
+    if (gridDim.z > 1) {
+        // Split-K finish inside the thread-block cluster (cluster = the
+        // gridDim.z CTAs of one output tile): every CTA sums one contiguous
+        // slice of (token, row-pair) elements over all peers' partials through
+        // distributed shared memory, in fixed rank order (deterministic), and
+        // applies the epilogue to it. No global partials, no second launch.
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();
+        const int S = (int)gridDim.z;
+        const int tv = min(bn, ep.m_tok - t0);
+        const int npairs = max(tv, 0) * (kBlockM / 2);
+        const int per = (npairs + S - 1) / S;
+        const int p0 = z * per, p1 = min(npairs, p0 + per);
+        float* P = reinterpret_cast<float*>(smem);
+        for (int p = p0 + (int)threadIdx.x; p < p1; p += (int)blockDim.x) {
+            const int c = p / (kBlockM / 2);
+            const int rp = (p % (kBlockM / 2)) * 2;
+            float2 acc = make_float2(0.f, 0.f);
+            for (int zz = 0; zz < S; ++zz) {
+                const float2 v = *reinterpret_cast<const float2*>(cluster.map_shared_rank(P + c * kBlockM + rp, zz));
+                acc.x += v.x;
+                acc.y += v.y;
+            }
+            epi_pair(ep, t0 + c, n0 + rp, acc.x, acc.y, 0);
+        }
+        cluster.sync();  // peers' smem stays alive until every remote read is done
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
                      : "memory");
-    }
-}
-
-__global__ void k_splitk_reduce(const float* __restrict__ ws, long long stride, int splits, int ld,
-                                EpiParams ep) {
-    pdl_wait();
-    const int npairs = (ep.n_out + 1) >> 1;
-    const long long total = (long long)ep.m_tok * npairs;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int t = static_cast<int>(idx / npairs);
-        const int n = static_cast<int>(idx % npairs) * 2;
-        const float* p = ws + (long long)t * ld + n;
-        float v0 = 0.f, v1 = 0.f;
-        const bool has1 = n + 1 < ep.n_out;
-        for (int z = 0; z < splits; ++z) {  // fixed order: deterministic
-            v0 += p[z * stride];
-            if (has1) v1 += p[z * stride + 1];
-        }
-        epi_pair(ep, t, n, v0, v1, 0);
     }
 }
 
@@ -393,66 +373,53 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     const int slots = num_sms() * ctas_per_sm;
     int splits = 1;
     if (tiles < slots) splits = std::max(1, std::min(slots / tiles, g.kb_total / 4));
+    // split-K CTAs of a tile form one cluster (portable size <= 8) and park
+    // their fp32 partial in the pipeline smem for the DSMEM reduction
+    splits = std::min(splits, kMaxSplits);
+    if (g.wm != 1 || g.stages * stage_bytes < bn * kBlockM * 4) splits = 1;
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
     g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
     return g;
 }
 
-constexpr long long kSplitCounters = 1 << 16;
-// per-device zeroed tile counters for the fused split-K finish (each last CTA
-// resets its counter, so the buffer stays zero between launches / replays)
-static int* split_counters() {
-    static int* ptrs[64] = {nullptr};
-    int dev = 0;
-    CUDA_CHECK(cudaGetDevice(&dev));
-    if (!ptrs[dev]) {
-        CUDA_CHECK(cudaMalloc(&ptrs[dev], sizeof(int) * kSplitCounters));
-        CUDA_CHECK(cudaMemset(ptrs[dev], 0, sizeof(int) * kSplitCounters));
-    }
-    return ptrs[dev];
-}
-
-void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep_in,
+void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep,
                  float* workspace, size_t workspace_elems, cudaStream_t st) {
+    (void)workspace;
+    (void)workspace_elems;
     static bool attr_set = false;
     if (!attr_set) {
         // 226 KB: leaves room for the kernel's few static shared words
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         attr_set = true;
     }
-    EpiParams ep = ep_in;
+    if (ep.kind == EPI_TOPK && g.splits > 1) throw CudaError("EPI_TOPK needs whole-K accumulators");
+    if (g.splits > kMaxSplits) throw CudaError("split-K cluster larger than the portable cluster size");
+    if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.bn * kBlockK * 2) < g.bn * kBlockM * 4))
+        throw CudaError("split-K partial does not fit the pipeline smem");
     dim3 grid(g.n_ttiles, g.n_wtiles, g.splits);
-    if (ep.kind == EPI_PARTIAL) {  // caller reduces (e.g. k_reduce_resid_norm)
-        ep.partial_stride = (long long)ep.m_tok * ep.n_out;
-        if ((size_t)(ep.partial_stride * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");
-        ep.ws = workspace;
-        ep.ws_ld = ep.n_out;
-        ep.counters = nullptr;
-        launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split, g.tmem_cols,
-                   g.wm, ep);
-        CUDA_CHECK(cudaGetLastError());
-        return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
     }
-    if (g.splits > 1) {
-        // fused split-K: partials + last-CTA reduction inside the same launch
-        const long long plane = (long long)ep.m_tok * ep.n_out;
-        if ((size_t)(plane * g.splits) > workspace_elems) throw CudaError("gemm split-K workspace too small");
-        if ((long long)g.n_ttiles * g.n_wtiles > kSplitCounters) throw CudaError("too many split-K tiles");
-        EpiParams pp = ep;
-        pp.kind = EPI_PARTIAL;
-        pp.final_kind = ep.kind;
-        pp.ws = workspace;
-        pp.ws_ld = ep.n_out;
-        pp.partial_stride = plane;
-        pp.counters = split_counters();
-        launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                   g.tmem_cols, g.wm, pp);
-    } else {
-        ep.counters = nullptr;
-        launch_pdl(k_gemm_swapab, grid, 192, g.smem, st, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                   g.tmem_cols, g.wm, ep);
-    }
-    CUDA_CHECK(cudaGetLastError());
+    // the split-K CTAs of one output tile form one cluster (DSMEM reduction)
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 1;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = g.splits;
+    ++na;
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_swapab, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
+                                       g.tmem_cols, g.wm, ep);
+    if (e != cudaSuccess) throw CudaError(std::string("gemm launch: ") + cudaGetErrorString(e));
 }
 
 }  // namespace tlt

@@ -10,7 +10,8 @@
 // once per token tile. Accumulators live in TMEM (128 lanes x BN fp32 columns),
 // operands arrive by TMA (128B swizzle) through an mbarrier ring, and one
 // elected thread issues tcgen05.mma. Epilogues (bias + RoPE + KV-cache write,
-// residual add, SwiGLU, fp32 store, split-K partial) are fused and read the
+// residual add, SwiGLU, fp32 store, LM-head top-k) are fused; split-K partials
+// are reduced inside a thread-block cluster through distributed shared memory and read the
 // accumulator with tcgen05.ld.
 #pragma once
 #include <cuda_bf16.h>
@@ -24,7 +25,6 @@ enum EpiKind : int {
     EPI_RESID_ADD = 2,  // out_f32[t][n] += acc  (fp32 residual stream)
     EPI_SWIGLU = 3,     // rows interleaved (gate, up): out_bf16[t][n/2] = bf16(silu(g) * u)
     EPI_QKV = 4,        // + bias, RoPE on q/k pairs, q -> out_bf16, k/v -> KV cache
-    EPI_PARTIAL = 5,    // split-K partial: out_f32[z][t][n] = acc
     EPI_TOPK = 6,       // LM head: per (128-vocab tile, token) max, sum-exp and top-k (logit desc, id asc)
 };
 
@@ -36,7 +36,6 @@ struct EpiParams {
     int ld_f32;
     __nv_bfloat16* out_bf16;
     int ld_bf16;
-    long long partial_stride;  // elements between split-K partial planes
     // EPI_QKV
     const __nv_bfloat16* bias;  // [n_out] or null
     const float* rope_cos;      // [max_pos][head_dim/2]
@@ -53,13 +52,6 @@ struct EpiParams {
     int max_ctx;
     // EPI_TOPK: out_f32 = partials [n_wtiles][m_tok][2 + 2*topk_k] (m, s, vals[k], ids[k])
     int topk_k;
-    // fused split-K: partials are written with EPI_PARTIAL, the last-arriving
-    // CTA of each tile (per-tile counter) reduces them in z order and applies
-    // final_kind — no separate reduce launch
-    int final_kind;
-    int* counters;
-    float* ws;  // EPI_PARTIAL destination: ws[split][t][n], row stride ws_ld
-    int ws_ld;
 };
 constexpr int kEpiTopkMax = 8;
 
@@ -72,11 +64,6 @@ __device__ __forceinline__ void epi_pair(const EpiParams& p, int t, int n, float
     switch (p.kind) {
         case EPI_F32: {
             float* o = p.out_f32 + (long long)t * p.ld_f32 + n;
-            o[0] = v0;
-            if (has1) o[1] = v1;
-        } break;
-        case EPI_PARTIAL: {
-            float* o = p.ws + split * p.partial_stride + (long long)t * p.ws_ld + n;
             o[0] = v0;
             if (has1) o[1] = v1;
         } break;

@@ -113,7 +113,8 @@ void launch_rmsnorm(const float* x, int R, int d, const bf16* g, float eps, bf16
 // Split-K reduce + residual add + RMSNorm of the updated row, one CTA per
 // token row (the O-proj / down-proj epilogue at long-tail batch sizes):
 //   x[r] += sum_z ws[z][r]   (fixed z order);  h[r] = bf16(x[r] * inv_rms * g)
-// Replaces k_splitk_reduce + k_rmsnorm (one launch and one pass over x).
+// splits == 0: RMSNorm only (the residual add already happened in the GEMM
+// epilogue), still spread over the cluster for the few-row long-tail case.
 // One 8-CTA thread-block cluster per token row: each CTA owns d/8 features
 // (so a single long-tail row still spreads over 8 SMs), the row's sum of
 // squares is combined through distributed shared memory in fixed rank order.
@@ -136,7 +137,7 @@ __global__ void __cluster_dims__(kNormCluster, 1, 1) __launch_bounds__(256)
         float v = 0.f;
         for (int z = 0; z < splits; ++z) v += wr[z * plane + i];
         const float nx = xr[i] + v;
-        xr[i] = nx;
+        if (splits) xr[i] = nx;
         ss += nx * nx;
     }
 #pragma unroll
