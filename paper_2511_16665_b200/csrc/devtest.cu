@@ -14,7 +14,7 @@ extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, 
             g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
         }
         CUtensorMap tw = make_tmap_bf16(w, n, k, k, 128);
-        CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.bn);
+        CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.box_rows);
         EpiParams ep{};
         ep.kind = kind;
         ep.n_out = n;
@@ -39,7 +39,7 @@ extern "C" TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void
     try {
         GemmPlan g = plan_gemm(m, n, k);
         CUtensorMap tw = make_tmap_bf16(w, n, k, k, 128);
-        CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.bn);
+        CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.box_rows);
         EpiParams ep{};
         ep.kind = kind;
         ep.n_out = n;

@@ -292,7 +292,7 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
         g.kb_per_split = g.kb_total;
         g.splits = 1;
     }
-    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.bn);
+    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.box_rows);
     EpiParams ep = ep_in;
     ep.n_out = N;
     ep.m_tok = M;
@@ -306,7 +306,7 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
 void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w) {
     const int d = cfg.hidden;
     GemmPlan g = plan_gemm(M, d, K);
-    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.bn);
+    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.box_rows);
     EpiParams e{};
     e.n_out = d;
     e.m_tok = M;

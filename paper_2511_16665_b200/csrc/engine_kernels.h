@@ -106,8 +106,7 @@ void launch_accept_stochastic(const StepIn* step, int b, int D, int V, double te
 void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int R, int d, float* x,
                               const __nv_bfloat16* g, float eps, __nv_bfloat16* out, cudaStream_t st);
 void launch_attention(const AttnParams& p, cudaStream_t st);
-void launch_row_topk(const float* logits, int R, int V, const int* live, int k, int need_sum, int* out_tok,
-                     float* out_logit, float* out_M, float* out_S, cudaStream_t st);
+
 int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, int k, float* part, cudaStream_t st);
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,
                        float* out_M, float* out_S, cudaStream_t st);

@@ -124,12 +124,54 @@ __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem
     }
 }
 
+
+__device__ __forceinline__ float* align16f(void* p) {
+    return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+}
+
+// Epilogue of one 128-row x bn-token accumulator tile (4 epilogue warps,
+// 128 threads, named barrier 1). Per 16-token chunk: TMEM -> registers ->
+// smem [16 tokens][128 rows] fp32 (lane = row: conflict-free), then every
+// thread applies the fused op to units of 8 consecutive rows of one token and
+// writes them with 16-byte stores (row-contiguous output, fully coalesced).
+__device__ __forceinline__ void epi_tile_staged(const EpiParams& ep, uint32_t acc, int q, int lane, int n0, int t0,
+                                                int bn, float* tr) {
+    const int ep_tid = threadIdx.x - 64;  // 0..127
+    for (int c = 0; c < bn; c += 16) {
+        if (t0 + c >= ep.m_tok) break;
+        float v[16];
+        tmem_ld16(acc + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tr[j * 128 + q * 32 + lane] = v[j];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int unit = ep_tid + 128 * u;  // 16 tokens x 16 row-octets
+            const int tk = unit >> 4, r8 = (unit & 15) * 8;
+            const float4 a = *reinterpret_cast<const float4*>(tr + tk * 128 + r8);
+            const float4 b = *reinterpret_cast<const float4*>(tr + tk * 128 + r8 + 4);
+            const float w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            epi_vec8(ep, t0 + c + tk, n0 + r8, w);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+}
+
+// PAIR == 2: a thread-block cluster of two CTAs on one TPC computes a
+// 256-row x bn-token tile with tcgen05.mma.cta_group::2 (M = 256): each CTA
+// stages its own 128 weight rows and HALF of the token tile, the leader CTA
+// issues the MMAs, each CTA's TMEM holds the accumulators of its 128 rows for
+// all bn tokens. Per SM this halves the token-operand smem traffic and the
+// L2->SMEM re-reads of the activations (the tensor-bound regime, M >~ 256).
+template <int PAIR>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_swapab(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                  int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, int wm, EpiParams ep) {
+                  int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, int wm, int l2pf,
+                  EpiParams ep) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int b_bytes = bn * kBlockK * 2;
+    const int b_rows = bn / PAIR;  // token rows staged by this CTA
+    const int b_bytes = b_rows * kBlockK * 2;
     const int a_bytes = wm * kABytes;  // wm weight sub-tiles of 128 rows share every token tile
     uint8_t* sA = smem;
     uint8_t* sB = smem + stages * a_bytes;
@@ -140,10 +182,11 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0u;
     // token tiles vary fastest: the CTAs sharing one weight tile run together,
     // so the weight tile is fetched from HBM once and re-read from L2
-    const int n0 = blockIdx.y * kBlockM * wm;
-    const int t0 = blockIdx.x * bn;
+    const int n0 = (blockIdx.y * PAIR + rank) * kBlockM * wm;
+    const int t0 = (blockIdx.x / PAIR) * bn;
     const int z = blockIdx.z;
     const int kb0 = z * kb_per_split;
     const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
@@ -159,63 +202,123 @@ __global__ void __launch_bounds__(192, 1)
         fence_barrier_init();
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_holder)),
-                     "r"(tmem_cols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (PAIR == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_holder)),
+                         "r"(tmem_cols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_holder)),
+                         "r"(tmem_cols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR == 2)
+        cluster_sync_all();  // peer barriers initialised before any cross-CTA signal
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+    // Weights do not depend on the previous kernel: the producer issues the
+    // weight tiles of the first pipeline stages BEFORE griddepcontrol.wait, so
+    // under PDL the weight stream overlaps the previous kernel's tail.
+    const int npre = min(stages, nkb);
+    const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+    const uint64_t pol_x = policy_evict_last();   // activations: re-read by every weight tile
+    const uint32_t full_bar0 = PAIR == 2 ? mapa_shared(smem_u32(&full[0]), 0) : 0u;
+    if (warp == 0 && lane == 0) {
+        // weight tiles beyond the smem ring: L2 prefetch l2pf k-blocks ahead
+        for (int i = npre; i < min(nkb, npre + l2pf); ++i)
+            for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, (kb0 + i) * kBlockK, n0 + a * kBlockM);
+        for (int i = 0; i < npre; ++i) {
+            const int kc = (kb0 + i) * kBlockK;
+            if (PAIR == 2) {
+                if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * (a_bytes + b_bytes));
+                tma_load_2d_pair(sA + i * a_bytes, &tmW, full_bar0 + 8u * i, kc, n0, pol_w);
+            } else {
+                mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
+                for (int a = 0; a < wm; ++a)
+                    tma_load_2d(sA + i * a_bytes + a * kABytes, &tmW, &full[i], kc, n0 + a * kBlockM, pol_w);
+            }
+        }
+    }
     pdl_wait();  // setup above overlaps the previous kernel's tail (PDL)
 
     if (warp == 0) {
-        // ---------------- TMA producer
-        if (elect_one()) {
-            const uint64_t pol_w = policy_evict_first();  // weights: streamed once
-            const uint64_t pol_x = policy_evict_last();   // activations: re-read by every weight tile
+        // ---------------- TMA producer (one per CTA; pair: both count on the leader's full barrier)
+        if (lane == 0) {
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % stages;
                 const uint32_t ph = (i / stages) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
                 const int kc = (kb0 + i) * kBlockK;
-                for (int a = 0; a < wm; ++a)
-                    tma_load_2d(sA + s * a_bytes + a * kABytes, &tmW, &full[s], kc, n0 + a * kBlockM, pol_w);
-                tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+                if (i < npre) {  // weight tile already in flight: activations only
+                    if (PAIR == 2)
+                        tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows, pol_x);
+                    else
+                        tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+                    continue;
+                }
+                if (i + l2pf < nkb)
+                    for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, kc + l2pf * kBlockK, n0 + a * kBlockM);
+                mbar_wait(&empty[s], ph ^ 1);
+                if (PAIR == 2) {
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
+                    tma_load_2d_pair(sA + s * a_bytes, &tmW, full_bar0 + 8u * s, kc, n0, pol_w);
+                    tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows, pol_x);
+                } else {
+                    mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
+                    for (int a = 0; a < wm; ++a)
+                        tma_load_2d(sA + s * a_bytes + a * kABytes, &tmW, &full[s], kc, n0 + a * kBlockM, pol_w);
+                    tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+                }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (single elected thread)
-        const uint32_t idesc = idesc_bf16_f32(kBlockM, bn);
-        for (int i = 0; i < nkb; ++i) {
-            const int s = i % stages;
-            const uint32_t ph = (i / stages) & 1;
-            mbar_wait(&full[s], ph);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint64_t db = sdesc_kmajor_sw128(sB + s * b_bytes);
-                for (int a = 0; a < wm; ++a) {
-                    const uint64_t da = sdesc_kmajor_sw128(sA + s * a_bytes + a * kABytes);
+        // ---------------- MMA issuer (single elected thread; pair: leader CTA only)
+        if (PAIR == 1 || rank == 0) {
+            const uint32_t idesc = idesc_bf16_f32(kBlockM * PAIR, bn);
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % stages;
+                const uint32_t ph = (i / stages) & 1;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t db = sdesc_kmajor_sw128(sB + s * b_bytes);
+                    for (int a = 0; a < wm; ++a) {
+                        const uint64_t da = sdesc_kmajor_sw128(sA + s * a_bytes + a * kABytes);
 #pragma unroll
-                    for (int kk = 0; kk < kBlockK / 16; ++kk) {
-                        // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
-                        tc_mma_bf16(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                        for (int kk = 0; kk < kBlockK / 16; ++kk) {
+                            // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
+                            if (ep.dbg & 1) continue;  // diagnostics: loads only
+                            if (PAIR == 2)
+                                tc_mma_bf16_pair(tmem, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                            else
+                                tc_mma_bf16(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                        }
+                    }
+                    if (PAIR == 2) {
+                        tc_commit_pair_mc(&empty[s], 0x3);
+                        if (i == nkb - 1) tc_commit_pair_mc(tfull, 0x3);
+                    } else {
+                        tc_commit(&empty[s]);
+                        if (i == nkb - 1) tc_commit(tfull);
                     }
                 }
-                tc_commit(&empty[s]);
-                if (i == nkb - 1) tc_commit(tfull);
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else {
         // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
         mbar_wait(tfull, 0);
         tc_fence_after();
         const int q = warp & 3;
-        if (gridDim.z > 1) {
+        if (ep.dbg & 2) {
+            // diagnostics: no epilogue
+        } else if (gridDim.z > 1) {
             // split-K: stage this CTA's fp32 partial in the (now idle) pipeline
             // smem, [token][128 weight rows]; the cluster reduces it below
             float* P = reinterpret_cast<float*>(smem);
@@ -234,27 +337,20 @@ __global__ void __launch_bounds__(192, 1)
         const int row = na + q * 32 + lane;
         const int n_even = row & ~1;
         if (ep.kind == EPI_TOPK) {
-            float* tr = reinterpret_cast<float*>(tmem_holder + 4);  // [16 cols][128 vocab rows]
-            const int tile = blockIdx.y * wm + a;
+            float* tr = align16f(tmem_holder + 4);  // [16 cols][128 vocab rows]
+            const int tile = (blockIdx.y * PAIR + rank) * wm + a;
             if (ep.topk_k <= 1)
                 epi_topk_tile<1>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
             else
                 epi_topk_tile<kEpiTopkMax>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
-        } else
-        for (int c = 0; c < bn; c += 16) {
-            if (t0 + c >= ep.m_tok) break;
-            float v[16];
-            tmem_ld16(tm_a + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
-                if ((lane & 1) == 0) epi_pair(ep, t0 + c + j, n_even, v[j], other, z);
-            }
+        } else {
+            epi_tile_staged(ep, tm_a, q, lane, na, t0, bn, align16f(tmem_holder + 4));
         }
+        (void)n_even;
         }  // a
         }
     }
-    if (gridDim.z > 1) {
+    if (gridDim.z > 1 && !(ep.dbg & 2)) {
         // Split-K finish inside the thread-block cluster (cluster = the
         // gridDim.z CTAs of one output tile): every CTA sums one contiguous
         // slice of (token, row-pair) elements over all peers' partials through
@@ -283,10 +379,223 @@ __global__ void __launch_bounds__(192, 1)
         cluster.sync();  // peers' smem stays alive until every remote read is done
     }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR == 2)
+        cluster_sync_all();
+    else
+        __syncthreads();
     if (warp == 1) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
-                     : "memory");
+        if (PAIR == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
+                         : "memory");
+    }
+}
+
+
+// ------------------------------------------------------------------ persistent
+// Persistent variant for the multi-wave regime (output tiles >= CTA slots):
+// one CTA (PAIR == 2: one CTA pair) per SM loops over output tiles
+// (token tile fastest, so co-running CTAs share weight tiles through L2).
+// The TMA producer streams k-blocks across tile boundaries without pausing;
+// the MMA issuer alternates between two TMEM accumulators, so the epilogue of
+// tile j (tcgen05.ld -> fused epilogue -> global) overlaps the mainloop of
+// tile j+1. Barriers: smem ring full/empty; per accumulator tfull (MMA ->
+// epilogue) and tempty (epilogue -> MMA, 4 warps per CTA of the pair arrive
+// on the leader's barrier).
+template <int PAIR>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_persist(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int bn,
+                   int stages, int kb_total, int n_ttiles, int n_tiles, uint32_t tmem_cols, EpiParams ep) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int b_rows = bn / PAIR;
+    const int b_bytes = b_rows * kBlockK * 2;
+    const int a_bytes = kABytes;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + stages * a_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + stages * b_bytes);
+    uint64_t* empty = full + stages;
+    uint64_t* tfull = empty + stages;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0u;
+    const int cid = blockIdx.x / PAIR, ncl = gridDim.x / PAIR;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4 * PAIR);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        if (PAIR == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_holder)),
+                         "r"(tmem_cols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_holder)),
+                         "r"(tmem_cols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+    }
+    tc_fence_before();
+    if (PAIR == 2)
+        cluster_sync_all();
+    else
+        __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const uint32_t full_bar0 = PAIR == 2 ? mapa_shared(smem_u32(&full[0]), 0) : 0u;
+    // first tile's weight stages before griddepcontrol.wait (weights are not
+    // produced by the previous kernel)
+    const int npre = (cid < n_tiles) ? min(stages, kb_total) : 0;
+    if (warp == 0 && lane == 0 && npre > 0) {
+        const int n0 = ((cid / n_ttiles) * PAIR + rank) * kBlockM;
+        for (int i = 0; i < npre; ++i) {
+            if (PAIR == 2) {
+                if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * (a_bytes + b_bytes));
+                tma_load_2d_pair(sA + i * a_bytes, &tmW, full_bar0 + 8u * i, i * kBlockK, n0, pol_w);
+            } else {
+                mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
+                tma_load_2d(sA + i * a_bytes, &tmW, &full[i], i * kBlockK, n0, pol_w);
+            }
+        }
+    }
+    pdl_wait();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int t = cid; t < n_tiles; t += ncl) {
+                const int n0 = ((t / n_ttiles) * PAIR + rank) * kBlockM;
+                const int t0 = (t % n_ttiles) * bn;
+                for (int kb = 0; kb < kb_total; ++kb, ++it) {
+                    const int s = it % stages;
+                    const uint32_t ph = (it / stages) & 1;
+                    const int kc = kb * kBlockK;
+                    if (it < npre) {  // weight tile already in flight
+                        if (PAIR == 2)
+                            tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows,
+                                             pol_x);
+                        else
+                            tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+                        continue;
+                    }
+                    mbar_wait(&empty[s], ph ^ 1);
+                    if (PAIR == 2) {
+                        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
+                        tma_load_2d_pair(sA + s * a_bytes, &tmW, full_bar0 + 8u * s, kc, n0, pol_w);
+                        tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows,
+                                         pol_x);
+                    } else {
+                        mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
+                        tma_load_2d(sA + s * a_bytes, &tmW, &full[s], kc, n0, pol_w);
+                        tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (PAIR == 1 || rank == 0) {
+            const uint32_t idesc = idesc_bf16_f32(kBlockM * PAIR, bn);
+            int it = 0, j = 0;
+            for (int t = cid; t < n_tiles; t += ncl, ++j) {
+                const int b = j & 1;
+                mbar_wait(&tempty[b], ((j >> 1) & 1) ^ 1);  // accumulator b drained by the epilogue
+                tc_fence_after();
+                const uint32_t acc = tmem + b * bn;
+                for (int kb = 0; kb < kb_total; ++kb, ++it) {
+                    const int s = it % stages;
+                    const uint32_t ph = (it / stages) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint64_t da = sdesc_kmajor_sw128(sA + s * a_bytes);
+                        const uint64_t db = sdesc_kmajor_sw128(sB + s * b_bytes);
+#pragma unroll
+                        for (int kk = 0; kk < kBlockK / 16; ++kk) {
+                            if (ep.dbg & 1) continue;
+                            if (PAIR == 2)
+                                tc_mma_bf16_pair(acc, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) != 0);
+                            else
+                                tc_mma_bf16(acc, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) != 0);
+                        }
+                        if (PAIR == 2) {
+                            tc_commit_pair_mc(&empty[s], 0x3);
+                            if (kb == kb_total - 1) tc_commit_pair_mc(&tfull[b], 0x3);
+                        } else {
+                            tc_commit(&empty[s]);
+                            if (kb == kb_total - 1) tc_commit(&tfull[b]);
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        // epilogue warps 2..5: TMEM lane quarter q = warp % 4
+        const int q = warp & 3;
+        float* tr = align16f(tmem_holder + 4);  // EPI_TOPK transpose scratch
+        const uint32_t tempty_leader = PAIR == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        int j = 0;
+        for (int t = cid; t < n_tiles; t += ncl, ++j) {
+            const int b = j & 1;
+            const int n0 = ((t / n_ttiles) * PAIR + rank) * kBlockM;
+            const int t0 = (t % n_ttiles) * bn;
+            mbar_wait(&tfull[b], (j >> 1) & 1);
+            tc_fence_after();
+            const uint32_t acc = tmem + b * bn;
+            if (!(ep.dbg & 2) && n0 < ep.n_out) {
+                if (ep.kind == EPI_TOPK) {
+                    const int tile = (t / n_ttiles) * PAIR + rank;
+                    if (ep.topk_k <= 1)
+                        epi_topk_tile<1>(ep, acc, q, lane, n0, t0, bn, tr, tile);
+                    else
+                        epi_topk_tile<kEpiTopkMax>(ep, acc, q, lane, n0, t0, bn, tr, tile);
+                } else {
+                    epi_tile_staged(ep, acc, q, lane, n0, t0, bn, tr);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (PAIR == 2)
+                    mbar_arrive_cluster(tempty_leader + 8u * b);
+                else
+                    mbar_arrive(&tempty[b]);
+            }
+        }
+    }
+    tc_fence_before();
+    if (PAIR == 2)
+        cluster_sync_all();
+    else
+        __syncthreads();
+    if (warp == 1) {
+        if (PAIR == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
+                         : "memory");
     }
 }
 
@@ -336,8 +645,61 @@ static int env_knob(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
+int gemm_dbg_flags() {
+    static const int f = env_knob("TLT_GEMM_DBG", 0);
+    return f;
+}
+
 GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     GemmPlan g;
+    static const int l2pf = env_knob("TLT_GEMM_L2PF", 0);
+    g.l2pf = l2pf;
+    g.kb_total = (k + kBlockK - 1) / kBlockK;
+    const int fixed = 1024 + 16 * 8 + 64 + 16 * 128 * 4;
+    // Tensor-bound regime: CTA pairs (cta_group::2, 256 weight rows x up to
+    // 256 tokens per pair), no split-K.
+    static const int pair_min_m = env_knob("TLT_GEMM_PAIR_MIN_M", 192);
+    static const int pair_bn_max = env_knob("TLT_GEMM_PAIR_BN_MAX", 256);
+    static const int pair_cps = env_knob("TLT_GEMM_PAIR_CPS", 2);
+    // 1: persistent kernel for CTA-pair plans; 2: also for single-CTA plans
+    // measured (profiles/r1_gemm_knobs_*.txt): with the staged epilogue the
+    // 2-CTA/SM non-persistent kernel wins below ~768 tokens, the persistent
+    // CTA-pair kernel above; the single-CTA persistent kernel never wins
+    static const int persist = env_knob("TLT_GEMM_PERSIST", 1);
+    static const int pair_persist_min_m = env_knob("TLT_GEMM_PAIR_PERSIST_MIN_M", 768);
+    static const int persist1_min_m = env_knob("TLT_GEMM_PERSIST1_MIN_M", 48);
+    // pairs only when they still put >= 1 CTA on every SM (else the 1-CTA
+    // plan with in-cluster split-K fills the machine better)
+    const int pair_ctas = 2 * ((n_out + 2 * kBlockM - 1) / (2 * kBlockM)) * ((m_tok + pair_bn_max - 1) / pair_bn_max);
+    if (pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas >= num_sms()) {
+        g.pair = 2;
+        g.wm = 1;
+        const int n_tt = (m_tok + pair_bn_max - 1) / pair_bn_max;
+        int bn = (m_tok + n_tt - 1) / n_tt;
+        bn = std::max(32, (bn + 15) / 16 * 16);
+        g.bn = bn;
+        g.box_rows = bn / 2;
+        g.n_ttiles = (m_tok + bn - 1) / bn;
+        g.n_wtiles = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
+        const int stage_bytes = kABytes + g.box_rows * kBlockK * 2;
+        g.kb_per_split = g.kb_total;
+        g.splits = 1;
+        if (persist >= 1 && m_tok >= pair_persist_min_m) {
+            // persistent: one pair per 2 SMs, full smem ring, 2 TMEM accumulators
+            const int pfixed = 1024 + 32 * 8 + 16 + 16 * 128 * 4;
+            g.persist = 1;
+            g.stages = std::max(2, std::min(12, (220 * 1024 - pfixed) / stage_bytes));
+            g.smem = g.stages * stage_bytes + pfixed;
+            const int cols = 2 * bn;
+            g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+            return g;
+        }
+        const int budget = (pair_cps == 2 ? 112 * 1024 : 220 * 1024) - fixed;
+        g.stages = std::max(2, std::min(8, budget / stage_bytes));
+        g.smem = g.stages * stage_bytes + fixed;
+        g.tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+        return g;
+    }
     // Measured on B200 (tools/gemm_sweep.sh, profiles/): two co-resident CTAs
     // per SM (one's epilogue/prologue overlapping the other's mainloop) beat
     // deeper pipelines and larger tiles: token tiles <= 128, <= ~110 KB smem.
@@ -348,21 +710,15 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     int bn = (m_tok + n_ttiles - 1) / n_ttiles;
     bn = std::max(16, (bn + 15) / 16 * 16);
     g.bn = bn;
+    g.box_rows = bn;
     g.n_ttiles = (m_tok + bn - 1) / bn;
-    g.kb_total = (k + kBlockK - 1) / kBlockK;
-    // Tensor-bound regime (many tokens): two 128-row weight sub-tiles per CTA
-    // share each staged token tile (halves the L2->SMEM re-reads of the
-    // activations), as long as there are still >= one CTA per SM.
-    const int wtiles2 = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
     g.wm = 1;  // 2 measured slower at every shape (fewer co-resident CTAs); kept behind TLT_GEMM_WM
-    (void)wtiles2;
     if (force_wm) g.wm = force_wm;
     g.n_wtiles = (n_out + kBlockM * g.wm - 1) / (kBlockM * g.wm);
     const int stage_bytes = g.wm * kABytes + bn * kBlockK * 2;
     const int ctas_per_sm = (bn <= 128 && g.wm == 1) ? 2 : 1;
     // per-CTA budget incl. barriers, alignment slack and the EPI_TOPK merge
     // scratch, so that 2 CTAs/SM really fit in the 228 KB SM carve-out
-    const int fixed = 1024 + 16 * 8 + 64 + 16 * 128 * 4;
     const int budget = (ctas_per_sm == 2 ? 112 * 1024 : 220 * 1024) - fixed;
     g.stages = std::max(2, std::min(8, budget / stage_bytes));
     if (force_stages) g.stages = std::min(force_stages, std::max(2, (220 * 1024 - fixed) / stage_bytes));
@@ -379,6 +735,14 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     if (g.wm != 1 || g.stages * stage_bytes < bn * kBlockM * 4) splits = 1;
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
     g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+    if (g.splits == 1 && persist >= 2 && g.wm == 1 && m_tok >= persist1_min_m) {
+        const int pfixed = 1024 + 32 * 8 + 16 + 16 * 128 * 4;
+        g.persist = 1;
+        g.stages = std::max(2, std::min(12, (220 * 1024 - pfixed) / stage_bytes));
+        g.smem = g.stages * stage_bytes + pfixed;
+        const int c2 = 2 * bn;
+        g.tmem_cols = c2 <= 32 ? 32 : c2 <= 64 ? 64 : c2 <= 128 ? 128 : c2 <= 256 ? 256 : 512;
+    }
     return g;
 }
 
@@ -389,14 +753,52 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     static bool attr_set = false;
     if (!attr_set) {
         // 226 KB: leaves room for the kernel's few static shared words
-        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         attr_set = true;
     }
     if (ep.kind == EPI_TOPK && g.splits > 1) throw CudaError("EPI_TOPK needs whole-K accumulators");
     if (g.splits > kMaxSplits) throw CudaError("split-K cluster larger than the portable cluster size");
+    if (g.pair == 2 && (g.splits != 1 || g.wm != 1 || g.bn % 16 || g.bn < 32 || g.bn > 256))
+        throw CudaError("invalid CTA-pair GEMM plan");
     if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.bn * kBlockK * 2) < g.bn * kBlockM * 4))
         throw CudaError("split-K partial does not fit the pipeline smem");
-    dim3 grid(g.n_ttiles, g.n_wtiles, g.splits);
+    dim3 grid(g.n_ttiles * g.pair, g.n_wtiles, g.splits);
+    EpiParams epd = ep;
+    epd.dbg = gemm_dbg_flags();
+    if (g.persist) {
+        static bool pattr = false;
+        if (!pattr) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_gemm_persist<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+            CUDA_CHECK(cudaFuncSetAttribute(k_gemm_persist<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+            pattr = true;
+        }
+        const int n_tiles = g.n_ttiles * g.n_wtiles;
+        const int groups = std::min(n_tiles, num_sms() / g.pair);
+        cudaLaunchConfig_t pc = {};
+        pc.gridDim = dim3(groups * g.pair, 1, 1);
+        pc.blockDim = dim3(192);
+        pc.dynamicSmemBytes = g.smem;
+        pc.stream = st;
+        cudaLaunchAttribute pa[2];
+        int npa = 0;
+        if (pdl_enabled()) {
+            pa[npa].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            pa[npa].val.programmaticStreamSerializationAllowed = 1;
+            ++npa;
+        }
+        pa[npa].id = cudaLaunchAttributeClusterDimension;
+        pa[npa].val.clusterDim.x = g.pair;
+        pa[npa].val.clusterDim.y = 1;
+        pa[npa].val.clusterDim.z = 1;
+        ++npa;
+        pc.attrs = pa;
+        pc.numAttrs = npa;
+        cudaError_t e = cudaLaunchKernelEx(&pc, g.pair == 2 ? k_gemm_persist<2> : k_gemm_persist<1>, tmW, tmX, g.bn,
+                                           g.stages, g.kb_total, g.n_ttiles, n_tiles, g.tmem_cols, epd);
+        if (e != cudaSuccess) throw CudaError(std::string("gemm launch: ") + cudaGetErrorString(e));
+        return;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(192);
@@ -409,16 +811,17 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         at[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
     }
-    // the split-K CTAs of one output tile form one cluster (DSMEM reduction)
+    // the split-K CTAs of one output tile form one cluster (DSMEM reduction);
+    // CTA pairs are (2, 1, 1) clusters
     at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = 1;
+    at[na].val.clusterDim.x = g.pair;
     at[na].val.clusterDim.y = 1;
     at[na].val.clusterDim.z = g.splits;
     ++na;
     cfg.attrs = at;
     cfg.numAttrs = na;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_swapab, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                                       g.tmem_cols, g.wm, ep);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, g.pair == 2 ? k_gemm_swapab<2> : k_gemm_swapab<1>, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
+                                       g.tmem_cols, g.wm, g.l2pf, epd);
     if (e != cudaSuccess) throw CudaError(std::string("gemm launch: ") + cudaGetErrorString(e));
 }
 

@@ -52,6 +52,7 @@ struct EpiParams {
     int max_ctx;
     // EPI_TOPK: out_f32 = partials [n_wtiles][m_tok][2 + 2*topk_k] (m, s, vals[k], ids[k])
     int topk_k;
+    int dbg;  // diagnostics (TLT_GEMM_DBG): bit0 skip MMA, bit1 skip epilogue
 };
 constexpr int kEpiTopkMax = 8;
 
@@ -110,6 +111,97 @@ __device__ __forceinline__ void epi_pair(const EpiParams& p, int t, int n, float
                 __nv_bfloat16* dst = (is_k ? p.kcache : p.vcache) + off;
                 *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
             }
+        } break;
+    }
+}
+
+
+// Vectorised epilogue for the 8 consecutive output rows n..n+7 (n % 8 == 0)
+// of token t, v[] = fp32 accumulators (rows interleaved exactly as the weight
+// rows). Rows >= n_out are dropped. One 16-byte (bf16) or 2x16-byte (fp32)
+// store per call where the layout allows it.
+__device__ __forceinline__ void epi_vec8(const EpiParams& p, int t, int n, const float (&v)[8]) {
+    if (t >= p.m_tok || n >= p.n_out) return;
+    if (n + 8 > p.n_out) {  // ragged tail: scalar pairs
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) epi_pair(p, t, n + i, v[i], v[i + 1], 0);
+        return;
+    }
+    switch (p.kind) {
+        case EPI_F32: {
+            float4* o = reinterpret_cast<float4*>(p.out_f32 + (long long)t * p.ld_f32 + n);
+            o[0] = make_float4(v[0], v[1], v[2], v[3]);
+            o[1] = make_float4(v[4], v[5], v[6], v[7]);
+        } break;
+        case EPI_RESID_ADD: {
+            float4* o = reinterpret_cast<float4*>(p.out_f32 + (long long)t * p.ld_f32 + n);
+            float4 a = o[0], b = o[1];
+            a.x += v[0]; a.y += v[1]; a.z += v[2]; a.w += v[3];
+            b.x += v[4]; b.y += v[5]; b.z += v[6]; b.w += v[7];
+            o[0] = a;
+            o[1] = b;
+        } break;
+        case EPI_BF16: {
+            uint4 u;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            *reinterpret_cast<uint4*>(p.out_bf16 + (long long)t * p.ld_bf16 + n) = u;
+        } break;
+        case EPI_SWIGLU: {
+            uint2 u;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+            h2[0] = __floats2bfloat162_rn(silu_f(v[0]) * v[1], silu_f(v[2]) * v[3]);
+            h2[1] = __floats2bfloat162_rn(silu_f(v[4]) * v[5], silu_f(v[6]) * v[7]);
+            *reinterpret_cast<uint2*>(p.out_bf16 + (long long)t * p.ld_bf16 + (n >> 1)) = u;
+        } break;
+        case EPI_QKV: {
+            float w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = v[i];
+            if (p.bias) {
+                const uint4 bu = *reinterpret_cast<const uint4*>(p.bias + n);
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bu);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f = __bfloat1622float2(b2[i]);
+                    w[2 * i] += f.x;
+                    w[2 * i + 1] += f.y;
+                }
+            }
+            const int hd = p.head_dim;
+            if (n < p.n_q + p.n_kvr) {  // q or k: rotate the (2i, 2i+1) pairs
+                const int i0 = (n % hd) >> 1;
+                const long long rb = (long long)p.tok_pos[t] * (hd >> 1) + i0;
+                const float4 c = *reinterpret_cast<const float4*>(p.rope_cos + rb);
+                const float4 s = *reinterpret_cast<const float4*>(p.rope_sin + rb);
+                const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float a = w[2 * i], b = w[2 * i + 1];
+                    w[2 * i] = a * cc[i] - b * ss[i];
+                    w[2 * i + 1] = a * ss[i] + b * cc[i];
+                }
+            }
+            uint4 u;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+            if (n < p.n_q) {
+                *reinterpret_cast<uint4*>(p.out_bf16 + (long long)t * p.ld_bf16 + n) = u;
+            } else {
+                const int slot = p.tok_slot[t];
+                if (slot < 0) return;
+                const bool is_k = n < p.n_q + p.n_kvr;
+                const int r = n - p.n_q - (is_k ? 0 : p.n_kvr);
+                const int h = r / hd, dd = r % hd;
+                const long long off = (((long long)slot * p.n_kv + h) * p.max_ctx + p.tok_cidx[t]) * hd + dd;
+                *reinterpret_cast<uint4*>((is_k ? p.kcache : p.vcache) + off) = u;
+            }
+        } break;
+        default: {
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) epi_pair(p, t, n + i, v[i], v[i + 1], 0);
         } break;
     }
 }

@@ -404,189 +404,178 @@ void launch_attention(const AttnParams& p, cudaStream_t st) {
 }
 
 // ------------------------------------------------------- row top-k / argmax
-// Per row: top-k by (logit desc, id asc) — the reference child order
-// (stable_sort over ascending id, spec_decode.hpp:121-125) — plus the row max
-// M and, when need_sum, S = sum_i expf(l_i - M) (fixed reduction order).
+// Top-k by (logit desc, id asc) — the reference child order (stable_sort over
+// ascending id, spec_decode.hpp:121-125) — plus the row max M and
+// S = sum_i exp(l_i - M). Everything stays in registers: per-thread sorted
+// K-lists with static-index insertion, then K rounds of warp arg-max
+// (shuffle butterfly over a strict total order, so every lane agrees) and one
+// more warp merge over the per-warp lists. (m, s) pairs are combined with
+// max-rescaling in a fixed order: deterministic.
 template <int K>
 struct TopK {
     float v[K];
     int id[K];
-    __device__ void init() {
+    __device__ __forceinline__ void init() {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             v[i] = -CUDART_INF_F;
             id[i] = 0x7fffffff;
         }
     }
-    __device__ static bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
-    __device__ void push(float x, int ix) {
+    __device__ __forceinline__ static bool better(float a, int ia, float b, int ib) {
+        return a > b || (a == b && ia < ib);
+    }
+    __device__ __forceinline__ void push(float x, int ix) {
         if (!better(x, ix, v[K - 1], id[K - 1])) return;
-        int p = K - 1;
-        while (p > 0 && better(x, ix, v[p - 1], id[p - 1])) {
-            v[p] = v[p - 1];
-            id[p] = id[p - 1];
-            --p;
+        bool placed = false;
+#pragma unroll
+        for (int s = K - 1; s > 0; --s) {
+            const bool shift = !placed && better(x, ix, v[s - 1], id[s - 1]);
+            const bool put = !placed && !shift;
+            const float nv = shift ? v[s - 1] : (put ? x : v[s]);
+            const int ni = shift ? id[s - 1] : (put ? ix : id[s]);
+            v[s] = nv;
+            id[s] = ni;
+            placed = placed || put;
         }
-        v[p] = x;
-        id[p] = ix;
+        if (!placed) {
+            v[0] = x;
+            id[0] = ix;
+        }
+    }
+    // After the call every lane holds the warp's top-K (sorted).
+    __device__ __forceinline__ void warp_merge() {
+        float ov[K];
+        int oi[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            float bv = v[0];
+            int bi = id[0];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float xv = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int xi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (better(xv, xi, bv, bi)) {
+                    bv = xv;
+                    bi = xi;
+                }
+            }
+            ov[r] = bv;
+            oi[r] = bi;
+            if (id[0] == bi && v[0] == bv) {  // this lane's head won: pop it
+#pragma unroll
+                for (int s = 0; s < K - 1; ++s) {
+                    v[s] = v[s + 1];
+                    id[s] = id[s + 1];
+                }
+                v[K - 1] = -CUDART_INF_F;
+                id[K - 1] = 0x7fffffff;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            v[r] = ov[r];
+            id[r] = oi[r];
+        }
     }
 };
 
-template <int K>
-__global__ void __launch_bounds__(256) k_row_topk(const float* __restrict__ logits, int V, const int* __restrict__ live,
-                                                  int k, int need_sum, int* __restrict__ out_tok,
-                                                  float* __restrict__ out_logit, float* __restrict__ out_M,
-                                                  float* __restrict__ out_S) {
-    pdl_wait();
-    __shared__ float sv[256][K];
-    __shared__ int si[256][K];
-    __shared__ float red[8];
-    const int r = blockIdx.x;
-    if (live && live[r] < 0) return;
-    const float* lr = logits + (long long)r * V;
-    TopK<K> t;
-    t.init();
-    for (int i = threadIdx.x; i < V; i += blockDim.x) t.push(lr[i], i);
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        sv[threadIdx.x][j] = t.v[j];
-        si[threadIdx.x][j] = t.id[j];
-    }
-    __syncthreads();
-    // pairwise merges of sorted K-lists: 256 -> 1
-    for (int stride = 1; stride < 256; stride <<= 1) {
-        if ((threadIdx.x % (2 * stride)) == 0) {
-            const int a = threadIdx.x, b = threadIdx.x + stride;
-            float mv[K];
-            int mi[K];
-            int ia = 0, ib = 0;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                const bool take_a = TopK<K>::better(sv[a][ia], si[a][ia], sv[b][ib], si[b][ib]);
-                mv[j] = take_a ? sv[a][ia] : sv[b][ib];
-                mi[j] = take_a ? si[a][ia] : si[b][ib];
-                if (take_a) ++ia; else ++ib;
-            }
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                sv[a][j] = mv[j];
-                si[a][j] = mi[j];
-            }
-        }
-        __syncthreads();
-    }
-    const float M = sv[0][0];
-    if (threadIdx.x < k) {
-        out_tok[(long long)r * k + threadIdx.x] = si[0][threadIdx.x];
-        out_logit[(long long)r * k + threadIdx.x] = sv[0][threadIdx.x];
-    }
-    if (threadIdx.x == 0 && out_M) out_M[r] = M;
-    if (!need_sum) return;
-    float s = 0.f;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) s += expf(lr[i] - M);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float tot = 0.f;
-        for (int w = 0; w < 8; ++w) tot += red[w];
-        out_S[r] = tot;
+// online (max, sum-exp) pair
+__device__ __forceinline__ void ms_add(float& m, float& s, float x) {
+    if (x > m) {
+        s = (m == -CUDART_INF_F ? 0.f : s * __expf(m - x)) + 1.f;
+        m = x;
+    } else if (x != -CUDART_INF_F) {
+        s += __expf(x - m);
     }
 }
+__device__ __forceinline__ void ms_merge(float& m, float& s, float om, float os) {
+    const float nm = fmaxf(m, om);
+    const float a = m == -CUDART_INF_F ? 0.f : s * __expf(m - nm);
+    const float b = om == -CUDART_INF_F ? 0.f : os * __expf(om - nm);
+    m = nm;
+    s = a + b;
+}
 
-void launch_row_topk(const float* logits, int R, int V, const int* live, int k, int need_sum, int* out_tok,
-                     float* out_logit, float* out_M, float* out_S, cudaStream_t st) {
-    if (k <= 1)
-        launch_pdl(k_row_topk<1>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
-    else if (k <= 2)
-        launch_pdl(k_row_topk<2>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
-    else if (k <= 4)
-        launch_pdl(k_row_topk<4>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
-    else
-        launch_pdl(k_row_topk<8>, R, 256, 0, st, logits, V, live, k, need_sum, out_tok, out_logit, out_M, out_S);
+// Block-level finish (256 threads = 8 warps): warp merges, then warp 0 merges
+// the 8 per-warp lists. Result (top-K, M, S) valid in warp 0 afterwards.
+template <int K>
+__device__ __forceinline__ void block_topk_finish(TopK<K>& t, float& m, float& s, float* sv, int* si, float* sm,
+                                                  float* ss) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, m, o);
+        const float os = __shfl_xor_sync(0xffffffffu, s, o);
+        ms_merge(m, s, om, os);
+    }
+    t.warp_merge();
+    if (lane == 0) {
+        sm[warp] = m;
+        ss[warp] = s;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            sv[warp * K + r] = t.v[r];
+            si[warp * K + r] = t.id[r];
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        t.init();
+        for (int e = lane; e < 8 * K; e += 32) t.push(sv[e], si[e]);
+        t.warp_merge();
+        m = sm[0];
+        s = ss[0];
+        for (int w = 1; w < 8; ++w) ms_merge(m, s, sm[w], ss[w]);  // fixed warp order
+    }
 }
 
 // Stage 1 of the multi-CTA row top-k (k > 1) over materialized logits: CTA
-// (chunk c, row r) reduces a 4096-entry chunk to the same partial record the
+// (chunk c, row r) reduces an 8192-entry chunk to the same partial record the
 // EPI_TOPK epilogue writes (chunk max m, sum exp(l - m), sorted top-k), so
 // k_topk_merge finishes both. Chunk order is fixed -> deterministic.
-constexpr int kTopkChunk = 4096;
+constexpr int kTopkChunk = 8192;
 template <int K>
 __global__ void __launch_bounds__(256) k_row_topk_chunk(const float* __restrict__ logits, int V, const int* live,
                                                         int k, float* __restrict__ part, int R) {
     pdl_wait();
-    __shared__ float sv[256][K];
-    __shared__ int si[256][K];
-    __shared__ float red[8];
-    __shared__ float sM;
+    __shared__ float sv[8 * K];
+    __shared__ int si[8 * K];
+    __shared__ float sm[8], ss[8];
     const int c = blockIdx.x, r = blockIdx.y;
     if (live && live[r] < 0) return;
     const float* lr = logits + (long long)r * V;
     const int i0 = c * kTopkChunk, i1 = min(V, i0 + kTopkChunk);
     TopK<K> t;
     t.init();
-    float m = -CUDART_INF_F;
-    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        const float x = lr[i];
-        m = fmaxf(m, x);
-        t.push(x, i);
-    }
+    float m = -CUDART_INF_F, s = 0.f;
+    for (int base = i0 + threadIdx.x; base < i1; base += 256 * 8) {
+        float x[8];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float M = red[0];
-        for (int w = 1; w < 8; ++w) M = fmaxf(M, red[w]);
-        sM = M;
-    }
-    __syncthreads();
-    const float M = sM;
-    float s = 0.f;
-    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) s += __expf(lr[i] - M);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        sv[threadIdx.x][j] = t.v[j];
-        si[threadIdx.x][j] = t.id[j];
-    }
-    __syncthreads();
-    for (int stride = 1; stride < 256; stride <<= 1) {
-        if ((threadIdx.x % (2 * stride)) == 0) {
-            const int a = threadIdx.x, b = threadIdx.x + stride;
-            float mv[K];
-            int mi[K];
-            int ia = 0, ib = 0;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                const bool take_a = TopK<K>::better(sv[a][ia], si[a][ia], sv[b][ib], si[b][ib]);
-                mv[j] = take_a ? sv[a][ia] : sv[b][ib];
-                mi[j] = take_a ? si[a][ia] : si[b][ib];
-                if (take_a) ++ia; else ++ib;
-            }
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                sv[a][j] = mv[j];
-                si[a][j] = mi[j];
-            }
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + u * 256;
+            x[u] = i < i1 ? __ldcs(lr + i) : -CUDART_INF_F;  // streamed once
         }
-        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            ms_add(m, s, x[u]);
+            t.push(x[u], base + u * 256);
+        }
     }
+    block_topk_finish<K>(t, m, s, sv, si, sm, ss);
     const int W = 2 + 2 * k;
     float* out = part + ((long long)c * R + r) * W;
     if (threadIdx.x == 0) {
-        float tot = 0.f;
-        for (int w = 0; w < 8; ++w) tot += red[w];
-        out[0] = M;
-        out[1] = tot;
+        out[0] = m;
+        out[1] = s;
     }
-    if (threadIdx.x < k) {
-        out[2 + threadIdx.x] = sv[0][threadIdx.x];
-        out[2 + k + threadIdx.x] = __int_as_float(si[0][threadIdx.x]);
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (threadIdx.x == j && j < k) {
+                out[2 + j] = t.v[j];
+                out[2 + k + j] = __int_as_float(t.id[j]);
+            }
     }
 }
 int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, int k, float* part, cudaStream_t st) {
@@ -601,88 +590,41 @@ int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, 
     return nch;
 }
 
-// Merge of the LM-head epilogue partials (EPI_TOPK): per token row, over the
-// 128-vocab tiles in fixed order: M = max m_t, S = sum s_t exp(m_t - M), and
-// top-k of the per-tile sorted candidate lists by (logit desc, id asc).
+// Merge of the partial records (LM-head EPI_TOPK tiles or top-k chunks) of
+// each row, one CTA per row: M and S by max-rescaled combination in a fixed
+// order, top-k of the per-tile sorted candidate lists by (logit desc, id asc).
 template <int K>
 __global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ part, int n_tiles, int m_tok, int k,
                                                     const int* __restrict__ live, int* __restrict__ out_tok,
                                                     float* __restrict__ out_logit, float* __restrict__ out_M,
                                                     float* __restrict__ out_S) {
     pdl_wait();
-    __shared__ float sv[256][K];
-    __shared__ int si[256][K];
-    __shared__ float red[8];
-    __shared__ float sM;
+    __shared__ float sv[8 * K];
+    __shared__ int si[8 * K];
+    __shared__ float sm[8], ss[8];
     const int r = blockIdx.x;
     if (live && live[r] < 0) return;
     const int W = 2 + 2 * k;
-    float m = -CUDART_INF_F;
+    float m = -CUDART_INF_F, s = 0.f;
     TopK<K> t;
     t.init();
     for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
         const float* pp = part + ((long long)i * m_tok + r) * W;
-        m = fmaxf(m, pp[0]);
+        ms_merge(m, s, pp[0], pp[1]);
         for (int c = 0; c < k; ++c) t.push(pp[2 + c], __float_as_int(pp[2 + k + c]));
     }
+    block_topk_finish<K>(t, m, s, sv, si, sm, ss);
+    if (threadIdx.x < 32) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float M = red[0];
-        for (int w = 1; w < 8; ++w) M = fmaxf(M, red[w]);
-        sM = M;
-    }
-    __syncthreads();
-    const float M = sM;
-    float s = 0.f;
-    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
-        const float* pp = part + ((long long)i * m_tok + r) * W;
-        if (pp[0] != -CUDART_INF_F) s += pp[1] * __expf(pp[0] - M);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        sv[threadIdx.x][j] = t.v[j];
-        si[threadIdx.x][j] = t.id[j];
-    }
-    __syncthreads();
-    for (int stride = 1; stride < 256; stride <<= 1) {
-        if ((threadIdx.x % (2 * stride)) == 0) {
-            const int a = threadIdx.x, b = threadIdx.x + stride;
-            float mv[K];
-            int mi[K];
-            int ia = 0, ib = 0;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                const bool take_a = TopK<K>::better(sv[a][ia], si[a][ia], sv[b][ib], si[b][ib]);
-                mv[j] = take_a ? sv[a][ia] : sv[b][ib];
-                mi[j] = take_a ? si[a][ia] : si[b][ib];
-                if (take_a) ++ia; else ++ib;
+        for (int j = 0; j < K; ++j)
+            if (threadIdx.x == j && j < k) {
+                out_tok[(long long)r * k + j] = t.id[j];
+                out_logit[(long long)r * k + j] = t.v[j];
             }
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                sv[a][j] = mv[j];
-                si[a][j] = mi[j];
-            }
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x < k) {
-        out_tok[(long long)r * k + threadIdx.x] = si[0][threadIdx.x];
-        out_logit[(long long)r * k + threadIdx.x] = sv[0][threadIdx.x];
     }
     if (threadIdx.x == 0) {
-        if (out_M) out_M[r] = M;
-        if (out_S) {
-            float tot = 0.f;
-            for (int w = 0; w < 8; ++w) tot += red[w];
-            out_S[r] = tot;
-        }
+        if (out_M) out_M[r] = m;
+        if (out_S) out_S[r] = s;
     }
 }
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,

@@ -38,6 +38,10 @@ struct GemmPlan {
     int smem = 0;
     unsigned tmem_cols = 32;
     int wm = 1;  // 128-row weight sub-tiles per CTA (1 or 2)
+    int pair = 1;      // 2: cta_group::2 CTA pair per 256-row tile
+    int box_rows = 16; // token rows per TMA box of the activation tensor map (bn / pair)
+    int l2pf = 0;      // weight k-blocks prefetched into L2 ahead of the smem ring
+    int persist = 0;   // 1: persistent kernel (double-buffered TMEM accumulators)
 };
 
 int num_sms();

@@ -11,6 +11,8 @@ SHAPES = [
     (17, 256, 512), (68, 256, 256), (4, 256, 1376), (64, 688, 256), (16, 256, 4096),
     (65, 3584, 4608), (200, 512, 640), (256, 1024, 384), (300, 512, 256), (528, 3584, 512),
     (1, 3584, 3584), (1088, 256, 256),
+    # CTA-pair (cta_group::2) path: M >= 192, ragged N / M tiles
+    (192, 256, 256), (193, 512, 384), (2048, 3584, 1000), (700, 1024, 4608), (4096, 256, 512),
 ]
 
 
@@ -31,8 +33,9 @@ def test_gemm_f32(m, k, n, max_splits):
     assert err < 2e-3 * max(1.0, ref.abs().max().item()), (err, rc)
 
 
-def test_gemm_swiglu():
-    m, k, f = 33, 512, 320
+@pytest.mark.parametrize("m", [33, 517])
+def test_gemm_swiglu(m):
+    k, f = 512, 320
     torch.manual_seed(0)
     x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
     w = (torch.randn(2 * f, k, device="cuda") / k ** 0.5).to(torch.bfloat16)
