@@ -251,6 +251,12 @@ TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int 
  * (CUDA events on a private stream). Returns the split-K factor. */
 TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
                               void* y_bf16, float* ws, long long ws_elems, int iters, float* avg_ms);
+/* Row top-k by (logit desc, id asc) + row max M and S = sum exp(l - M) over
+ * fp32 logits [R][V] (the drafter child selection); `part` is scratch of
+ * [ceil(V/128)][R][2+2k] floats. Average ms over `iters` launches. Returns the
+ * number of chunks per row. */
+TLT_API int tlt_dev_row_topk(const float* logits, int R, int V, int k, float* part, int* out_tok, float* out_logit,
+                             float* out_M, float* out_S, int iters, float* avg_ms);
 
 #ifdef __cplusplus
 }

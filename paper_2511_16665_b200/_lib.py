@@ -48,6 +48,9 @@ def _declare(L: C.CDLL) -> None:
     L.tlt_dev_gemm.restype = C.c_int
     L.tlt_dev_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int]
+    L.tlt_dev_row_topk.restype = C.c_int
+    L.tlt_dev_row_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
 
 
 def last_error(engine=None) -> str:

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "engine_kernels.h"
 #include "kernels.cuh"
 #include "pdl.cuh"
@@ -280,6 +282,254 @@ __global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-row variant for tree verify / drafter levels (many query vectors per
+// request and KV head): CTA = (128 query vectors, KV head, request, 256-key
+// split), 8 warps, warp w owns query m16-tile w. K/V tiles of 64 keys are
+// staged ONCE per CTA in shared memory (cp.async, double-buffered) and shared
+// by all 8 warps, so each K/V byte is read once per 128 query vectors instead
+// of once per 16 (7 query heads x T+1 rows of a request share one KV head).
+// Same split alignment and partial layout as k_attention_mma, so
+// k_attn_combine merges either.
+constexpr int kTQV = 128;   // query vectors per CTA
+constexpr int kTKeys = 64;  // keys per stage
+constexpr int kTRows = kTQV / 2 + 2;  // >= distinct rows covered by 128 qv (G >= 2)
+
+template <int kHD>
+__global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
+    pdl_wait();
+    constexpr int kStride = kHD + 8;
+    constexpr int KS = kHD / 16;
+    constexpr int NT = kHD / 8;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    bf16* Qs = reinterpret_cast<bf16*>(sm_raw);            // [128][kStride]
+    bf16* Kb = Qs + kTQV * kStride;                        // [2][64][kStride]
+    bf16* Vb = Kb + 2 * kTKeys * kStride;                  // [2][64][kStride]
+    uint32_t* Ms = reinterpret_cast<uint32_t*>(Vb + 2 * kTKeys * kStride);  // [kTRows][kMaskWords]
+    __shared__ int s_lrow[kTQV];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int G = p.H / p.KV;
+    const int kvh = blockIdx.y;
+    const int grp = blockIdx.z / p.max_splits;
+    const int split = blockIdx.z % p.max_splits;
+    const int qv0 = blockIdx.x * kTQV;
+    const int nqv = p.rows_per_req * G;
+    const int slot = p.g.slot[grp];
+    const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
+    const int total = slot >= 0 ? lc + ntail : 0;
+    const int k0 = split * kSplit;
+    const int k1 = min(total, k0 + kSplit);
+    const int row_base = qv0 / G;  // first request-local row of this CTA
+
+    // ---- stage Q and the rows' tail masks
+    if (threadIdx.x < kTQV) {
+        const int gqv = qv0 + threadIdx.x;
+        int lr = -1;
+        if (gqv < nqv) {
+            const int row = grp * p.rows_per_req + gqv / G;
+            if (p.rows.slot[row] >= 0) lr = gqv / G - row_base;
+        }
+        s_lrow[threadIdx.x] = lr;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kTQV * (kHD / 8); c += blockDim.x) {
+        const int l = c / (kHD / 8), w = c % (kHD / 8);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (s_lrow[l] >= 0) {
+            const int gqv = qv0 + l;
+            const int row = grp * p.rows_per_req + gqv / G;
+            const int head = kvh * G + gqv % G;
+            v = reinterpret_cast<const uint4*>(p.q + (long long)row * p.H * kHD + head * kHD)[w];
+        }
+        *reinterpret_cast<uint4*>(Qs + l * kStride + w * 8) = v;
+    }
+    const int nrows = min(kTRows, p.rows_per_req - row_base);
+    const int mw = (ntail + 31) >> 5;
+    for (int c = threadIdx.x; c < nrows * kMaskWords; c += blockDim.x) {
+        const int l = c / kMaskWords, w = c % kMaskWords;
+        const int row = grp * p.rows_per_req + row_base + l;
+        Ms[c] = w < mw ? p.rows.mask[(long long)row * kMaskWords + w] : 0u;
+    }
+
+    // ---- K/V tile loader (all 256 threads): 64 keys x kHD of K and of V
+    const long long slot_base = ((long long)(slot < 0 ? 0 : slot) * p.KV + kvh) * p.cap;
+    auto load_tile = [&](int kb, int buf) {
+        bf16* Kd = Kb + buf * kTKeys * kStride;
+        bf16* Vd = Vb + buf * kTKeys * kStride;
+        const int nk = min(kTKeys, k1 - kb);
+#pragma unroll
+        for (int c = threadIdx.x; c < kTKeys * (kHD / 8); c += 256) {
+            const int j = c / (kHD / 8), w = c % (kHD / 8);
+            const bool ok = j < nk;
+            const int v = kb + j;
+            const long long ci = ok ? (v < lc ? v : tail0 + (v - lc)) : 0;
+            const long long off = (slot_base + ci) * kHD + w * 8;
+            cp_async16(Kd + j * kStride + w * 8, p.kc + off, ok);
+            cp_async16(Vd + j * kStride + w * 8, p.vc + off, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (k0 < k1) load_tile(k0, 0);
+    __syncthreads();  // Q / masks staged
+
+    // this warp's 16 query vectors
+    const int wq0 = warp * 16;
+    const bool active = qv0 + wq0 < nqv;
+    uint32_t qa[KS][4];
+    int lr0 = -1, lr1 = -1;
+    if (active) {
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            qa[kk][0] = *reinterpret_cast<const uint32_t*>(Qs + (wq0 + g) * kStride + kk * 16 + 2 * t);
+            qa[kk][1] = *reinterpret_cast<const uint32_t*>(Qs + (wq0 + g + 8) * kStride + kk * 16 + 2 * t);
+            qa[kk][2] = *reinterpret_cast<const uint32_t*>(Qs + (wq0 + g) * kStride + kk * 16 + 8 + 2 * t);
+            qa[kk][3] = *reinterpret_cast<const uint32_t*>(Qs + (wq0 + g + 8) * kStride + kk * 16 + 8 + 2 * t);
+        }
+        lr0 = s_lrow[wq0 + g];
+        lr1 = s_lrow[wq0 + g + 8];
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
+
+    int buf = 0;
+    for (int kb = k0; kb < k1; kb += kTKeys, buf ^= 1) {
+        if (kb + kTKeys < k1) {
+            load_tile(kb + kTKeys, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (active) {
+            const bf16* Ks = Kb + buf * kTKeys * kStride;
+            const bf16* Vs = Vb + buf * kTKeys * kStride;
+            const int nk = min(kTKeys, k1 - kb);
+            // ---- S = Q K^T (16 x 64)
+            float s[8][4];
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk) {
+                    const bf16* kr = Ks + (nt * 8 + g) * kStride + kk * 16 + 2 * t;
+                    mma16816(s[nt], qa[kk], *reinterpret_cast<const uint32_t*>(kr),
+                             *reinterpret_cast<const uint32_t*>(kr + 8));
+                }
+            }
+            // ---- scale + visibility (committed prefix, or the row's tree-mask bit)
+            float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int col = nt * 8 + 2 * t + (e & 1);
+                    const int lr = e < 2 ? lr0 : lr1;
+                    const int v = kb + col;
+                    bool vis = col < nk && lr >= 0;
+                    if (vis && v >= lc) {
+                        const int tt = v - lc;
+                        vis = (Ms[lr * kMaskWords + (tt >> 5)] >> (tt & 31)) & 1u;
+                    }
+                    const float x = vis ? s[nt][e] * p.scale_log2 : -CUDART_INF_F;
+                    s[nt][e] = x;
+                    if (e < 2) mx0 = fmaxf(mx0, x);
+                    else mx1 = fmaxf(mx1, x);
+                }
+            }
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+            const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
+            const float c0 = nm0 == -CUDART_INF_F ? 1.f : exp2f(m0 - nm0);
+            const float c1 = nm1 == -CUDART_INF_F ? 1.f : exp2f(m1 - nm1);
+            m0 = nm0;
+            m1 = nm1;
+            l0 *= c0;
+            l1 *= c1;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                o[n][0] *= c0;
+                o[n][1] *= c0;
+                o[n][2] *= c1;
+                o[n][3] *= c1;
+            }
+            uint32_t pa[4][4];
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const float p0 = m0 == -CUDART_INF_F ? 0.f : exp2f(s[nt][0] - m0);
+                const float p1 = m0 == -CUDART_INF_F ? 0.f : exp2f(s[nt][1] - m0);
+                const float p2 = m1 == -CUDART_INF_F ? 0.f : exp2f(s[nt][2] - m1);
+                const float p3 = m1 == -CUDART_INF_F ? 0.f : exp2f(s[nt][3] - m1);
+                l0 += p0 + p1;
+                l1 += p2 + p3;
+                const int j = nt >> 1;
+                if ((nt & 1) == 0) {
+                    pa[j][0] = pack_bf16(p0, p1);
+                    pa[j][1] = pack_bf16(p2, p3);
+                } else {
+                    pa[j][2] = pack_bf16(p0, p1);
+                    pa[j][3] = pack_bf16(p2, p3);
+                }
+            }
+            // ---- O += P V (64 keys = 4 k16 steps)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+#pragma unroll
+                for (int nd = 0; nd < NT; nd += 2) {
+                    const int mi = lane >> 3, r = lane & 7;
+                    const int key = 16 * j + (mi & 1) * 8 + r;
+                    const int dim = (nd + (mi >> 1)) * 8;
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_trans(b0, b1, b2, b3, Vs + key * kStride + dim);
+                    mma16816(o[nd], pa[j], b0, b1);
+                    mma16816(o[nd + 1], pa[j], b2, b3);
+                }
+            }
+        }
+        __syncthreads();  // buffer `buf` is refilled by the next iteration's prefetch
+    }
+    if (!active) return;
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    // ---- split partial of each of this warp's query vectors
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int gqv = qv0 + wq0 + g + 8 * h;
+        if (gqv >= nqv) continue;
+        const long long pidx = ((long long)(grp * p.max_splits + split) * p.qv_cap + gqv) * p.KV + kvh;
+        float* dst = p.ws_o + pidx * kHD;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+            *reinterpret_cast<float2*>(dst + n * 8 + 2 * t) = make_float2(o[n][2 * h], o[n][2 * h + 1]);
+        if (t == 0) {
+            p.ws_m[pidx] = h ? m1 : m0;
+            p.ws_l[pidx] = h ? l1 : l0;
+        }
+    }
+}
+
+template <int kHD>
+void launch_attention_tree_t(const AttnParams& p, cudaStream_t st) {
+    constexpr int kStride = kHD + 8;
+    const size_t smem = sizeof(bf16) * (kTQV + 4 * kTKeys) * kStride + sizeof(uint32_t) * kTRows * kMaskWords;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attention_tree<kHD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int G = p.H / p.KV;
+    const int nqv = p.rows_per_req * G;
+    dim3 grid((nqv + kTQV - 1) / kTQV, p.KV, p.n_groups * p.max_splits);
+    launch_pdl(k_attention_tree<kHD>, grid, 256, smem, st, p);
+}
+
 template <int kHD>
 size_t attention_mma_smem() {
     constexpr int kStride = kHD + 8;
@@ -305,6 +555,18 @@ void launch_attention_mma_t(const AttnParams& p, cudaStream_t st) {
 int attention_mma_split() { return kSplit; }
 
 void launch_attention_mma(const AttnParams& p, cudaStream_t st) {
+    // many query vectors per (request, KV head): share each K/V tile across them
+    static const int tree_min = [] {
+        const char* v = std::getenv("TLT_ATTN_TREE_MIN_QV");
+        return v ? std::atoi(v) : 17;
+    }();
+    if (p.rows_per_req * (p.H / p.KV) >= tree_min && p.H / p.KV >= 2) {
+        if (p.hd == 128)
+            launch_attention_tree_t<128>(p, st);
+        else
+            launch_attention_tree_t<64>(p, st);
+        return;
+    }
     if (p.hd == 128)
         launch_attention_mma_t<128>(p, st);
     else

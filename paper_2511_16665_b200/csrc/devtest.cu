@@ -1,6 +1,8 @@
 // Kernel-level entry points used by the GPU unit tests (plain pointers, C-ABI).
 #include <cuda_runtime.h>
 #include "tlt_internal.h"
+#include "engine_kernels.h"
+#include <algorithm>
 #include "../../include/tlt_b200.h"
 
 using namespace tlt;
@@ -65,6 +67,37 @@ extern "C" TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void
         cudaEventDestroy(e1);
         cudaStreamDestroy(st);
         return g.splits;
+    } catch (const std::exception& e) {
+        tlt_set_last_error(e.what());
+        return -1;
+    }
+}
+
+// Row top-k over materialised fp32 logits (chunked scan + merge), timed with
+// CUDA events over `iters` launches; outputs of the last launch.
+extern "C" TLT_API int tlt_dev_row_topk(const float* logits, int R, int V, int k, float* part, int* out_tok,
+                                        float* out_logit, float* out_M, float* out_S, int iters, float* avg_ms) {
+    try {
+        cudaStream_t st;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        cudaEvent_t e0, e1;
+        CUDA_CHECK(cudaEventCreate(&e0));
+        CUDA_CHECK(cudaEventCreate(&e1));
+        int nch = 0;
+        CUDA_CHECK(cudaEventRecord(e0, st));
+        for (int i = 0; i < std::max(1, iters); ++i) {
+            nch = launch_row_topk_chunked(logits, R, V, nullptr, k, part, st);
+            launch_topk_merge(part, nch, R, k, nullptr, out_tok, out_logit, out_M, out_S, st);
+        }
+        CUDA_CHECK(cudaEventRecord(e1, st));
+        CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        if (avg_ms) *avg_ms = ms / std::max(1, iters);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+        return nch;
     } catch (const std::exception& e) {
         tlt_set_last_error(e.what());
         return -1;

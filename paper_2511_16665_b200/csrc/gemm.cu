@@ -671,7 +671,8 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     // pairs only when they still put >= 1 CTA on every SM (else the 1-CTA
     // plan with in-cluster split-K fills the machine better)
     const int pair_ctas = 2 * ((n_out + 2 * kBlockM - 1) / (2 * kBlockM)) * ((m_tok + pair_bn_max - 1) / pair_bn_max);
-    if (pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas >= num_sms()) {
+    static const int pair_min_ctas = env_knob("TLT_GEMM_PAIR_MIN_CTAS", 148);
+    if (pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas >= pair_min_ctas) {
         g.pair = 2;
         g.wm = 1;
         const int n_tt = (m_tok + pair_bn_max - 1) / pair_bn_max;

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Engine kernels: weight init, gathers, RMSNorm, tree-masked attention,
 // row top-k / argmax, drafter tree select (K6), greedy accept (K7), KV
 // compaction + commit (K8), row-metadata builders. The GEMMs are in gemm.cu.
@@ -534,35 +535,119 @@ __device__ __forceinline__ void block_topk_finish(TopK<K>& t, float& m, float& s
 // (chunk c, row r) reduces an 8192-entry chunk to the same partial record the
 // EPI_TOPK epilogue writes (chunk max m, sum exp(l - m), sorted top-k), so
 // k_topk_merge finishes both. Chunk order is fixed -> deterministic.
+// Stage 1 of the multi-CTA row top-k (k > 1) over materialised logits: CTA
+// (chunk c, row r) reduces an 8192-entry chunk (held in registers, 32 per
+// thread, all loads in flight at once) to the partial record the EPI_TOPK
+// epilogue writes (chunk max m, sum exp(l - m), sorted top-k), so
+// k_topk_merge finishes both. Selection: the K-th largest of the 256
+// per-thread maxima is a lower bound of the chunk's K-th value (K distinct
+// entries reach it), entries at or above it are appended to a small smem
+// candidate list (typically ~K of 8192) and only those are ranked. Ties are
+// ranked by id, so the result is deterministic whatever the append order.
 constexpr int kTopkChunk = 8192;
+constexpr int kTopkPer = kTopkChunk / 256;
+constexpr int kTopkCap = 512;
 template <int K>
-__global__ void __launch_bounds__(256) k_row_topk_chunk(const float* __restrict__ logits, int V, const int* live,
+__global__ void __launch_bounds__(256, 3) k_row_topk_chunk(const float* __restrict__ logits, int V, const int* live,
                                                         int k, float* __restrict__ part, int R) {
     pdl_wait();
     __shared__ float sv[8 * K];
     __shared__ int si[8 * K];
     __shared__ float sm[8], ss[8];
+    __shared__ float s_thr, s_max;
+    __shared__ float cv[kTopkCap];
+    __shared__ int ci[kTopkCap];
+    __shared__ int s_cnt;
     const int c = blockIdx.x, r = blockIdx.y;
     if (live && live[r] < 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float* lr = logits + (long long)r * V;
     const int i0 = c * kTopkChunk, i1 = min(V, i0 + kTopkChunk);
-    TopK<K> t;
-    t.init();
-    float m = -CUDART_INF_F, s = 0.f;
-    for (int base = i0 + threadIdx.x; base < i1; base += 256 * 8) {
-        float x[8];
+    float x[kTopkPer];
+    float mx = -CUDART_INF_F;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = base + u * 256;
-            x[u] = i < i1 ? __ldcs(lr + i) : -CUDART_INF_F;  // streamed once
+    for (int u = 0; u < kTopkPer; ++u) {
+        const int i = i0 + u * 256 + threadIdx.x;
+        x[u] = i < i1 ? __ldcs(lr + i) : -CUDART_INF_F;
+        mx = fmaxf(mx, x[u]);
+    }
+    if (threadIdx.x == 0) s_cnt = 0;
+    {  // per warp: bitonic sort (descending) of the 32 lane maxima
+        float v = mx;
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const float o = __shfl_xor_sync(0xffffffffu, v, stride);
+                const bool desc = (lane & size) == 0 || size == 32;
+                const bool lower = (lane & stride) == 0;
+                v = (lower == desc) ? fmaxf(v, o) : fminf(v, o);
+            }
         }
+        // the warp's K-th largest lane maximum bounds the chunk's K-th value
+        const float kth = __shfl_sync(0xffffffffu, v, K - 1);
+        const float wmax = __shfl_sync(0xffffffffu, v, 0);
+        if (lane == 0) {
+            sm[warp] = kth;
+            ss[warp] = wmax;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float t0 = sm[0], m0 = ss[0];
+            for (int w = 1; w < 8; ++w) {
+                t0 = fmaxf(t0, sm[w]);
+                m0 = fmaxf(m0, ss[w]);
+            }
+            s_thr = t0;
+            s_max = m0;
+        }
+        __syncthreads();
+    }
+    const float thr = s_thr, M = s_max;
+    float s = 0.f;
+    if (M != -CUDART_INF_F) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            ms_add(m, s, x[u]);
-            t.push(x[u], base + u * 256);
+        for (int u = 0; u < kTopkPer; ++u) s += __expf(x[u] - M);  // exp(-inf) = 0
+    }
+#pragma unroll
+    for (int u = 0; u < kTopkPer; ++u) {
+        if (x[u] >= thr) {
+            const int p = atomicAdd(&s_cnt, 1);
+            if (p < kTopkCap) {
+                cv[p] = x[u];
+                ci[p] = i0 + u * 256 + threadIdx.x;
+            }
         }
     }
-    block_topk_finish<K>(t, m, s, sv, si, sm, ss);
+    // s: fixed-order block sum
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __syncthreads();  // candidates complete; sm/ss reused
+    if (lane == 0) ss[warp] = s;
+    const int cnt = s_cnt;
+    TopK<K> t;
+    t.init();
+    float m = M;
+    if (cnt <= kTopkCap) {
+        __syncthreads();
+        if (warp != 0) return;
+        for (int e = lane; e < cnt; e += 32) t.push(cv[e], ci[e]);
+        t.warp_merge();
+        s = ss[0];
+        for (int w = 1; w < 8; ++w) s += ss[w];
+    } else {  // pathological ties at the threshold: rank every thread's entries
+#pragma unroll
+        for (int u = 0; u < kTopkPer; ++u)
+            if (x[u] >= thr) t.push(x[u], i0 + u * 256 + threadIdx.x);
+        __syncthreads();
+        float tot = ss[0];
+        for (int w = 1; w < 8; ++w) tot += ss[w];
+        __syncthreads();  // ss is scratch of block_topk_finish below
+        float mm = M, s0 = 0.f;
+        block_topk_finish<K>(t, mm, s0, sv, si, sm, ss);  // (m, s) of this call unused
+        s = tot;
+        if (warp != 0) return;
+    }
     const int W = 2 + 2 * k;
     float* out = part + ((long long)c * R + r) * W;
     if (threadIdx.x == 0) {

@@ -1,0 +1,51 @@
+"""Row top-k kernel (drafter child selection) vs a torch fp32 reference:
+ids ordered by (logit desc, id asc) — the reference child order
+(spec_decode.hpp:121-125) — exact; M exact; S within fp32 tolerance."""
+import ctypes as C
+
+import pytest
+import torch
+
+from paper_2511_16665_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def run(logits, k):
+    R, V = logits.shape
+    part = torch.empty(((V + 127) // 128) * R * (2 + 2 * k), device="cuda")
+    tok = torch.empty(R, k, dtype=torch.int32, device="cuda")
+    val = torch.empty(R, k, device="cuda")
+    M = torch.empty(R, device="cuda")
+    S = torch.empty(R, device="cuda")
+    ms = C.c_float()
+    rc = _lib.lib().tlt_dev_row_topk(logits.data_ptr(), R, V, k, part.data_ptr(), tok.data_ptr(), val.data_ptr(),
+                                     M.data_ptr(), S.data_ptr(), 1, C.byref(ms))
+    assert rc >= 1, _lib.last_error()
+    torch.cuda.synchronize()
+    return tok, val, M, S
+
+
+def ref_topk(logits, k):
+    # stable sort of -logit keeps ascending ids among equal logits
+    return torch.argsort(-logits.double(), dim=1, stable=True)[:, :k]
+
+
+@pytest.mark.parametrize("R,V,k", [(3, 4096, 8), (17, 152064, 8), (64, 152064, 4), (5, 1000, 2), (300, 4096, 8)])
+@pytest.mark.parametrize("pattern", ["randn", "ramp", "ties"])
+def test_row_topk(R, V, k, pattern):
+    g = torch.Generator(device="cuda").manual_seed(R * 31 + V + k)
+    if pattern == "randn":
+        x = torch.randn(R, V, device="cuda", generator=g) * 3
+    elif pattern == "ramp":  # monotone in id: worst case for insertion-based scans
+        x = torch.arange(V, device="cuda", dtype=torch.float32).expand(R, V) * 1e-3 + torch.arange(R, device="cuda")[:, None]
+        x = x.contiguous()
+    else:  # heavy exact ties: lowest id must win
+        x = torch.randint(0, 5, (R, V), device="cuda", generator=g).float()
+    tok, val, M, S = run(x, k)
+    want = ref_topk(x, k)
+    assert torch.equal(tok.long(), want), (tok[:2], want[:2])
+    assert torch.equal(val, torch.gather(x, 1, want))
+    assert torch.equal(M, x.max(dim=1).values)
+    Sref = torch.exp(x.double() - x.max(dim=1, keepdim=True).values.double()).sum(dim=1)
+    assert torch.allclose(S.double(), Sref, rtol=1e-4)
