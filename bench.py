@@ -208,32 +208,47 @@ def run_reference(a):
 
 
 # ----------------------------------------------------------------- GPU arm
-def gemm_roofline(model_name, m_tok, peak_gbs):
-    """Dominant kernel: gate_up GEMM (largest weight) at the long-tail verify
-    M, timed back to back with CUDA events on its own stream."""
-    import ctypes as C
+PROBES = [  # (name, probe kind, M, bound)  -- SURVEY.md 8(d) per-kernel rooflines
+    ("gate_up GEMM+SwiGLU, long-tail verify (b=1, T=16)", 0, 17, "hbm"),
+    ("gate_up GEMM+SwiGLU, plain decode b=1", 0, 1, "hbm"),
+    ("down GEMM+residual, long-tail verify (b=1, T=16)", 2, 17, "hbm"),
+    ("LM head + fused top-1, long-tail verify (b=1, T=16)", 4, 17, "hbm"),
+    ("gate_up GEMM+SwiGLU, verify b=31 T=16", 0, 527, "tensor"),
+    ("down GEMM+residual, verify b=31 T=16", 2, 527, "tensor"),
+    ("LM head fp32 logits, drafter level b=31 (496 rows)", 3, 496, "tensor"),
+    ("gate_up GEMM+SwiGLU, verify b=16 T=64", 0, 1040, "tensor"),
+]
 
-    import torch
 
-    from paper_2511_16665_b200 import _lib
-    from paper_2511_16665_b200.engine import MODELS
-    mm = MODELS[model_name]
-    K, N = mm["hidden"], 2 * mm["ffn"]
-    L = _lib.lib()
-    x = torch.randn(m_tok, K, device="cuda").to(torch.bfloat16)
-    w = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
-    y = torch.empty(m_tok, N // 2, device="cuda", dtype=torch.bfloat16)
-    ws = torch.empty(64 << 20, device="cuda", dtype=torch.float32)
-    ms = C.c_float()
-    rc = L.tlt_dev_time_gemm(x.data_ptr(), m_tok, K, w.data_ptr(), N, 3, None, y.data_ptr(), ws.data_ptr(),
-                             ws.numel(), 50, C.byref(ms))
-    if rc < 0:
-        return None
-    byts = N * K * 2 + m_tok * K * 2 + m_tok * (N // 2) * 2
-    ach = byts / (ms.value * 1e-3) / 1e9
-    return {"kernel": f"gate_up tcgen05 GEMM+SwiGLU [M={m_tok}]x[{K}]x[{N}]", "bound": "hbm",
-            "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 3),
-            "traffic": None, "algorithmic_bytes": byts, "avg_launch_ms": round(ms.value, 4)}
+def traffic_table():
+    """dram bytes per launch from the committed ncu --set full captures."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind):
+    """Each probe: the engine's own GEMM site, successive layers' weights,
+    CUDA events on the engine stream (tlt_probe_kernel)."""
+    traffic = traffic_table()
+    out = []
+    for name, kind, m, bound in PROBES:
+        ms, byts, flops = eng.probe_kernel(kind, m, 56)
+        if bound == "hbm":
+            ach = byts / (ms * 1e-3) / 1e9
+            rec = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
+                   "frac": round(ach / peak_gbs, 3)}
+        else:
+            ach = flops / (ms * 1e-3) / 1e12
+            rec = {"kernel": name, "bound": "tensor", "achieved": round(ach, 1), "peak": peak_tf, "unit": "TFLOP/s",
+                   "frac": round(ach / peak_tf, 3)}
+        t = traffic.get(f"{kind}:{m}")
+        rec.update({"traffic": t, "algorithmic_bytes": int(byts), "M": m, "avg_launch_ms": round(ms, 4),
+                    "peak_kind": peak_kind})
+        out.append(rec)
+    return out
 
 
 def run_ours(a):
@@ -290,9 +305,8 @@ def run_ours(a):
     sd_same = res[0] if res else None
     out = None
     if rank == 0:
-        roof = gemm_roofline(a.model, a.roof_m, peak_gbs)
-        if roof is not None:
-            roof["peak_kind"] = peak_kind
+        kernels = kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind)
+        roof = kernels[0]
         cpu = None
         if a.cpu_gen > 0:
             threads = os.cpu_count() or 1
@@ -320,6 +334,7 @@ def run_ours(a):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": roof,
+            "kernels": kernels,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
@@ -348,7 +363,6 @@ def main():
     ap.add_argument("--len-sigma", type=float, default=1.0)
     ap.add_argument("--max-len", type=int, default=2048)
     ap.add_argument("--elastic", type=int, default=32)
-    ap.add_argument("--roof-m", type=int, default=17)
     ap.add_argument("--ar-baseline", type=int, default=1)
     ap.add_argument("--cpu-gen", type=int, default=8)
     ap.add_argument("--cpu-prompt", type=int, default=8)

@@ -242,6 +242,14 @@ TLT_API int tlt_debug_target_rows(tlt_engine* e, int i, double* rows, int max_ro
 /* Target logits of the last tlt_ar_step: [b][V]. */
 TLT_API int tlt_debug_ar_logits(tlt_engine* e, float* logits, int b);
 
+/* Live timing of one of the engine's own GEMM sites on its stream with its
+ * own weights (successive layers, so every launch streams fresh weights):
+ * kind 0 gate_up+SwiGLU, 1 qkv (+RoPE, KV write), 2 down (+residual),
+ * 3 LM head fp32 logits, 4 LM head + fused top-1. Reports the average launch
+ * duration and the algorithmic bytes / flops of one launch. */
+TLT_API int tlt_probe_kernel(tlt_engine* e, int kind, int m_tok, int iters, float* avg_ms, double* bytes,
+                             double* flops);
+
 /* ---- kernel-level entry points for unit tests ---------------------------- */
 /* Y = X W^T through the tcgen05 GEMM. kind: 0 f32 store, 1 bf16 store,
  * 3 SwiGLU (W rows interleaved gate/up). Returns the split-K factor used. */

@@ -57,6 +57,59 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 }  // namespace
 
+
+// Fused split combine: the last CTA (of the max_splits CTAs that share this
+// (request, KV head, query-vector tile)) merges every split's (m, l, O) in
+// fixed split order — the same arithmetic as k_attn_combine — and writes the
+// bf16 output, so no separate combine launch is needed. Called by all
+// threads of the CTA at the very end of the attention kernels.
+template <int kHD>
+__device__ __forceinline__ void attn_fused_combine(const AttnParams& p, int grp, int kvh, int qtile, int qv_lo,
+                                                   int qv_hi) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    const int n_qt = gridDim.x;
+    const long long cidx = ((long long)grp * p.KV + kvh) * n_qt + qtile;
+    if (threadIdx.x == 0) s_last = atomicAdd(p.counters + cidx, 1) == p.max_splits - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int G = p.H / p.KV;
+    const int nqv = p.rows_per_req * G;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int total_keys = p.g.lc[grp] + p.g.ntail[grp];
+    const int nsplit = min(p.max_splits, (total_keys + p.chunk - 1) / p.chunk);
+    constexpr int DPL = kHD / 32;
+    for (int gqv = qv_lo + warp; gqv < min(qv_hi, nqv); gqv += nw) {
+        const int row = grp * p.rows_per_req + gqv / G;
+        const int head = kvh * G + gqv % G;
+        if (p.rows.slot[row] < 0) continue;
+        float M = -CUDART_INF_F;
+        for (int sp = 0; sp < nsplit; ++sp) {
+            const long long pidx = ((long long)(grp * p.max_splits + sp) * p.qv_cap + gqv) * p.KV + kvh;
+            M = fmaxf(M, __ldcg(p.ws_m + pidx));
+        }
+        float L = 0.f, o[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[e] = 0.f;
+        for (int sp = 0; sp < nsplit; ++sp) {  // fixed order
+            const long long pidx = ((long long)(grp * p.max_splits + sp) * p.qv_cap + gqv) * p.KV + kvh;
+            const float ms = __ldcg(p.ws_m + pidx);
+            if (ms == -CUDART_INF_F) continue;
+            const float w = exp2f(ms - M);
+            L += __ldcg(p.ws_l + pidx) * w;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) o[e] += __ldcg(p.ws_o + pidx * kHD + lane * DPL + e) * w;
+        }
+        const float inv = L > 0.f ? 1.0f / L : 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+            p.out[(long long)row * p.H * kHD + head * kHD + lane * DPL + e] = __float2bfloat16_rn(o[e] * inv);
+    }
+    if (threadIdx.x == 0) p.counters[cidx] = 0;  // ready for the next launch / graph replay
+}
+
 template <int kHD>
 __global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
     pdl_wait();
@@ -280,6 +333,7 @@ __global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
             p.ws_l[pidx] = L;
         }
     }
+    if (p.counters) attn_fused_combine<kHD>(p, grp, kvh, blockIdx.x, qv0, qv0 + kQV);
 }
 
 // ---------------------------------------------------------------------------
@@ -493,7 +547,7 @@ __global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
         }
         __syncthreads();  // buffer `buf` is refilled by the next iteration's prefetch
     }
-    if (!active) return;
+    if (active) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
@@ -513,6 +567,8 @@ __global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
             p.ws_l[pidx] = h ? l1 : l0;
         }
     }
+    }  // active
+    if (p.counters) attn_fused_combine<kHD>(p, grp, kvh, blockIdx.x, qv0, qv0 + kTQV);
 }
 
 template <int kHD>
@@ -560,7 +616,12 @@ void launch_attention_mma(const AttnParams& p, cudaStream_t st) {
         const char* v = std::getenv("TLT_ATTN_TREE_MIN_QV");
         return v ? std::atoi(v) : 17;
     }();
-    if (p.rows_per_req * (p.H / p.KV) >= tree_min && p.H / p.KV >= 2) {
+    // ... as long as that still yields enough CTAs to cover the SMs (at
+    // batch 1 the 16-vector kernel's 8x more CTAs win)
+    const int G = p.H / p.KV;
+    const long long tree_ctas =
+        (long long)((p.rows_per_req * G + kTQV - 1) / kTQV) * p.KV * p.n_groups * p.max_splits;
+    if (p.rows_per_req * G >= tree_min && G >= 2 && tree_ctas >= 96) {
         if (p.hd == 128)
             launch_attention_tree_t<128>(p, st);
         else

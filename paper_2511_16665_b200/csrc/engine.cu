@@ -121,6 +121,7 @@ Engine::~Engine() {
     f(dkc_), f(dvc_), f(d_kc_arr_), f(d_vc_arr_), f(tok_hist_), f(feat_hist_);
     f(x_), f(xg_), f(h_), f(q_), f(attn_), f(act_), f(feat_), f(x2_), f(dfeat_), f(logits_), f(ws_);
     f(aws_m_), f(aws_l_), f(aws_o_);
+    if (attn_counters_) cudaFree(attn_counters_);
     free_rows(drows_), free_rows(vrows_), free_rows(prows_);
     for (auto& g : dg_) free_groups(g);
     free_groups(vg_), free_groups(pg_);
@@ -313,6 +314,21 @@ void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const C
     e.kind = EPI_RESID_ADD;
     e.out_f32 = x_;
     e.ld_f32 = d;
+    static const int fuse_max_m = [] {
+        // off by default: the serial tail of the electing CTA measured slower
+        // than the 8-CTA cluster norm kernel under PDL (profiles/r1_*)
+        const char* v = std::getenv("TLT_FUSED_NORM_MAX_M");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (norm_w && M <= fuse_max_m && g.pair == 1 && !g.persist) {
+        // long-tail M: the GEMM's last CTA normalises the updated rows
+        e.norm_w = norm_w;
+        e.norm_out = h_;
+        e.norm_eps = cfg.rms_eps;
+        launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
+        count_launch();
+        return;
+    }
     launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
     count_launch();
     if (norm_w) {
@@ -350,8 +366,20 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
     p.ws_m = aws_m_;
     p.ws_l = aws_l_;
     p.ws_o = aws_o_;
+    static const int fused_combine = [] {
+        const char* v = std::getenv("TLT_ATTN_FUSED_COMBINE");
+        return v ? std::atoi(v) : 1;
+    }();
+    if (fused_combine && p.impl == 1) {
+        if (!attn_counters_) {
+            attn_counters_ = dmalloc<int>(1 << 16);
+            CUDA_CHECK(cudaMemset(attn_counters_, 0, sizeof(int) << 16));
+        }
+        const long long n_qt = (p.rows_per_req * (cfg.heads / cfg.kv_heads) + 15) / 16;
+        if ((long long)ngroups * cfg.kv_heads * n_qt <= (1 << 16)) p.counters = attn_counters_;
+    }
     launch_attention(p, st_);
-    count_launch(2);
+    count_launch(p.counters ? 1 : 2);
 }
 
 // One decoder layer over R rows (residual x_ in place).
@@ -629,6 +657,97 @@ void Engine::catchup_drafter(int b, const int32_t* slots) {
 int Engine::bucket_hi_for(int b, int T) const {
     (void)T;
     return b;
+}
+
+
+// ------------------------------------------------------------ kernel probe
+// Live per-kernel timing on the engine stream with the engine's own weights:
+// `iters` launches of one GEMM site over successive layers (every launch
+// streams a different weight matrix from HBM, as in a real forward), CUDA
+// events around the whole sequence. Activations are whatever the buffers
+// hold (values do not change the timing). kind: 0 gate_up (+SwiGLU), 1 qkv
+// (+bias/RoPE/KV write into slot 0), 2 down (+residual), 3 LM head fp32
+// logits (drafter k > 1 path), 4 LM head + fused top-1 (verify / decode).
+float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* flops) {
+    if (M < 1 || M > R_) throw ConfigErr("M", "out of range for the activation buffers");
+    const int d = cfg.hidden, L = cfg.layers;
+    const int nq = cfg.heads * cfg.head_dim, nkv = cfg.kv_heads * cfg.head_dim;
+    long long N = 0, K = 0;
+    for (int i = 0; i < 2; ++i) {  // warm-up: plans, tensor maps, first-touch
+        CUDA_CHECK(cudaEventRecord(ev0_, st_));
+        for (int it = 0; it < iters; ++it) {
+            const LayerW& w = layers_[it % L];
+            EpiParams ep{};
+            switch (kind) {
+                case 0:
+                    ep.kind = EPI_SWIGLU;
+                    ep.out_bf16 = act_;
+                    ep.ld_bf16 = cfg.ffn;
+                    gemm(h_, M, d, d, w.tm_gu, 2 * cfg.ffn, ep);
+                    N = 2LL * cfg.ffn;
+                    K = d;
+                    break;
+                case 1:
+                    ep.kind = EPI_QKV;
+                    ep.out_bf16 = q_;
+                    ep.ld_bf16 = nq;
+                    ep.bias = w.qkv_b;
+                    ep.rope_cos = rope_cos_;
+                    ep.rope_sin = rope_sin_;
+                    ep.tok_pos = prows_.pos;
+                    ep.tok_slot = prows_.slot;
+                    ep.tok_cidx = prows_.cidx;
+                    ep.kcache = kc_[it % L];
+                    ep.vcache = vc_[it % L];
+                    ep.n_q = nq;
+                    ep.n_kvr = nkv;
+                    ep.head_dim = cfg.head_dim;
+                    ep.n_kv = cfg.kv_heads;
+                    ep.max_ctx = cap_;
+                    gemm(h_, M, d, d, w.tm_qkv, nq + 2 * nkv, ep);
+                    N = nq + 2LL * nkv;
+                    K = d;
+                    break;
+                case 2: {
+                    GemmPlan g = plan_gemm(M, d, cfg.ffn);
+                    const CUtensorMap& tx = tmap_act(act_, M, cfg.ffn, cfg.ffn, g.box_rows);
+                    ep.kind = EPI_RESID_ADD;
+                    ep.n_out = d;
+                    ep.m_tok = M;
+                    ep.out_f32 = x_;
+                    ep.ld_f32 = d;
+                    launch_gemm(g, w.tm_down, tx, ep, ws_, ws_elems_, st_);
+                    N = d;
+                    K = cfg.ffn;
+                } break;
+                case 3:
+                    ep.kind = EPI_F32;
+                    ep.out_f32 = logits_;
+                    ep.ld_f32 = cfg.vocab;
+                    gemm(h_, M, d, d, tm_lm_, cfg.vocab, ep);
+                    N = cfg.vocab;
+                    K = d;
+                    break;
+                default:
+                    ep.kind = EPI_TOPK;
+                    ep.out_f32 = topk_part_;
+                    ep.topk_k = 1;
+                    gemm(h_, M, d, d, tm_lm_, cfg.vocab, ep);
+                    N = cfg.vocab;
+                    K = d;
+                    break;
+            }
+        }
+        CUDA_CHECK(cudaEventRecord(ev1_, st_));
+        CUDA_CHECK(cudaEventSynchronize(ev1_));
+    }
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    const double out_b = kind == 0 ? (double)M * N / 2 * 2 : kind == 1 ? (double)M * N * 2
+                         : kind == 2 ? (double)M * N * 8 : kind == 3 ? (double)M * N * 4 : (double)M * 16;
+    if (bytes) *bytes = (double)N * K * 2 + (double)M * K * 2 + out_b;
+    if (flops) *flops = 2.0 * M * N * K;
+    return ms / iters;
 }
 
 // ----------------------------------------------------------- SD device seq

@@ -69,6 +69,7 @@ public:
     size_t graph_pool_build(const std::vector<tlt_capture_entry>& entries);
     void graph_pool_clear();
     int bucket_hi_for(int b, int T) const;
+    float probe_kernel(int kind, int M, int iters, double* bytes, double* flops);
 
     // parity exports
     std::vector<std::vector<DebugExp>> dbg_exp;  // [request i] expansions of the last sd_step
@@ -150,6 +151,7 @@ private:
     size_t ws_elems_ = 0;
     float *aws_m_ = nullptr, *aws_l_ = nullptr, *aws_o_ = nullptr;
     size_t aws_elems_ = 0;
+    int* attn_counters_ = nullptr;  // fused attention split-combine election
     // row metadata
     Rows drows_, vrows_, prows_;
     Groups dg_[kMaxDepth + 2], vg_, pg_;

@@ -21,6 +21,7 @@ struct AttnParams {
     int chunk, max_splits, qv_cap;
     float *ws_m, *ws_l, *ws_o;
     int impl;  // 0: CUDA-core reference kernel, 1: tensor-core flash-decode (attn_mma.cu)
+    int* counters;  // non-null: fused split combine (last CTA per tile), zeroed buffer
 };
 void launch_attention_mma(const AttnParams& p, cudaStream_t st);
 int attention_mma_split();

@@ -378,6 +378,47 @@ __global__ void __launch_bounds__(192, 1)
         }
         cluster.sync();  // peers' smem stays alive until every remote read is done
     }
+    if (ep.norm_w) {
+        // Fused RMSNorm of the updated rows (long-tail M): the last CTA to
+        // finish its epilogue normalises out_f32[0..m_tok) into norm_out.
+        __shared__ int s_last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int total = (int)(gridDim.x * gridDim.y * gridDim.z);
+            s_last = atomicAdd(ep.norm_counter, 1) == total - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            const int d = ep.n_out;
+            const int nw = blockDim.x >> 5;
+            for (int t = warp; t < ep.m_tok; t += nw) {  // one warp per token row
+                const float* xr = ep.out_f32 + (long long)t * ep.ld_f32;
+                float ss = 0.f;
+                for (int i = lane * 4; i < d; i += 128) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(xr + i));
+                    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                const float inv = 1.0f / sqrtf(ss / (float)d + ep.norm_eps);
+                __nv_bfloat16* hr = ep.norm_out + (long long)t * d;
+                for (int i = lane * 4; i < d; i += 128) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(xr + i));
+                    const uint2 gw = *reinterpret_cast<const uint2*>(ep.norm_w + i);
+                    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gw);
+                    const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+                    uint2 o;
+                    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+                    o2[0] = __floats2bfloat162_rn(v.x * inv * ga.x, v.y * inv * ga.y);
+                    o2[1] = __floats2bfloat162_rn(v.z * inv * gb.x, v.w * inv * gb.y);
+                    *reinterpret_cast<uint2*>(hr + i) = o;
+                }
+            }
+            if (threadIdx.x == 0) *ep.norm_counter = 0;  // ready for the next launch / graph replay
+        }
+    }
     tc_fence_before();
     if (PAIR == 2)
         cluster_sync_all();
@@ -645,6 +686,19 @@ static int env_knob(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
+// per-device zeroed counter for the fused-norm "last CTA" election (each last
+// CTA resets it, so the buffer stays zero between launches / graph replays)
+int* gemm_norm_counter() {
+    static int* ptrs[64] = {nullptr};
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    if (!ptrs[dev]) {
+        CUDA_CHECK(cudaMalloc(&ptrs[dev], sizeof(int) * 32));
+        CUDA_CHECK(cudaMemset(ptrs[dev], 0, sizeof(int) * 32));
+    }
+    return ptrs[dev];
+}
+
 int gemm_dbg_flags() {
     static const int f = env_knob("TLT_GEMM_DBG", 0);
     return f;
@@ -767,6 +821,9 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     dim3 grid(g.n_ttiles * g.pair, g.n_wtiles, g.splits);
     EpiParams epd = ep;
     epd.dbg = gemm_dbg_flags();
+    if (ep.norm_w && (g.persist || g.pair != 1 || ep.kind != EPI_RESID_ADD || (ep.n_out & 3) || ep.ld_f32 != ep.n_out))
+        throw CudaError("fused RMSNorm epilogue needs a single-CTA residual-add plan");
+    if (ep.norm_w) epd.norm_counter = gemm_norm_counter();
     if (g.persist) {
         static bool pattr = false;
         if (!pattr) {

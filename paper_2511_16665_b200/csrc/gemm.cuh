@@ -53,6 +53,12 @@ struct EpiParams {
     // EPI_TOPK: out_f32 = partials [n_wtiles][m_tok][2 + 2*topk_k] (m, s, vals[k], ids[k])
     int topk_k;
     int dbg;  // diagnostics (TLT_GEMM_DBG): bit0 skip MMA, bit1 skip epilogue
+    // fused RMSNorm after EPI_RESID_ADD (long-tail M): the last CTA writes
+    // norm_out[t] = bf16(rmsnorm(out_f32[t]) * norm_w) for every token row
+    const __nv_bfloat16* norm_w;
+    __nv_bfloat16* norm_out;
+    float norm_eps;
+    int* norm_counter;
 };
 constexpr int kEpiTopkMax = 8;
 

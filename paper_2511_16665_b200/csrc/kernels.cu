@@ -393,6 +393,7 @@ void launch_attention(const AttnParams& p, cudaStream_t st) {
     const int cblocks = (int)((warps * 32 + 255) / 256);
     if (p.impl == 1) {
         launch_attention_mma(p, st);  // tensor-core path (attn_mma.cu), chunk = 256 keys
+        if (p.counters) return;       // split combine fused into the attention kernel
     } else if (p.hd == 128) {
         launch_pdl(k_attention<128>, grid, 128, 0, st, p);
     } else {

@@ -47,6 +47,7 @@ struct GemmPlan {
 int num_sms();
 CUtensorMap make_tmap_bf16(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
 GemmPlan plan_gemm(int m_tok, int n_out, int k);
+int* gemm_norm_counter();
 void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep,
                  float* workspace, size_t workspace_elems, cudaStream_t st);
 

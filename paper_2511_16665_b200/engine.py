@@ -205,6 +205,13 @@ class Engine:
         return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
                           [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), tree)
 
+    def probe_kernel(self, kind: int, m_tok: int, iters: int = 56):
+        """Live timing of one engine GEMM site (tlt_probe_kernel): returns
+        (avg_ms, algorithmic_bytes, flops) of one launch."""
+        ms, b, f = C.c_float(), C.c_double(), C.c_double()
+        _check(self.L.tlt_probe_kernel(self.h, kind, m_tok, iters, C.byref(ms), C.byref(b), C.byref(f)))
+        return ms.value, b.value, f.value
+
     def ar_step(self, slots):
         slots = np.asarray(slots, np.int32)
         out = np.zeros(len(slots), np.int32)
