@@ -182,7 +182,12 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0u;
+    // pair: rank = position in the CTA pair (cluster x); with split-K the
+    // cluster is (2, 1, splits) and the pair of split z has cluster ranks
+    // (2z, 2z+1): the leader (MMA issuer, full barriers) is rank 2z
+    const uint32_t rank = PAIR == 2 ? (blockIdx.x & 1u) : 0u;
+    const uint32_t lead_rank = PAIR == 2 ? 2u * blockIdx.z : 0u;
+    const uint16_t pair_mask = (uint16_t)(0x3u << lead_rank);
     // token tiles vary fastest: the CTAs sharing one weight tile run together,
     // so the weight tile is fetched from HBM once and re-read from L2
     const int n0 = (blockIdx.y * PAIR + rank) * kBlockM * wm;
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(192, 1)
     const int npre = min(stages, nkb);
     const uint64_t pol_w = policy_evict_first();  // weights: streamed once
     const uint64_t pol_x = policy_evict_last();   // activations: re-read by every weight tile
-    const uint32_t full_bar0 = PAIR == 2 ? mapa_shared(smem_u32(&full[0]), 0) : 0u;
+    const uint32_t full_bar0 = PAIR == 2 ? mapa_shared(smem_u32(&full[0]), lead_rank) : 0u;
     if (warp == 0 && lane == 0) {
         // weight tiles beyond the smem ring: L2 prefetch l2pf k-blocks ahead
         for (int i = npre; i < min(nkb, npre + l2pf); ++i)
@@ -301,8 +306,8 @@ __global__ void __launch_bounds__(192, 1)
                         }
                     }
                     if (PAIR == 2) {
-                        tc_commit_pair_mc(&empty[s], 0x3);
-                        if (i == nkb - 1) tc_commit_pair_mc(tfull, 0x3);
+                        tc_commit_pair_mc(&empty[s], pair_mask);
+                        if (i == nkb - 1) tc_commit_pair_mc(tfull, pair_mask);
                     } else {
                         tc_commit(&empty[s]);
                         if (i == nkb - 1) tc_commit(tfull);
@@ -369,8 +374,9 @@ __global__ void __launch_bounds__(192, 1)
             const int c = p / (kBlockM / 2);
             const int rp = (p % (kBlockM / 2)) * 2;
             float2 acc = make_float2(0.f, 0.f);
-            for (int zz = 0; zz < S; ++zz) {
-                const float2 v = *reinterpret_cast<const float2*>(cluster.map_shared_rank(P + c * kBlockM + rp, zz));
+            for (int zz = 0; zz < S; ++zz) {  // same pair position in every split: cluster rank rank + PAIR*zz
+                const float2 v = *reinterpret_cast<const float2*>(
+                    cluster.map_shared_rank(P + c * kBlockM + rp, (int)rank + PAIR * zz));
                 acc.x += v.x;
                 acc.y += v.y;
             }
@@ -726,6 +732,33 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     // plan with in-cluster split-K fills the machine better)
     const int pair_ctas = 2 * ((n_out + 2 * kBlockM - 1) / (2 * kBlockM)) * ((m_tok + pair_bn_max - 1) / pair_bn_max);
     static const int pair_min_ctas = env_knob("TLT_GEMM_PAIR_MIN_CTAS", 148);
+    static const int pair_split = env_knob("TLT_GEMM_PAIR_SPLIT", 1);
+    if (pair_split && pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas < pair_min_ctas) {
+        // few weight tiles (N = d): CTA pairs with <= 128-token tiles and
+        // split-K across a (2, 1, splits) cluster, reduced through DSMEM
+        const int n_tt = (m_tok + 127) / 128;
+        int bn = (m_tok + n_tt - 1) / n_tt;
+        bn = std::max(32, (bn + 15) / 16 * 16);
+        const int n_wt = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
+        const int ctas = 2 * n_wt * ((m_tok + bn - 1) / bn);
+        int splits = std::max(1, std::min({(2 * num_sms()) / ctas, g.kb_total / 4, kMaxSplits / 2}));
+        const int stage_bytes = kABytes + (bn / 2) * kBlockK * 2;
+        const int stages = std::max(2, std::min(8, (112 * 1024 - fixed) / stage_bytes));
+        if (splits > 1 && stages * stage_bytes >= bn * kBlockM * 4) {
+            g.pair = 2;
+            g.wm = 1;
+            g.bn = bn;
+            g.box_rows = bn / 2;
+            g.n_ttiles = (m_tok + bn - 1) / bn;
+            g.n_wtiles = n_wt;
+            g.stages = stages;
+            g.smem = stages * stage_bytes + fixed;
+            g.tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : 128;
+            g.kb_per_split = (g.kb_total + splits - 1) / splits;
+            g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+            return g;
+        }
+    }
     if (pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas >= pair_min_ctas) {
         g.pair = 2;
         g.wm = 1;
@@ -814,9 +847,10 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     }
     if (ep.kind == EPI_TOPK && g.splits > 1) throw CudaError("EPI_TOPK needs whole-K accumulators");
     if (g.splits > kMaxSplits) throw CudaError("split-K cluster larger than the portable cluster size");
-    if (g.pair == 2 && (g.splits != 1 || g.wm != 1 || g.bn % 16 || g.bn < 32 || g.bn > 256))
+    if (g.pair == 2 && (g.wm != 1 || g.bn % 16 || g.bn < 32 || g.bn > 256 || (g.splits > 1 && g.bn > 128) ||
+                        2 * g.splits > kMaxSplits))
         throw CudaError("invalid CTA-pair GEMM plan");
-    if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.bn * kBlockK * 2) < g.bn * kBlockM * 4))
+    if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.box_rows * kBlockK * 2) < g.bn * kBlockM * 4))
         throw CudaError("split-K partial does not fit the pipeline smem");
     dim3 grid(g.n_ttiles * g.pair, g.n_wtiles, g.splits);
     EpiParams epd = ep;

@@ -13,6 +13,8 @@ SHAPES = [
     (1, 3584, 3584), (1088, 256, 256),
     # CTA-pair (cta_group::2) path: M >= 192, ragged N / M tiles
     (192, 256, 256), (193, 512, 384), (2048, 3584, 1000), (700, 1024, 4608), (4096, 256, 512),
+    # CTA pair + split-K across a (2, 1, splits) cluster (few weight tiles)
+    (300, 4096, 512), (527, 3584, 3584), (272, 18944, 3584), (200, 2048, 1000),
 ]
 
 
