@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }  // namespace
 
 
-// Fused split combine: the last CTA (of the max_splits CTAs that share this
+// Fused split combine: the last CTA (of the non-empty split CTAs that share this
 // (request, KV head, query-vector tile)) merges every split's (m, l, O) in
 // fixed split order — the same arithmetic as k_attn_combine — and writes the
 // bf16 output, so no separate combine launch is needed. Called by all
@@ -71,7 +71,8 @@ __device__ __forceinline__ void attn_fused_combine(const AttnParams& p, int grp,
     __syncthreads();
     const int n_qt = gridDim.x;
     const long long cidx = ((long long)grp * p.KV + kvh) * n_qt + qtile;
-    if (threadIdx.x == 0) s_last = atomicAdd(p.counters + cidx, 1) == p.max_splits - 1;
+    const int n_active = min(p.max_splits, (p.g.lc[grp] + p.g.ntail[grp] + kSplit - 1) / kSplit);
+    if (threadIdx.x == 0) s_last = atomicAdd(p.counters + cidx, 1) == n_active - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
     const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
     const int total = slot >= 0 ? lc + ntail : 0;
     const int k0 = split * kSplit;
+    if (k0 >= total) return;  // empty split: nothing reads its partial (combine stops at the last non-empty one)
 
     // ---- stage Q (bf16) and the query rows' tail masks
     __shared__ int s_row[kQV];
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
     const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
     const int total = slot >= 0 ? lc + ntail : 0;
     const int k0 = split * kSplit;
+    if (k0 >= total) return;  // empty split: nothing reads its partial (combine stops at the last non-empty one)
     const int k1 = min(total, k0 + kSplit);
     const int row_base = qv0 / G;  // first request-local row of this CTA
 
