@@ -71,7 +71,7 @@ __device__ __forceinline__ void attn_fused_combine(const AttnParams& p, int grp,
     __syncthreads();
     const int n_qt = gridDim.x;
     const long long cidx = ((long long)grp * p.KV + kvh) * n_qt + qtile;
-    const int n_active = min(p.max_splits, (p.g.lc[grp] + p.g.ntail[grp] + kSplit - 1) / kSplit);
+    const int n_active = min(p.max_splits, (p.g.lc[grp] + p.g.ntail[grp] + p.chunk - 1) / p.chunk);
     if (threadIdx.x == 0) s_last = atomicAdd(p.counters + cidx, 1) == n_active - 1;
     __syncthreads();
     if (!s_last) return;
@@ -589,6 +589,276 @@ void launch_attention_tree_t(const AttnParams& p, cudaStream_t st) {
     launch_pdl(k_attention_tree<kHD>, grid, 256, smem, st, p);
 }
 
+// ---------------------------------------------------------------------------
+// Decode variant (<= 16 query vectors per request and KV head, e.g. plain AR
+// decode: 1 row x 7 q-heads): CTA = (KV head, request, key split of p.chunk
+// keys, a multiple of 256 chosen so the grid covers the SMs ~2x). All 128
+// threads stage 64-key K/V tiles into a 3-deep cp.async ring (contiguous
+// 16-byte chunks: committed-prefix keys are consecutive rows), and warp w
+// consumes keys [16w, 16w+16) of every tile (ldmatrix fragments), keeping its
+// own online-softmax state; the 4 warps merge in smem at the end. One
+// partial per split -> fused combine.
+constexpr int kDKeys = 64;
+constexpr int kDStages = 3;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(a));
+}
+
+template <int kHD>
+__global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
+    pdl_wait();
+    constexpr int kStride = kHD + 8;
+    constexpr int KS = kHD / 16;
+    constexpr int NT = kHD / 8;
+    constexpr int CPR = kHD / 8;  // 16-byte chunks per key row
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    bf16* Qs = reinterpret_cast<bf16*>(sm_raw);                 // [16][kStride]
+    bf16* Kb = Qs + kQV * kStride;                              // [stages][64][kStride]
+    bf16* Vb = Kb + kDStages * kDKeys * kStride;                // [stages][64][kStride]
+    uint32_t* Ms = reinterpret_cast<uint32_t*>(Vb + kDStages * kDKeys * kStride);  // [16][kMaskWords]
+    float* red = reinterpret_cast<float*>(Kb);                  // merge scratch (aliases the ring after the loop)
+    __shared__ int s_row[kQV];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int G = p.H / p.KV;
+    const int kvh = blockIdx.y;
+    const int grp = blockIdx.z / p.max_splits;
+    const int split = blockIdx.z % p.max_splits;
+    const int nqv = p.rows_per_req * G;
+    const int slot = p.g.slot[grp];
+    const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
+    const int total = slot >= 0 ? lc + ntail : 0;
+    const int k0 = split * p.chunk;
+    if (k0 >= total) return;  // empty split
+    const int k1 = min(total, k0 + p.chunk);
+    const int ntiles = (k1 - k0 + kDKeys - 1) / kDKeys;
+    const long long slot_base = ((long long)slot * p.KV + kvh) * p.cap;
+
+    auto load_tile = [&](int ti) {
+        const int st = ti % kDStages;
+        const int kb = k0 + ti * kDKeys;
+        const int nk = min(kDKeys, k1 - kb);
+        bf16* Kd = Kb + st * kDKeys * kStride;
+        bf16* Vd = Vb + st * kDKeys * kStride;
+#pragma unroll
+        for (int c = threadIdx.x; c < kDKeys * CPR; c += 128) {
+            const int j = c / CPR, w = c % CPR;
+            const bool ok = j < nk;
+            const int v = kb + j;
+            const long long ci = ok ? (v < lc ? v : tail0 + (v - lc)) : 0;
+            const long long off = (slot_base + ci) * kHD + w * 8;
+            cp_async16(Kd + j * kStride + w * 8, p.kc + off, ok);
+            cp_async16(Vd + j * kStride + w * 8, p.vc + off, ok);
+        }
+    };
+    // prologue: first stages in flight before Q / masks are staged
+#pragma unroll
+    for (int i = 0; i < kDStages - 1; ++i) {
+        if (i < ntiles) load_tile(i);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    if (threadIdx.x < kQV) {
+        const int gqv = threadIdx.x;
+        int row = -1;
+        if (gqv < nqv) {
+            row = grp * p.rows_per_req + gqv / G;
+            if (p.rows.slot[row] < 0) row = -1;
+        }
+        s_row[threadIdx.x] = row;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kQV * CPR; c += 128) {
+        const int l = c / CPR, w = c % CPR;
+        const int row = s_row[l];
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row >= 0) v = reinterpret_cast<const uint4*>(p.q + (long long)row * p.H * kHD + (kvh * G + l % G) * kHD)[w];
+        *reinterpret_cast<uint4*>(Qs + l * kStride + w * 8) = v;
+    }
+    const int mw = (ntail + 31) >> 5;
+    for (int c = threadIdx.x; c < kQV * kMaskWords; c += 128) {
+        const int l = c / kMaskWords, w = c % kMaskWords;
+        const int row = s_row[l];
+        Ms[c] = (row >= 0 && w < mw) ? p.rows.mask[(long long)row * kMaskWords + w] : 0u;
+    }
+    __syncthreads();
+    uint32_t qa[KS][4];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        qa[kk][0] = *reinterpret_cast<const uint32_t*>(Qs + g * kStride + kk * 16 + 2 * t);
+        qa[kk][1] = *reinterpret_cast<const uint32_t*>(Qs + (g + 8) * kStride + kk * 16 + 2 * t);
+        qa[kk][2] = *reinterpret_cast<const uint32_t*>(Qs + g * kStride + kk * 16 + 8 + 2 * t);
+        qa[kk][3] = *reinterpret_cast<const uint32_t*>(Qs + (g + 8) * kStride + kk * 16 + 8 + 2 * t);
+    }
+    const bool live0 = s_row[g] >= 0, live1 = s_row[g + 8] >= 0;
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
+
+    for (int ti = 0; ti < ntiles; ++ti) {
+        if (ti + kDStages - 1 < ntiles) load_tile(ti + kDStages - 1);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kDStages - 1) : "memory");
+        __syncthreads();
+        const int st = ti % kDStages;
+        const bf16* Ks = Kb + st * kDKeys * kStride + warp * 16 * kStride;  // this warp's 16 keys
+        const bf16* Vs = Vb + st * kDKeys * kStride + warp * 16 * kStride;
+        const int kb = k0 + ti * kDKeys + warp * 16;
+        const int nk = min(16, k1 - kb);
+        if (nk > 0) {
+            // ---- S = Q K^T (16 x 16): ldmatrix x4 = (keys 0-7 | 8-15) x (dims k | k+8)
+            float s[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+            const int mi = lane >> 3, r = lane & 7;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) {
+                uint32_t b0, b1, b2, b3;
+                // matrices: 0 = keys 0-7 dims kk*16+0..7, 1 = keys 0-7 dims +8, 2 = keys 8-15 dims +0, 3 = keys 8-15 dims +8
+                ldsm_x4(b0, b1, b2, b3, Ks + ((mi >> 1) * 8 + r) * kStride + kk * 16 + (mi & 1) * 8);
+                mma16816(s[0], qa[kk], b0, b1);
+                mma16816(s[1], qa[kk], b2, b3);
+            }
+            float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int col = nt * 8 + 2 * t + (e & 1);
+                    const int rr = e < 2 ? g : g + 8;
+                    const int v = kb + col;
+                    bool vis = col < nk && (e < 2 ? live0 : live1);
+                    if (vis && v >= lc) {
+                        const int tt = v - lc;
+                        vis = (Ms[rr * kMaskWords + (tt >> 5)] >> (tt & 31)) & 1u;
+                    }
+                    const float x = vis ? s[nt][e] * p.scale_log2 : -CUDART_INF_F;
+                    s[nt][e] = x;
+                    if (e < 2) mx0 = fmaxf(mx0, x);
+                    else mx1 = fmaxf(mx1, x);
+                }
+            }
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+            const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
+            const float c0 = nm0 == -CUDART_INF_F ? 1.f : exp2f(m0 - nm0);
+            const float c1 = nm1 == -CUDART_INF_F ? 1.f : exp2f(m1 - nm1);
+            m0 = nm0;
+            m1 = nm1;
+            l0 *= c0;
+            l1 *= c1;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                o[n][0] *= c0;
+                o[n][1] *= c0;
+                o[n][2] *= c1;
+                o[n][3] *= c1;
+            }
+            uint32_t pa[4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const float p0 = m0 == -CUDART_INF_F ? 0.f : exp2f(s[nt][0] - m0);
+                const float p1 = m0 == -CUDART_INF_F ? 0.f : exp2f(s[nt][1] - m0);
+                const float p2 = m1 == -CUDART_INF_F ? 0.f : exp2f(s[nt][2] - m1);
+                const float p3 = m1 == -CUDART_INF_F ? 0.f : exp2f(s[nt][3] - m1);
+                l0 += p0 + p1;
+                l1 += p2 + p3;
+                pa[nt * 2 + 0] = pack_bf16(p0, p1);
+                pa[nt * 2 + 1] = pack_bf16(p2, p3);
+            }
+            // A fragment order for m16n8k16: {rows g, k 0-7}, {rows g+8, k 0-7}, {rows g, k 8-15}, {rows g+8, k 8-15}
+            const uint32_t pf[4] = {pa[0], pa[1], pa[2], pa[3]};
+#pragma unroll
+            for (int nd = 0; nd < NT; nd += 2) {
+                const int key = (mi & 1) * 8 + r;
+                const int dim = (nd + (mi >> 1)) * 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_trans(b0, b1, b2, b3, Vs + key * kStride + dim);
+                mma16816(o[nd], pf, b0, b1);
+                mma16816(o[nd + 1], pf, b2, b3);
+            }
+        }
+        __syncthreads();  // stage st is refilled by a later iteration's prefetch
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    // ---- merge the 4 warps' partials (fixed order) in shared memory
+    __syncthreads();
+    float* wm = red;
+    float* wl = wm + 4 * kQV;
+    float* wo = wl + 4 * kQV;
+    if (t == 0) {
+        wm[warp * kQV + g] = m0;
+        wm[warp * kQV + g + 8] = m1;
+        wl[warp * kQV + g] = l0;
+        wl[warp * kQV + g + 8] = l1;
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        *reinterpret_cast<float2*>(wo + (warp * kQV + g) * kHD + n * 8 + 2 * t) = make_float2(o[n][0], o[n][1]);
+        *reinterpret_cast<float2*>(wo + (warp * kQV + g + 8) * kHD + n * 8 + 2 * t) = make_float2(o[n][2], o[n][3]);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kQV * kHD; c += blockDim.x) {
+        const int q = c / kHD, e = c % kHD;
+        if (q >= nqv) continue;
+        float M = -CUDART_INF_F;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w * kQV + q]);
+        float L = 0.f, O = 0.f;
+        if (M != -CUDART_INF_F)
+            for (int w = 0; w < 4; ++w) {
+                const float sc = exp2f(wm[w * kQV + q] - M);
+                L += wl[w * kQV + q] * sc;
+                O += wo[(w * kQV + q) * kHD + e] * sc;
+            }
+        const long long pidx = ((long long)(grp * p.max_splits + split) * p.qv_cap + q) * p.KV + kvh;
+        p.ws_o[pidx * kHD + e] = O;
+        if (e == 0) {
+            p.ws_m[pidx] = M;
+            p.ws_l[pidx] = L;
+        }
+    }
+    if (p.counters) attn_fused_combine<kHD>(p, grp, kvh, 0, 0, kQV);
+}
+
+template <int kHD>
+void launch_attention_dec_t(const AttnParams& p, cudaStream_t st) {
+    constexpr int kStride = kHD + 8;
+    const size_t ring = sizeof(bf16) * 2 * kDStages * kDKeys * kStride;
+    const size_t merge = sizeof(float) * (8 * kQV + 4 * kQV * kHD);
+    const size_t smem = sizeof(bf16) * kQV * kStride + (ring > merge ? ring : merge) + sizeof(uint32_t) * kQV * kMaskWords;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attention_dec<kHD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    dim3 grid(1, p.KV, p.n_groups * p.max_splits);
+    launch_pdl(k_attention_dec<kHD>, grid, 128, smem, st, p);
+}
+
+int attention_dec_chunk(int n_groups, int kv, int max_keys) {
+    // chunk (multiple of 256 keys) so that (groups x KV heads x splits) ~ 2 CTAs per SM
+    static const int off = [] {
+        const char* v = std::getenv("TLT_ATTN_DEC");
+        return v ? std::atoi(v) : 1;
+    }();
+    if (!off) return 0;
+    const int chunks = std::max(1, (max_keys + kSplit - 1) / kSplit);
+    const int want_splits = std::max(1, (2 * 148) / std::max(1, n_groups * kv));
+    const int per = std::max(1, (chunks + want_splits - 1) / want_splits);
+    return per * kSplit;
+}
+
 template <int kHD>
 size_t attention_mma_smem() {
     constexpr int kStride = kHD + 8;
@@ -629,6 +899,13 @@ void launch_attention_mma(const AttnParams& p, cudaStream_t st) {
             launch_attention_tree_t<128>(p, st);
         else
             launch_attention_tree_t<64>(p, st);
+        return;
+    }
+    if (p.dec) {
+        if (p.hd == 128)
+            launch_attention_dec_t<128>(p, st);
+        else
+            launch_attention_dec_t<64>(p, st);
         return;
     }
     if (p.hd == 128)

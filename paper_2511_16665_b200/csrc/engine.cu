@@ -358,6 +358,13 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)cfg.head_dim));
     p.impl = attn_impl_;
     p.chunk = p.impl == 1 ? attention_mma_split() : 512;
+    if (p.impl == 1 && rpr * (cfg.heads / cfg.kv_heads) <= 16) {
+        const int ch = attention_dec_chunk(ngroups, cfg.kv_heads, max_keys);
+        if (ch > 0) {
+            p.chunk = ch;
+            p.dec = 1;
+        }
+    }
     p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
     p.qv_cap = rpr * (cfg.heads / cfg.kv_heads);
     const size_t need = (size_t)ngroups * p.max_splits * p.qv_cap * cfg.kv_heads;

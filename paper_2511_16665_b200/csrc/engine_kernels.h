@@ -22,9 +22,11 @@ struct AttnParams {
     float *ws_m, *ws_l, *ws_o;
     int impl;  // 0: CUDA-core reference kernel, 1: tensor-core flash-decode (attn_mma.cu)
     int* counters;  // non-null: fused split combine (last CTA per tile), zeroed buffer
+    int dec;        // 1: decode kernel (<= 16 query vectors per request/head), chunk = multiple of 256
 };
 void launch_attention_mma(const AttnParams& p, cudaStream_t st);
 int attention_mma_split();
+int attention_dec_chunk(int n_groups, int kv, int max_keys);
 
 struct TreeParams {
     const StepIn* step;
