@@ -235,6 +235,7 @@ def kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind):
     traffic = traffic_table()
     out = []
     for name, kind, m, bound in PROBES:
+        print(f"[bench] probe {name}", file=sys.stderr, flush=True)
         ms, byts, flops = eng.probe_kernel(kind, m, 56)
         if bound == "hbm":
             ach = byts / (ms * 1e-3) / 1e9
@@ -278,6 +279,7 @@ def run_ours(a):
 
     for s in range(a.warmup):
         rollout(s)
+        print(f"[bench] warmup rollout {s} done", file=sys.stderr, flush=True)
     barrier(pg, local)
     res = []
     with ClockSampler(local) as clk:
@@ -305,6 +307,7 @@ def run_ours(a):
     sd_same = res[0] if res else None
     out = None
     if rank == 0:
+        print("[bench] probes", file=sys.stderr, flush=True)
         kernels = kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind)
         roof = kernels[0]
         cpu = None

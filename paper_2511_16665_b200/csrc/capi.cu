@@ -2,6 +2,8 @@
 // engine lifecycle, steps, graph pool, BEG-MAB / RNG / capture plan, and the
 // rollout loop (reference run_rollout, rollout.hpp:130-276).
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <deque>
 #include <cstring>
 #include <memory>
@@ -329,6 +331,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
             if (act.empty()) break;
             const int batch = (int)act.size();
             const bool sd = cfg->enable_sd && batch < cfg->elastic_threshold;  // rollout.hpp:174
+            static const bool trace = std::getenv("TLT_TRACE") != nullptr;
             auto emit = [&](int i, int32_t t) {
                 out->generated[(size_t)i * max_len_stride + glen[i]] = t;
                 glen[i] += 1;
@@ -343,6 +346,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 tlt_strategy s = cfg->fixed_strategy;
                 if (cfg->use_mab) s = mab->m->arms[mab->m->select(batch, select_rng)].strategy;
                 const int D = s.draft_depth;
+                if (trace) std::fprintf(stderr, "[tlt] sd b=%d (%d,%d,%d)\n", batch, D, s.top_k, s.tokens_to_verify);
                 acc_len.assign(batch, 0);
                 bonus.assign(batch, 0);
                 accepted.assign((size_t)batch * D, 0);
@@ -369,6 +373,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 if (cfg->use_mab) mab->m->record(s, (double)ms, acc_len.data(), batch);  // rollout.hpp:244
                 out->sd_steps += 1;
             } else {
+                if (trace) std::fprintf(stderr, "[tlt] ar b=%d\n", batch);
                 tok.assign(batch, 0);
                 ubuf.assign(batch, 0.0);
                 // sample_token consumes one draw per request (rollout.hpp:252-253)

@@ -374,8 +374,10 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
     p.ws_l = aws_l_;
     p.ws_o = aws_o_;
     static const int fused_combine = [] {
+        // off by default: the electing CTA's serial merge measured slower than
+        // the separate combine launch (rollout 5072 vs 5604 tok/s)
         const char* v = std::getenv("TLT_ATTN_FUSED_COMBINE");
-        return v ? std::atoi(v) : 1;
+        return v ? std::atoi(v) : 0;
     }();
     if (fused_combine && p.impl == 1) {
         if (!attn_counters_) {
