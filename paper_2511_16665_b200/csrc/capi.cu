@@ -346,7 +346,6 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 tlt_strategy s = cfg->fixed_strategy;
                 if (cfg->use_mab) s = mab->m->arms[mab->m->select(batch, select_rng)].strategy;
                 const int D = s.draft_depth;
-                if (trace) std::fprintf(stderr, "[tlt] sd b=%d (%d,%d,%d)\n", batch, D, s.top_k, s.tokens_to_verify);
                 acc_len.assign(batch, 0);
                 bonus.assign(batch, 0);
                 accepted.assign((size_t)batch * D, 0);
@@ -370,10 +369,15 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                     if (!done) emit(i, bonus[j]);
                 }
                 out->device_ms += ms;
+                if (trace) {
+                    int acc = 0;
+                    for (int j = 0; j < batch; ++j) acc += acc_len[j];
+                    std::fprintf(stderr, "[tlt] sd_ms %.3f b=%d D=%d k=%d T=%d acc=%d\n", ms, batch, D, s.top_k,
+                                 s.tokens_to_verify, acc);
+                }
                 if (cfg->use_mab) mab->m->record(s, (double)ms, acc_len.data(), batch);  // rollout.hpp:244
                 out->sd_steps += 1;
             } else {
-                if (trace) std::fprintf(stderr, "[tlt] ar b=%d\n", batch);
                 tok.assign(batch, 0);
                 ubuf.assign(batch, 0.0);
                 // sample_token consumes one draw per request (rollout.hpp:252-253)
@@ -386,6 +390,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                     emit(act[j], tok[j]);
                 }
                 out->device_ms += ms;
+                if (trace) std::fprintf(stderr, "[tlt] ar_ms %.3f b=%d\n", ms, batch);
                 out->plain_steps += 1;
             }
             for (int j = 0; j < batch; ++j)

@@ -293,6 +293,12 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
         g.kb_per_split = g.kb_total;
         g.splits = 1;
     }
+    if (ep_in.kind == EPI_QKV && g.pair == 1 && g.splits > 4) {
+        // measured (tools/probe.py): the QKV epilogue (bias, RoPE, KV-cache
+        // scatter) after the in-cluster reduction prefers <= 4 splits
+        g.kb_per_split = (g.kb_total + 3) / 4;
+        g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+    }
     const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.box_rows);
     EpiParams ep = ep_in;
     ep.n_out = N;
@@ -729,6 +735,18 @@ float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* fl
                     N = d;
                     K = cfg.ffn;
                 } break;
+                case 5: {  // o-proj + residual
+                    GemmPlan g = plan_gemm(M, d, nq);
+                    const CUtensorMap& tx = tmap_act(attn_, M, nq, nq, g.box_rows);
+                    ep.kind = EPI_RESID_ADD;
+                    ep.n_out = d;
+                    ep.m_tok = M;
+                    ep.out_f32 = x_;
+                    ep.ld_f32 = d;
+                    launch_gemm(g, w.tm_o, tx, ep, ws_, ws_elems_, st_);
+                    N = d;
+                    K = nq;
+                } break;
                 case 3:
                     ep.kind = EPI_F32;
                     ep.out_f32 = logits_;
@@ -753,7 +771,7 @@ float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* fl
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
     const double out_b = kind == 0 ? (double)M * N / 2 * 2 : kind == 1 ? (double)M * N * 2
-                         : kind == 2 ? (double)M * N * 8 : kind == 3 ? (double)M * N * 4 : (double)M * 16;
+                         : (kind == 2 || kind == 5) ? (double)M * N * 8 : kind == 3 ? (double)M * N * 4 : (double)M * 16;
     if (bytes) *bytes = (double)N * K * 2 + (double)M * K * 2 + out_b;
     if (flops) *flops = 2.0 * M * N * K;
     return ms / iters;

@@ -366,21 +366,37 @@ __global__ void __launch_bounds__(192, 1)
         cluster.sync();
         const int S = (int)gridDim.z;
         const int tv = min(bn, ep.m_tok - t0);
-        const int npairs = max(tv, 0) * (kBlockM / 2);
-        const int per = (npairs + S - 1) / S;
-        const int p0 = z * per, p1 = min(npairs, p0 + per);
+        // units of 8 consecutive rows of one token: all S remote float4 pairs
+        // are loaded before the fixed-order sum (DSMEM latency overlapped),
+        // then the vectorised epilogue
+        const int nunits = max(tv, 0) * (kBlockM / 8);
+        const int per = (nunits + S - 1) / S;
+        const int u0 = z * per, u1 = min(nunits, u0 + per);
         float* P = reinterpret_cast<float*>(smem);
-        for (int p = p0 + (int)threadIdx.x; p < p1; p += (int)blockDim.x) {
-            const int c = p / (kBlockM / 2);
-            const int rp = (p % (kBlockM / 2)) * 2;
-            float2 acc = make_float2(0.f, 0.f);
-            for (int zz = 0; zz < S; ++zz) {  // same pair position in every split: cluster rank rank + PAIR*zz
-                const float2 v = *reinterpret_cast<const float2*>(
-                    cluster.map_shared_rank(P + c * kBlockM + rp, (int)rank + PAIR * zz));
-                acc.x += v.x;
-                acc.y += v.y;
-            }
-            epi_pair(ep, t0 + c, n0 + rp, acc.x, acc.y, 0);
+        const float4* peer[kMaxSplits];
+#pragma unroll
+        for (int zz = 0; zz < kMaxSplits; ++zz)
+            peer[zz] = zz < S ? reinterpret_cast<const float4*>(cluster.map_shared_rank(P, (int)rank + PAIR * zz))
+                              : nullptr;
+        for (int u = u0 + (int)threadIdx.x; u < u1; u += (int)blockDim.x) {
+            const int c = u / (kBlockM / 8);
+            const int r8 = (u % (kBlockM / 8)) * 8;
+            const int off4 = (c * kBlockM + r8) >> 2;
+            float4 va[kMaxSplits], vb[kMaxSplits];
+#pragma unroll
+            for (int zz = 0; zz < kMaxSplits; ++zz)
+                if (zz < S) {
+                    va[zz] = peer[zz][off4];
+                    vb[zz] = peer[zz][off4 + 1];
+                }
+            float w[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int zz = 0; zz < kMaxSplits; ++zz)  // fixed split order: deterministic
+                if (zz < S) {
+                    w[0] += va[zz].x; w[1] += va[zz].y; w[2] += va[zz].z; w[3] += va[zz].w;
+                    w[4] += vb[zz].x; w[5] += vb[zz].y; w[6] += vb[zz].z; w[7] += vb[zz].w;
+                }
+            epi_vec8(ep, t0 + c, n0 + r8, w);
         }
         cluster.sync();  // peers' smem stays alive until every remote read is done
     }
@@ -819,7 +835,8 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     if (tiles < slots) splits = std::max(1, std::min(slots / tiles, g.kb_total / 4));
     // split-K CTAs of a tile form one cluster (portable size <= 8) and park
     // their fp32 partial in the pipeline smem for the DSMEM reduction
-    splits = std::min(splits, kMaxSplits);
+    static const int max_splits = env_knob("TLT_GEMM_MAX_SPLITS", kMaxSplits);
+    splits = std::min({splits, kMaxSplits, std::max(1, max_splits)});
     if (g.wm != 1 || g.stages * stage_bytes < bn * kBlockM * 4) splits = 1;
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
     g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
