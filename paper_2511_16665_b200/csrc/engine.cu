@@ -454,9 +454,12 @@ void Engine::lm_topk(const float* x, int n, int k, const int* live, bool want_lo
         launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
         count_launch();
     }
-    if (k > 1) {
+    static const int fused_k = [] {
+        const char* v = std::getenv("TLT_FUSED_TOPK_K");
+        return v ? std::atoi(v) : 1;
+    }();
+    if (k > 1 && (k > fused_k || want_logits)) {
         // top-k > 1 (drafter children): fp32 logits + multi-CTA chunked top-k
-        // (the per-column k-selection is too branchy for the MMA epilogue)
         EpiParams f{};
         f.kind = EPI_F32;
         f.out_f32 = logits_;

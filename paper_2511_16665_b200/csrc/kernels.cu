@@ -694,12 +694,76 @@ __global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ pa
     float m = -CUDART_INF_F, s = 0.f;
     TopK<K> t;
     t.init();
-    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
-        const float* pp = part + ((long long)i * m_tok + r) * W;
-        ms_merge(m, s, pp[0], pp[1]);
-        for (int c = 0; c < k; ++c) t.push(pp[2 + c], __float_as_int(pp[2 + k + c]));
+    if (K == 1) {
+        for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+            const float* pp = part + ((long long)i * m_tok + r) * W;
+            ms_merge(m, s, pp[0], pp[1]);
+            t.push(pp[2], __float_as_int(pp[2 + k]));
+        }
+        block_topk_finish<K>(t, m, s, sv, si, sm, ss);
+    } else {
+        // K > 1: the K-th largest per-lane best (within a warp) bounds the
+        // row's K-th value; only list entries at or above it are ranked
+        __shared__ float cv[kTopkCap];
+        __shared__ int ci[kTopkCap];
+        __shared__ int s_cnt;
+        __shared__ float s_thr;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        float best = -CUDART_INF_F;
+        for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+            const float* pp = part + ((long long)i * m_tok + r) * W;
+            ms_merge(m, s, pp[0], pp[1]);
+            best = fmaxf(best, pp[2]);
+        }
+        if (threadIdx.x == 0) s_cnt = 0;
+        float v = best;
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const float o = __shfl_xor_sync(0xffffffffu, v, stride);
+                const bool desc = (lane & size) == 0 || size == 32;
+                const bool lower = (lane & stride) == 0;
+                v = (lower == desc) ? fmaxf(v, o) : fminf(v, o);
+            }
+        }
+        const float kth = __shfl_sync(0xffffffffu, v, K - 1);
+        if (lane == 0) sv[warp] = kth;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float tt = sv[0];
+            for (int w = 1; w < 8; ++w) tt = fmaxf(tt, sv[w]);
+            s_thr = tt;
+        }
+        __syncthreads();
+        const float thr = s_thr;
+        for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+            const float* pp = part + ((long long)i * m_tok + r) * W;
+            if (pp[2] < thr) continue;
+            for (int c = 0; c < k; ++c) {
+                const float x = pp[2 + c];
+                if (x < thr) break;  // tile lists are sorted
+                const int p = atomicAdd(&s_cnt, 1);
+                if (p < kTopkCap) {
+                    cv[p] = x;
+                    ci[p] = __float_as_int(pp[2 + k + c]);
+                }
+            }
+        }
+        __syncthreads();
+        const int cnt = s_cnt;
+        if (cnt <= kTopkCap) {
+            for (int e = threadIdx.x; e < cnt; e += blockDim.x) t.push(cv[e], ci[e]);
+        } else {  // pathological ties: rank every entry at or above the bound
+            for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+                const float* pp = part + ((long long)i * m_tok + r) * W;
+                for (int c = 0; c < k; ++c)
+                    if (pp[2 + c] >= thr) t.push(pp[2 + c], __float_as_int(pp[2 + k + c]));
+            }
+        }
+        __syncthreads();
+        block_topk_finish<K>(t, m, s, sv, si, sm, ss);
     }
-    block_topk_finish<K>(t, m, s, sv, si, sm, ss);
     if (threadIdx.x < 32) {
 #pragma unroll
         for (int j = 0; j < K; ++j)

@@ -1,0 +1,5 @@
+#!/bin/bash
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+TLT_FUSED_TOPK_K=8 timeout 600 python -m pytest tests/test_gpu_parity_tiny.py -x -q 2>&1 | tail -1
+for v in 1 8; do echo "== fused_k=$v"; for b in 1 5 31; do
+  TLT_FUSED_TOPK_K=$v timeout 120 python tools/profile_step.py --model qwen2.5-7b --b $b --ar 0 --sd 3 --strategy 6,8,$([ $b = 5 ] && echo 48 || echo 16) --ctx 2400 --prompt 700 2>&1 | tail -1; done; done
