@@ -220,6 +220,14 @@ PROBES = [  # (name, probe kind, M, bound)  -- SURVEY.md 8(d) per-kernel rooflin
 ]
 
 
+ATTN_PROBES = [  # (name, requests, committed keys, query rows per request)
+    ("attention (flash-decode + combine), plain decode b=64 ctx=1024", 64, 1024, 1),
+    ("attention (flash-decode + combine), plain decode b=1 ctx=1024", 1, 1024, 1),
+    ("tree attention (+combine), verify b=5 T=48 ctx=700", 5, 700, 49),
+    ("tree attention (+combine), verify b=31 T=16 ctx=700", 31, 700, 17),
+]
+
+
 def traffic_table():
     """dram bytes per launch from the committed ncu --set full captures."""
     try:
@@ -249,6 +257,13 @@ def kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind):
         rec.update({"traffic": t, "algorithmic_bytes": int(byts), "M": m, "avg_launch_ms": round(ms, 4),
                     "peak_kind": peak_kind})
         out.append(rec)
+    for name, bb, ctx, rpr in ATTN_PROBES:
+        print(f"[bench] probe {name}", file=sys.stderr, flush=True)
+        ms, byts = eng.probe_attention(bb, ctx, rpr, 56)
+        ach = byts / (ms * 1e-3) / 1e9
+        out.append({"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
+                    "frac": round(ach / peak_gbs, 3), "traffic": None, "algorithmic_bytes": int(byts),
+                    "M": bb * rpr, "avg_launch_ms": round(ms, 4), "peak_kind": peak_kind})
     return out
 
 

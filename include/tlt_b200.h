@@ -250,6 +250,13 @@ TLT_API int tlt_debug_ar_logits(tlt_engine* e, float* logits, int b);
 TLT_API int tlt_probe_kernel(tlt_engine* e, int kind, int m_tok, int iters, float* avg_ms, double* bytes,
                              double* flops);
 
+/* Live timing of the engine's attention (flash-decode + split combine) on
+ * its stream over successive layers' caches: b requests x ctx committed keys
+ * x rows_per_req query rows (1 = plain decode, T+1 = tree verify). Reports
+ * the average per-layer duration and the algorithmic bytes (K/V read + q/out). */
+TLT_API int tlt_probe_attention(tlt_engine* e, int b, int ctx, int rows_per_req, int iters, float* avg_ms,
+                                double* bytes);
+
 /* ---- kernel-level entry points for unit tests ---------------------------- */
 /* Y = X W^T through the tcgen05 GEMM. kind: 0 f32 store, 1 bf16 store,
  * 3 SwiGLU (W rows interleaved gate/up). Returns the split-K factor used. */

@@ -347,12 +347,15 @@ __global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
 // of once per 16 (7 query heads x T+1 rows of a request share one KV head).
 // Same split alignment and partial layout as k_attention_mma, so
 // k_attn_combine merges either.
-constexpr int kTQV = 128;   // query vectors per CTA
 constexpr int kTKeys = 64;  // keys per stage
-constexpr int kTRows = kTQV / 2 + 2;  // >= distinct rows covered by 128 qv (G >= 2)
 
-template <int kHD>
-__global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
+// QV query vectors per CTA (QV / 16 warps): 128 shares each K/V tile widest,
+// 64 fits two CTAs per SM (more latency hiding when there are few CTAs)
+template <int kHD, int QV>
+__global__ void __launch_bounds__(QV * 2, QV == 64 ? 2 : 1) k_attention_tree(AttnParams p) {
+    constexpr int kTQV = QV;
+    constexpr int kTRows = kTQV / 2 + 2;  // >= distinct rows covered by QV qv (G >= 2)
+    constexpr int kThreads = QV * 2;
     pdl_wait();
     constexpr int kStride = kHD + 8;
     constexpr int KS = kHD / 16;
@@ -380,7 +383,27 @@ __global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
     const int k1 = min(total, k0 + kSplit);
     const int row_base = qv0 / G;  // first request-local row of this CTA
 
-    // ---- stage Q and the rows' tail masks
+    // ---- K/V tile loader (all threads): 64 keys x kHD of K and of V
+    const long long slot_base = ((long long)(slot < 0 ? 0 : slot) * p.KV + kvh) * p.cap;
+    auto load_tile = [&](int kb, int buf) {
+        bf16* Kd = Kb + buf * kTKeys * kStride;
+        bf16* Vd = Vb + buf * kTKeys * kStride;
+        const int nk = min(kTKeys, k1 - kb);
+#pragma unroll
+        for (int c = threadIdx.x; c < kTKeys * (kHD / 8); c += kThreads) {
+            const int j = c / (kHD / 8), w = c % (kHD / 8);
+            const bool ok = j < nk;
+            const int v = kb + j;
+            const long long ci = ok ? (v < lc ? v : tail0 + (v - lc)) : 0;
+            const long long off = (slot_base + ci) * kHD + w * 8;
+            cp_async16(Kd + j * kStride + w * 8, p.kc + off, ok);
+            cp_async16(Vd + j * kStride + w * 8, p.vc + off, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    load_tile(k0, 0);  // first K/V tile in flight while Q and the masks are staged
+
+    // ---- stage Q (async, zero-filled for padding rows) and the rows' tail masks
     if (threadIdx.x < kTQV) {
         const int gqv = qv0 + threadIdx.x;
         int lr = -1;
@@ -393,42 +416,28 @@ __global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
     __syncthreads();
     for (int c = threadIdx.x; c < kTQV * (kHD / 8); c += blockDim.x) {
         const int l = c / (kHD / 8), w = c % (kHD / 8);
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (s_lrow[l] >= 0) {
-            const int gqv = qv0 + l;
-            const int row = grp * p.rows_per_req + gqv / G;
-            const int head = kvh * G + gqv % G;
-            v = reinterpret_cast<const uint4*>(p.q + (long long)row * p.H * kHD + head * kHD)[w];
-        }
-        *reinterpret_cast<uint4*>(Qs + l * kStride + w * 8) = v;
+        const bool ok = s_lrow[l] >= 0;
+        const int gqv = qv0 + l;
+        const int row = ok ? grp * p.rows_per_req + gqv / G : 0;
+        const int head = kvh * G + gqv % G;
+        cp_async16(Qs + l * kStride + w * 8, p.q + (long long)row * p.H * kHD + head * kHD + w * 8, ok);
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     const int nrows = min(kTRows, p.rows_per_req - row_base);
     const int mw = (ntail + 31) >> 5;
-    for (int c = threadIdx.x; c < nrows * kMaskWords; c += blockDim.x) {
-        const int l = c / kMaskWords, w = c % kMaskWords;
+    for (int c = threadIdx.x; c < nrows * (kMaskWords / 4); c += blockDim.x) {
+        const int l = c / (kMaskWords / 4), w4 = c % (kMaskWords / 4);
         const int row = grp * p.rows_per_req + row_base + l;
-        Ms[c] = w < mw ? p.rows.mask[(long long)row * kMaskWords + w] : 0u;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (w4 * 4 < mw) v = reinterpret_cast<const uint4*>(p.rows.mask + (long long)row * kMaskWords)[w4];
+        const int w = w4 * 4;
+        if (w + 0 >= mw) v.x = 0u;
+        if (w + 1 >= mw) v.y = 0u;
+        if (w + 2 >= mw) v.z = 0u;
+        if (w + 3 >= mw) v.w = 0u;
+        *reinterpret_cast<uint4*>(Ms + l * kMaskWords + w) = v;
     }
-
-    // ---- K/V tile loader (all 256 threads): 64 keys x kHD of K and of V
-    const long long slot_base = ((long long)(slot < 0 ? 0 : slot) * p.KV + kvh) * p.cap;
-    auto load_tile = [&](int kb, int buf) {
-        bf16* Kd = Kb + buf * kTKeys * kStride;
-        bf16* Vd = Vb + buf * kTKeys * kStride;
-        const int nk = min(kTKeys, k1 - kb);
-#pragma unroll
-        for (int c = threadIdx.x; c < kTKeys * (kHD / 8); c += 256) {
-            const int j = c / (kHD / 8), w = c % (kHD / 8);
-            const bool ok = j < nk;
-            const int v = kb + j;
-            const long long ci = ok ? (v < lc ? v : tail0 + (v - lc)) : 0;
-            const long long off = (slot_base + ci) * kHD + w * 8;
-            cp_async16(Kd + j * kStride + w * 8, p.kc + off, ok);
-            cp_async16(Vd + j * kStride + w * 8, p.vc + off, ok);
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    if (k0 < k1) load_tile(k0, 0);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // Q (and K/V tile 0)
     __syncthreads();  // Q / masks staged
 
     // this warp's 16 query vectors
@@ -574,19 +583,19 @@ __global__ void __launch_bounds__(256, 1) k_attention_tree(AttnParams p) {
     if (p.counters) attn_fused_combine<kHD>(p, grp, kvh, blockIdx.x, qv0, qv0 + kTQV);
 }
 
-template <int kHD>
+template <int kHD, int QV>
 void launch_attention_tree_t(const AttnParams& p, cudaStream_t st) {
     constexpr int kStride = kHD + 8;
-    const size_t smem = sizeof(bf16) * (kTQV + 4 * kTKeys) * kStride + sizeof(uint32_t) * kTRows * kMaskWords;
+    const size_t smem = sizeof(bf16) * (QV + 4 * kTKeys) * kStride + sizeof(uint32_t) * (QV / 2 + 2) * kMaskWords;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_attention_tree<kHD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_attention_tree<kHD, QV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const int G = p.H / p.KV;
     const int nqv = p.rows_per_req * G;
-    dim3 grid((nqv + kTQV - 1) / kTQV, p.KV, p.n_groups * p.max_splits);
-    launch_pdl(k_attention_tree<kHD>, grid, 256, smem, st, p);
+    dim3 grid((nqv + QV - 1) / QV, p.KV, p.n_groups * p.max_splits);
+    launch_pdl(k_attention_tree<kHD, QV>, grid, QV * 2, smem, st, p);
 }
 
 // ---------------------------------------------------------------------------
@@ -821,6 +830,13 @@ __global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
                 L += wl[w * kQV + q] * sc;
                 O += wo[(w * kQV + q) * kHD + e] * sc;
             }
+        if (p.max_splits == 1) {  // single split: final normalised output, no combine
+            const int row = s_row[q];
+            if (row >= 0)
+                p.out[(long long)row * p.H * kHD + (kvh * G + q % G) * kHD + e] =
+                    __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+            continue;
+        }
         const long long pidx = ((long long)(grp * p.max_splits + split) * p.qv_cap + q) * p.KV + kvh;
         p.ws_o[pidx * kHD + e] = O;
         if (e == 0) {
@@ -828,7 +844,7 @@ __global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
             p.ws_l[pidx] = L;
         }
     }
-    if (p.counters) attn_fused_combine<kHD>(p, grp, kvh, 0, 0, kQV);
+    if (p.counters && p.max_splits > 1) attn_fused_combine<kHD>(p, grp, kvh, 0, 0, kQV);
 }
 
 template <int kHD>
@@ -853,8 +869,14 @@ int attention_dec_chunk(int n_groups, int kv, int max_keys) {
         return v ? std::atoi(v) : 1;
     }();
     if (!off) return 0;
+    static const int target_ctas = [] {
+        const char* v = std::getenv("TLT_ATTN_DEC_CTAS");
+        return v ? std::atoi(v) : 296;
+    }();
     const int chunks = std::max(1, (max_keys + kSplit - 1) / kSplit);
-    const int want_splits = std::max(1, (2 * 148) / std::max(1, n_groups * kv));
+    // >= one CTA per SM already: a single split (the kernel then writes the
+    // normalised output itself, no partials, no combine launch)
+    const int want_splits = n_groups * kv >= 148 ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
     const int per = std::max(1, (chunks + want_splits - 1) / want_splits);
     return per * kSplit;
 }
@@ -892,13 +914,24 @@ void launch_attention_mma(const AttnParams& p, cudaStream_t st) {
     // ... as long as that still yields enough CTAs to cover the SMs (at
     // batch 1 the 16-vector kernel's 8x more CTAs win)
     const int G = p.H / p.KV;
+    static const int tree_qv = [] {
+        const char* v = std::getenv("TLT_ATTN_TREE_QV");
+        return v ? std::atoi(v) : 64;
+    }();
     const long long tree_ctas =
-        (long long)((p.rows_per_req * G + kTQV - 1) / kTQV) * p.KV * p.n_groups * p.max_splits;
-    if (p.rows_per_req * G >= tree_min && G >= 2 && tree_ctas >= 96) {
-        if (p.hd == 128)
-            launch_attention_tree_t<128>(p, st);
-        else
-            launch_attention_tree_t<64>(p, st);
+        (long long)((p.rows_per_req * G + tree_qv - 1) / tree_qv) * p.KV * p.n_groups * p.max_splits;
+    if (p.rows_per_req * G >= tree_min && G >= 2 && tree_ctas >= 128) {
+        if (tree_qv == 128) {
+            if (p.hd == 128)
+                launch_attention_tree_t<128, 128>(p, st);
+            else
+                launch_attention_tree_t<64, 128>(p, st);
+        } else {
+            if (p.hd == 128)
+                launch_attention_tree_t<128, 64>(p, st);
+            else
+                launch_attention_tree_t<64, 64>(p, st);
+        }
         return;
     }
     if (p.dec) {

@@ -146,6 +146,12 @@ TLT_API int tlt_probe_kernel(tlt_engine* e, int kind, int m_tok, int iters, floa
     return guard([&] { *avg_ms = e->e->probe_kernel(kind, m_tok, iters < 1 ? 1 : iters, bytes, flops); });
 }
 
+TLT_API int tlt_probe_attention(tlt_engine* e, int b, int ctx, int rows_per_req, int iters, float* avg_ms,
+                                double* bytes) {
+    if (!e || !avg_ms) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { *avg_ms = e->e->probe_attention(b, ctx, rows_per_req, iters < 1 ? 1 : iters, bytes); });
+}
+
 TLT_API int tlt_set_debug(tlt_engine* e, int on) {
     if (!e) return fail(TLT_ERR_STATE, "null engine");
     e->e->set_debug(on != 0);

@@ -338,7 +338,11 @@ void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const C
     launch_gemm(g, tmW, tx, e, ws_, ws_elems_, st_);
     count_launch();
     if (norm_w) {
-        if (M <= 256)
+        static const int cluster_norm_max_m = [] {
+            const char* v = std::getenv("TLT_CLUSTER_NORM_MAX_M");
+            return v ? std::atoi(v) : 256;
+        }();
+        if (M <= cluster_norm_max_m)
             launch_reduce_resid_norm(nullptr, 0, 0, M, d, x_, norm_w, cfg.rms_eps, h_, st_);
         else
             launch_rmsnorm(x_, M, d, norm_w, cfg.rms_eps, h_, st_);
@@ -394,7 +398,7 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
         if ((long long)ngroups * cfg.kv_heads * n_qt <= (1 << 16)) p.counters = attn_counters_;
     }
     launch_attention(p, st_);
-    count_launch(p.counters ? 1 : 2);
+    count_launch(p.counters || (p.dec && p.max_splits == 1) ? 1 : 2);
 }
 
 // One decoder layer over R rows (residual x_ in place).
@@ -777,6 +781,48 @@ float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* fl
                          : (kind == 2 || kind == 5) ? (double)M * N * 8 : kind == 3 ? (double)M * N * 4 : (double)M * 16;
     if (bytes) *bytes = (double)N * K * 2 + (double)M * K * 2 + out_b;
     if (flops) *flops = 2.0 * M * N * K;
+    return ms / iters;
+}
+
+
+// Live timing of the engine's attention (tree-masked flash-decode + split
+// combine) over successive layers' caches: b requests with ctx committed keys
+// and rpr query rows each (rpr = 1: plain decode; T + 1: tree verify with a
+// chain mask). Cache contents are whatever the buffers hold.
+float Engine::probe_attention(int b, int ctx, int rpr, int iters, double* bytes) {
+    if (b < 1 || b > cfg.max_slots || rpr < 1 || b * rpr > R_ || ctx + rpr + 1 > cap_ || rpr > 32 * kMaskWords)
+        throw ConfigErr("probe", "attention probe shape out of range");
+    const int R = b * rpr;
+    std::vector<int> tok(R, 1), pos(R), slot(R), cidx(R), fk(R, 0), gs(b), glc(b), gt0(b), gnt(b);
+    std::vector<long long> fidx(R, 0);
+    std::vector<uint32_t> mask((size_t)R * kMaskWords, 0u);
+    for (int i = 0; i < b; ++i) {
+        gs[i] = i;
+        glc[i] = ctx;
+        gt0[i] = ctx;
+        gnt[i] = rpr;
+        for (int j = 0; j < rpr; ++j) {
+            const int r = i * rpr + j;
+            pos[r] = cidx[r] = ctx + j;
+            slot[r] = i;
+            for (int t = 0; t <= j; ++t) mask[(size_t)r * kMaskWords + (t >> 5)] |= 1u << (t & 31);
+        }
+    }
+    upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, gs, glc, gt0, gnt);
+    float ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {  // warm-up, then timed
+        CUDA_CHECK(cudaEventRecord(ev0_, st_));
+        for (int it = 0; it < iters; ++it) {
+            const int l = it % cfg.layers;
+            attention(kc_[l], vc_[l], cap_, prows_, pg_, rpr, b, ctx + rpr);
+        }
+        CUDA_CHECK(cudaEventRecord(ev1_, st_));
+        CUDA_CHECK(cudaEventSynchronize(ev1_));
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    }
+    const double kv = (double)b * (ctx + rpr) * cfg.kv_heads * cfg.head_dim * 2 * 2;
+    const double qo = (double)R * cfg.heads * cfg.head_dim * 2 * 2;
+    if (bytes) *bytes = kv + qo;
     return ms / iters;
 }
 

@@ -70,6 +70,7 @@ public:
     void graph_pool_clear();
     int bucket_hi_for(int b, int T) const;
     float probe_kernel(int kind, int M, int iters, double* bytes, double* flops);
+    float probe_attention(int b, int ctx, int rpr, int iters, double* bytes);
 
     // parity exports
     std::vector<std::vector<DebugExp>> dbg_exp;  // [request i] expansions of the last sd_step

@@ -394,6 +394,7 @@ void launch_attention(const AttnParams& p, cudaStream_t st) {
     if (p.impl == 1) {
         launch_attention_mma(p, st);  // tensor-core path (attn_mma.cu), chunk = 256 keys
         if (p.counters) return;       // split combine fused into the attention kernel
+        if (p.dec && p.max_splits == 1) return;  // decode kernel wrote the output itself
     } else if (p.hd == 128) {
         launch_pdl(k_attention<128>, grid, 128, 0, st, p);
     } else {
@@ -1213,9 +1214,8 @@ void launch_accept_greedy(const AcceptParams& p, cudaStream_t st) { launch_pdl(k
 // (tree slot lt+1+n_j -> lt+1+j, all sources read before any write), block y
 // == layers commits tokens (accepted ++ bonus) and target features of the
 // root + accepted rows into the per-slot histories.
-__global__ void k_commit(CommitParams p) {
+__global__ void __launch_bounds__(256) k_commit(CommitParams p) {
     pdl_wait();
-    extern __shared__ __align__(16) unsigned char cm_smem[];
     const int i = blockIdx.x;
     const bool live = i < p.b && p.step[i].slot >= 0;
     if (!live) return;
@@ -1223,24 +1223,36 @@ __global__ void k_commit(CommitParams p) {
     const int a = p.acc_len[i];
     const int y = blockIdx.y;
     if (y < p.layers) {
-        const int per = p.KV * p.hd;  // elements per cache position
-        bf16* buf = reinterpret_cast<bf16*>(cm_smem);  // [2][a][per]
-        for (int c = threadIdx.x; c < 2 * a * per; c += blockDim.x) {
-            const int which = c / (a * per), rem = c % (a * per);
-            const int jj = rem / per, e = rem % per;
-            const int h = e / p.hd, dd = e % p.hd;
-            const int src = lt + 1 + p.acc_nodes[(long long)i * p.maxD + jj];
-            const bf16* cache = which == 0 ? p.kc[y] : p.vc[y];
-            buf[c] = cache[(((long long)slot * p.KV + h) * p.cap + src) * p.hd + dd];
+        // 16-byte chunks of (K|V, accepted j, head h, chunk w): every source is
+        // read into registers before any destination is written (in-place
+        // compaction: a destination may be another accepted node's source)
+        const int cph = p.hd / 8;                  // chunks per head row
+        const int total = 2 * a * p.KV * cph;
+        constexpr int kPer = 16;                   // chunks per thread (2 * kMaxDepth * KV * cph <= 16 * 256)
+        uint4 v[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int c = threadIdx.x + u * 256;
+            if (c < total) {
+                const int which = c / (a * p.KV * cph), rem = c % (a * p.KV * cph);
+                const int jj = rem / (p.KV * cph), r2 = rem % (p.KV * cph);
+                const int h = r2 / cph, w = r2 % cph;
+                const int src = lt + 1 + p.acc_nodes[(long long)i * p.maxD + jj];
+                const bf16* cache = which == 0 ? p.kc[y] : p.vc[y];
+                v[u] = reinterpret_cast<const uint4*>(cache + (((long long)slot * p.KV + h) * p.cap + src) * p.hd)[w];
+            }
         }
         __syncthreads();
-        for (int c = threadIdx.x; c < 2 * a * per; c += blockDim.x) {
-            const int which = c / (a * per), rem = c % (a * per);
-            const int jj = rem / per, e = rem % per;
-            const int h = e / p.hd, dd = e % p.hd;
-            const int dst = lt + 1 + jj;
-            bf16* cache = which == 0 ? p.kc[y] : p.vc[y];
-            cache[(((long long)slot * p.KV + h) * p.cap + dst) * p.hd + dd] = buf[c];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int c = threadIdx.x + u * 256;
+            if (c < total) {
+                const int which = c / (a * p.KV * cph), rem = c % (a * p.KV * cph);
+                const int jj = rem / (p.KV * cph), r2 = rem % (p.KV * cph);
+                const int h = r2 / cph, w = r2 % cph;
+                bf16* cache = which == 0 ? p.kc[y] : p.vc[y];
+                reinterpret_cast<uint4*>(cache + (((long long)slot * p.KV + h) * p.cap + lt + 1 + jj) * p.hd)[w] = v[u];
+            }
         }
     } else {
         // tokens: accepted at lt+1.., bonus at lt+1+a
@@ -1248,19 +1260,22 @@ __global__ void k_commit(CommitParams p) {
             const int tokv = t < a ? p.acc_tok[(long long)i * p.maxD + t] : p.bonus[i];
             p.tok_hist[(long long)slot * p.cap + lt + 1 + t] = tokv;
         }
-        // features of root (verify row 0) and accepted nodes at positions lt..lt+a
-        for (int c = threadIdx.x; c < (a + 1) * p.d; c += blockDim.x) {
-            const int t = c / p.d, e = c % p.d;
+        // features of root (verify row 0) and accepted nodes at positions lt..lt+a (16-byte chunks)
+        const int cpr = p.d / 8;
+        for (int c = threadIdx.x; c < (a + 1) * cpr; c += blockDim.x) {
+            const int t = c / cpr, w = c % cpr;
             const int vrow = i * p.row_stride + (t == 0 ? 0 : 1 + p.acc_nodes[(long long)i * p.maxD + t - 1]);
-            p.feat_hist[((long long)slot * p.cap + lt + t) * p.d + e] = p.vfeat[(long long)vrow * p.d + e];
+            reinterpret_cast<uint4*>(p.feat_hist + ((long long)slot * p.cap + lt + t) * p.d)[w] =
+                reinterpret_cast<const uint4*>(p.vfeat + (long long)vrow * p.d)[w];
         }
         if (threadIdx.x == 0 && p.kv_len) p.kv_len[i] = lt + 1 + a;
     }
 }
 void launch_commit(const CommitParams& p, cudaStream_t st) {
-    const int smem = 2 * p.maxD * p.KV * p.hd * 2;
+    if (2 * p.maxD * p.KV * (p.hd / 8) > 16 * 256 || (p.hd % 8) || (p.d % 8))
+        throw CudaError("k_commit: per-thread chunk budget exceeded");
     dim3 grid(p.b_hi, p.layers + 1);
-    launch_pdl(k_commit, grid, 256, smem, st, p);
+    launch_pdl(k_commit, grid, 256, 0, st, p);
 }
 
 // AR commit: token at lt+1, feature at lt

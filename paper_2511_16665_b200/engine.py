@@ -212,6 +212,13 @@ class Engine:
         _check(self.L.tlt_probe_kernel(self.h, kind, m_tok, iters, C.byref(ms), C.byref(b), C.byref(f)))
         return ms.value, b.value, f.value
 
+    def probe_attention(self, b: int, ctx: int, rows_per_req: int = 1, iters: int = 56):
+        """Live timing of the attention of b requests x ctx keys (tlt_probe_attention):
+        returns (avg_ms, algorithmic_bytes) per layer."""
+        ms, by = C.c_float(), C.c_double()
+        _check(self.L.tlt_probe_attention(self.h, b, ctx, rows_per_req, iters, C.byref(ms), C.byref(by)))
+        return ms.value, by.value
+
     def ar_step(self, slots):
         slots = np.asarray(slots, np.int32)
         out = np.zeros(len(slots), np.int32)
