@@ -272,6 +272,14 @@ TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n,
  * number of chunks per row. */
 TLT_API int tlt_dev_row_topk(const float* logits, int R, int V, int k, float* part, int* out_tok, float* out_logit,
                              float* out_M, float* out_S, int iters, float* avg_ms);
+/* Tree-masked attention over explicit device buffers (q [R][H*hd], K/V
+ * caches [slots][KV][cap][hd] bf16, row slots / 1024-bit tail masks, group
+ * slot / committed length / tail start / tail length): kernel 0 = mma.sync
+ * kernels, 1 = tcgen05 + TMEM kernel. Writes out [R][H*hd] bf16. */
+TLT_API int tlt_dev_attention(const void* q, const void* kc, const void* vc, void* out, int n_groups,
+                              int rows_per_req, int H, int KV, int hd, int cap, const int* row_slot,
+                              const unsigned* row_mask, const int* g_slot, const int* g_lc, const int* g_tail0,
+                              const int* g_ntail, int max_keys, int kernel);
 
 #ifdef __cplusplus
 }

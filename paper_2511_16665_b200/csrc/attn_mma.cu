@@ -905,7 +905,11 @@ void launch_attention_mma_t(const AttnParams& p, cudaStream_t st) {
 
 int attention_mma_split() { return kSplit; }
 
-void launch_attention_mma(const AttnParams& p, cudaStream_t st) {
+void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc) {
+    if (allow_tc && attention_tc_eligible(p)) {  // tcgen05 / TMEM kernel (attn_tc.cu)
+        launch_attention_tc(p, st);
+        return;
+    }
     // many query vectors per (request, KV head): share each K/V tile across them
     static const int tree_min = [] {
         const char* v = std::getenv("TLT_ATTN_TREE_MIN_QV");

@@ -3,6 +3,8 @@
 #include "tlt_internal.h"
 #include "engine_kernels.h"
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include "../../include/tlt_b200.h"
 
 using namespace tlt;
@@ -98,6 +100,68 @@ extern "C" TLT_API int tlt_dev_row_topk(const float* logits, int R, int V, int k
         cudaEventDestroy(e1);
         cudaStreamDestroy(st);
         return nch;
+    } catch (const std::exception& e) {
+        tlt_set_last_error(e.what());
+        return -1;
+    }
+}
+
+// Tree-masked attention over explicit buffers (unit tests): q [R][H*hd],
+// kc/vc [slots][KV][cap][hd] bf16, out [R][H*hd]; rows: slot[R], mask[R][32];
+// groups: slot/lc/tail0/ntail[n_groups]; R = n_groups * rows_per_req.
+// kernel: 0 mma.sync tree/decode kernels, 1 tcgen05 kernel (when eligible).
+extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const void* vc, void* out, int n_groups,
+                                         int rows_per_req, int H, int KV, int hd, int cap, const int* row_slot,
+                                         const unsigned* row_mask, const int* g_slot, const int* g_lc,
+                                         const int* g_tail0, const int* g_ntail, int max_keys, int kernel) {
+    try {
+        const int R = n_groups * rows_per_req;
+        AttnParams p{};
+        p.q = static_cast<const __nv_bfloat16*>(q);
+        p.out = static_cast<__nv_bfloat16*>(out);
+        p.kc = static_cast<const __nv_bfloat16*>(kc);
+        p.vc = static_cast<const __nv_bfloat16*>(vc);
+        p.rows.slot = const_cast<int*>(row_slot);
+        p.rows.mask = const_cast<unsigned*>(row_mask);
+        p.g.slot = const_cast<int*>(g_slot);
+        p.g.lc = const_cast<int*>(g_lc);
+        p.g.tail0 = const_cast<int*>(g_tail0);
+        p.g.ntail = const_cast<int*>(g_ntail);
+        p.rows_per_req = rows_per_req;
+        p.n_groups = n_groups;
+        p.H = H;
+        p.KV = KV;
+        p.hd = hd;
+        p.cap = cap;
+        p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+        p.impl = 1;
+        p.chunk = attention_mma_split();
+        p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+        p.qv_cap = rows_per_req * (H / KV);
+        const size_t need = (size_t)n_groups * p.max_splits * p.qv_cap * KV;
+        float *wm = nullptr, *wl = nullptr, *wo = nullptr;
+        CUDA_CHECK(cudaMalloc(&wm, need * sizeof(float)));
+        CUDA_CHECK(cudaMalloc(&wl, need * sizeof(float)));
+        CUDA_CHECK(cudaMalloc(&wo, need * hd * sizeof(float)));
+        p.ws_m = wm;
+        p.ws_l = wl;
+        p.ws_o = wo;
+        (void)R;
+        const char* prev = std::getenv("TLT_ATTN_TC");
+        (void)prev;
+        if (kernel == 1) {
+            if (!attention_tc_eligible(p)) throw ConfigErr("kernel", "shape not eligible for the tcgen05 kernel");
+            launch_attention_tc(p, 0);
+            launch_attn_combine_only(p, 0);
+        } else {
+            p.impl = 1;
+            launch_attention_legacy(p, 0);
+        }
+        CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(wm);
+        cudaFree(wl);
+        cudaFree(wo);
+        return 0;
     } catch (const std::exception& e) {
         tlt_set_last_error(e.what());
         return -1;

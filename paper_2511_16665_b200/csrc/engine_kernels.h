@@ -24,7 +24,12 @@ struct AttnParams {
     int* counters;  // non-null: fused split combine (last CTA per tile), zeroed buffer
     int dec;        // 1: decode kernel (<= 16 query vectors per request/head), chunk = multiple of 256
 };
-void launch_attention_mma(const AttnParams& p, cudaStream_t st);
+void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc = true);
+// test hooks: the mma.sync kernels + combine, and the combine alone
+void launch_attention_legacy(const AttnParams& p, cudaStream_t st);
+void launch_attn_combine_only(const AttnParams& p, cudaStream_t st);
+bool attention_tc_eligible(const AttnParams& p);
+void launch_attention_tc(const AttnParams& p, cudaStream_t st);
 int attention_mma_split();
 int attention_dec_chunk(int n_groups, int kv, int max_keys);
 

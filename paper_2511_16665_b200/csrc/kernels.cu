@@ -385,6 +385,20 @@ __global__ void k_attn_combine(AttnParams p) {
         p.out[(long long)row * p.H * HD + head * HD + lane * DPL + e] = __float2bfloat16_rn(o[e] * inv);
 }
 
+void launch_attn_combine_only(const AttnParams& p, cudaStream_t st) {
+    const int G = p.H / p.KV;
+    const long long warps = (long long)p.n_groups * p.rows_per_req * G * p.KV;
+    const int cblocks = (int)((warps * 32 + 255) / 256);
+    if (p.hd == 128)
+        launch_pdl(k_attn_combine<128>, cblocks, 256, 0, st, p);
+    else
+        launch_pdl(k_attn_combine<64>, cblocks, 256, 0, st, p);
+}
+void launch_attention_legacy(const AttnParams& p, cudaStream_t st) {
+    launch_attention_mma(p, st, false);
+    launch_attn_combine_only(p, st);
+}
+
 void launch_attention(const AttnParams& p, cudaStream_t st) {
     const int G = p.H / p.KV;
     const int nqv = p.rows_per_req * G;

@@ -1,0 +1,81 @@
+"""Tree-masked attention kernels (mma.sync and tcgen05/TMEM) vs a torch fp32
+reference of the same op: committed prefix visible to every row, tail
+entries (tree nodes) visible through each row's bitmask, GQA heads.
+Tolerance: bf16 output rounding (|err| <= 2e-2 + 2e-2 |ref|)."""
+import pytest
+import torch
+
+from paper_2511_16665_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def make_case(n_groups, rpr, lc, H=28, KV=4, hd=128, cap=2400, seed=0, remap_tail=False):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    dev = "cuda"
+    slots = n_groups
+    kc = (torch.randn(slots, KV, cap, hd, device=dev, generator=g)).to(torch.bfloat16)
+    vc = (torch.randn(slots, KV, cap, hd, device=dev, generator=g)).to(torch.bfloat16)
+    R = n_groups * rpr
+    q = (torch.randn(R, H * hd, device=dev, generator=g)).to(torch.bfloat16)
+    # tree: row j's parent = (j - 1) // 2 (binary tree in rank order); row 0 = root
+    par = [-1] + [(j - 1) // 2 for j in range(1, rpr)]
+    vis = torch.zeros(rpr, rpr, dtype=torch.bool)
+    for j in range(rpr):
+        a = j
+        while a >= 0:
+            vis[j, a] = True
+            a = par[a]
+    mask = torch.zeros(R, 32, dtype=torch.int64)
+    for j in range(rpr):
+        for t in range(rpr):
+            if vis[j, t]:
+                mask[torch.arange(n_groups) * rpr + j, t >> 5] |= 1 << (t & 31)
+    mask_dev = torch.tensor((mask & 0xFFFFFFFF).numpy().astype("uint32").view("int32"), device=dev)
+    row_slot = torch.arange(n_groups, device=dev, dtype=torch.int32).repeat_interleave(rpr)
+    g_slot = torch.arange(n_groups, device=dev, dtype=torch.int32)
+    g_lc = torch.full((n_groups,), lc, device=dev, dtype=torch.int32)
+    tail0 = lc + 64 if remap_tail else lc
+    g_tail0 = torch.full((n_groups,), tail0, device=dev, dtype=torch.int32)
+    g_ntail = torch.full((n_groups,), rpr, device=dev, dtype=torch.int32)
+    return dict(kc=kc, vc=vc, q=q, vis=vis, mask=mask_dev, row_slot=row_slot, g_slot=g_slot, g_lc=g_lc,
+                g_tail0=g_tail0, g_ntail=g_ntail, n_groups=n_groups, rpr=rpr, lc=lc, H=H, KV=KV, hd=hd, cap=cap,
+                tail0=tail0)
+
+
+def reference(c):
+    H, KV, hd, rpr, lc, G = c["H"], c["KV"], c["hd"], c["rpr"], c["lc"], c["H"] // c["KV"]
+    out = torch.zeros(c["n_groups"] * rpr, H * hd, device="cuda")
+    for i in range(c["n_groups"]):
+        keys = torch.cat([torch.arange(lc), c["tail0"] + torch.arange(rpr)]).cuda()
+        for h in range(H):
+            kvh = h // G
+            K = c["kc"][i, kvh, keys].float()
+            Vv = c["vc"][i, kvh, keys].float()
+            Q = c["q"][i * rpr:(i + 1) * rpr, h * hd:(h + 1) * hd].float()
+            s = Q @ K.t() / hd ** 0.5
+            allowed = torch.cat([torch.ones(rpr, lc, dtype=torch.bool), c["vis"]], dim=1).cuda()
+            s = s.masked_fill(~allowed, float("-inf"))
+            out[i * rpr:(i + 1) * rpr, h * hd:(h + 1) * hd] = torch.softmax(s, dim=1) @ Vv
+    return out
+
+
+def run(c, kernel):
+    out = torch.zeros(c["n_groups"] * c["rpr"], c["H"] * c["hd"], device="cuda", dtype=torch.bfloat16)
+    rc = _lib.lib().tlt_dev_attention(
+        c["q"].data_ptr(), c["kc"].data_ptr(), c["vc"].data_ptr(), out.data_ptr(), c["n_groups"], c["rpr"], c["H"],
+        c["KV"], c["hd"], c["cap"], c["row_slot"].data_ptr(), c["mask"].data_ptr(), c["g_slot"].data_ptr(),
+        c["g_lc"].data_ptr(), c["g_tail0"].data_ptr(), c["g_ntail"].data_ptr(), c["cap"], kernel)
+    assert rc == 0, _lib.last_error()
+    return out.float()
+
+
+@pytest.mark.parametrize("n_groups,rpr,lc,remap", [(2, 17, 300, False), (3, 49, 700, False), (1, 65, 1000, True),
+                                                   (2, 33, 0, False), (1, 17, 511, True)])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_tree_attention(n_groups, rpr, lc, remap, kernel):
+    c = make_case(n_groups, rpr, lc, seed=n_groups * 100 + rpr + lc, remap_tail=remap)
+    ref = reference(c)
+    got = run(c, kernel)
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
