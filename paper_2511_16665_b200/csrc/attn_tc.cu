@@ -324,6 +324,11 @@ __global__ void __launch_bounds__(256, 1) k_attention_tc(AttnParams p, int dbg_s
 
 size_t attention_tc_smem() { return 1024 + 32768 + 2 * 65536 + kRows * kMaskWords * 4 + 64; }
 
+bool attention_tc_shape_ok(const AttnParams& p) {
+    const int G = p.H / p.KV;
+    return p.hd == kHDt && G >= 2 && p.rows_per_req > 1 && p.rows_per_req * G > 16 && !p.dec && p.chunk == kKeys;
+}
+
 bool attention_tc_eligible(const AttnParams& p) {
     static const int on = [] {
         // off by default: correct (tests/test_gpu_attention.py) but measured
@@ -332,9 +337,7 @@ bool attention_tc_eligible(const AttnParams& p) {
         const char* v = std::getenv("TLT_ATTN_TC");
         return v ? std::atoi(v) : 0;
     }();
-    const int G = p.H / p.KV;
-    return on && p.hd == kHDt && G >= 2 && p.rows_per_req > 1 && p.rows_per_req * G > 16 && !p.dec &&
-           p.chunk == kKeys;
+    return on && attention_tc_shape_ok(p);
 }
 
 void launch_attention_tc(const AttnParams& p, cudaStream_t st) {

@@ -150,7 +150,7 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
         const char* prev = std::getenv("TLT_ATTN_TC");
         (void)prev;
         if (kernel == 1) {
-            if (!attention_tc_eligible(p)) throw ConfigErr("kernel", "shape not eligible for the tcgen05 kernel");
+            if (!attention_tc_shape_ok(p)) throw ConfigErr("kernel", "shape not eligible for the tcgen05 kernel");
             launch_attention_tc(p, 0);
             launch_attn_combine_only(p, 0);
         } else {

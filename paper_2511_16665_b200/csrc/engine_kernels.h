@@ -29,6 +29,7 @@ void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc = 
 void launch_attention_legacy(const AttnParams& p, cudaStream_t st);
 void launch_attn_combine_only(const AttnParams& p, cudaStream_t st);
 bool attention_tc_eligible(const AttnParams& p);
+bool attention_tc_shape_ok(const AttnParams& p);
 void launch_attention_tc(const AttnParams& p, cudaStream_t st);
 int attention_mma_split();
 int attention_dec_chunk(int n_groups, int kv, int max_keys);
