@@ -309,6 +309,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         for (int i = 0; i < n; ++i) req_rng.push_back(root.fork(0x52515254ULL + (uint64_t)request_ids[i]));
         tlt::Rng select_rng = root.fork(0x53454CULL);
         E.prefill(n, slots.data(), prompt_lens, prompts);
+        if (std::getenv("TLT_TRACE")) std::fprintf(stderr, "[tlt] prefill_ms %.3f n=%d\n", E.last_prefill_ms, n);
         std::vector<int> running(n, 1), glen(n, 0);
         out->sd_steps = out->plain_steps = out->verify_events = out->accepted_total = out->emitted_total = 0;
         out->device_ms = E.last_prefill_ms;

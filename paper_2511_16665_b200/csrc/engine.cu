@@ -591,7 +591,11 @@ void Engine::prefill(int b, const int32_t* slots, const int32_t* lens, const int
     for (int i = 0; i < b; ++i)
         CUDA_CHECK(cudaMemcpyAsync(tok_hist_ + (size_t)slots[i] * cap_, tokens + off[i], sizeof(int32_t) * lens[i],
                                    cudaMemcpyHostToDevice, st_));
-    const int chunk = std::min(512, std::max(1, R_ / 2));
+    // rows per request per forward: the longest prompt (no padding rows for
+    // short prompts), at most 512 so several requests share each GEMM
+    int longest = 1;
+    for (int i = 0; i < b; ++i) longest = std::max(longest, lens[i] - 1);
+    const int chunk = std::max(16, std::min({512, std::max(1, R_ / 2), (longest + 15) / 16 * 16}));
     // process requests in groups; each group forward has stride = chunk rows per request
     for (int i0 = 0; i0 < b;) {
         int nreq = std::max(1, std::min(b - i0, R_ / chunk));

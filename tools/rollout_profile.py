@@ -13,6 +13,11 @@ for line in open(sys.argv[1]):
         a = agg[key]
         a[0] += 1; a[1] += ms; a[2] += acc + b; a[3] += b
         continue
+    m = re.match(r"\[tlt\] prefill_ms ([\d.]+) n=(\d+)", line)
+    if m:
+        a = agg["prefill"]
+        a[0] += 1; a[1] += float(m[1]); a[3] += int(m[2])
+        continue
     m = re.match(r"\[tlt\] ar_ms ([\d.]+) b=(\d+)", line)
     if m:
         ms, b = float(m[1]), int(m[2])
