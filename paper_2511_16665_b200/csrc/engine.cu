@@ -293,10 +293,14 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
         g.kb_per_split = g.kb_total;
         g.splits = 1;
     }
-    if (ep_in.kind == EPI_QKV && g.pair == 1 && g.splits > 4) {
+    static const int qkv_max_splits = [] {
+        const char* v = std::getenv("TLT_QKV_MAX_SPLITS");
+        return v ? std::atoi(v) : 4;
+    }();
+    if (ep_in.kind == EPI_QKV && g.pair == 1 && g.splits > qkv_max_splits) {
         // measured (tools/probe.py): the QKV epilogue (bias, RoPE, KV-cache
         // scatter) after the in-cluster reduction prefers <= 4 splits
-        g.kb_per_split = (g.kb_total + 3) / 4;
+        g.kb_per_split = (g.kb_total + qkv_max_splits - 1) / qkv_max_splits;
         g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
     }
     const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.box_rows);

@@ -1,6 +1,4 @@
 #!/bin/bash
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-S="1:1 1:16 1:48 1:100 1:245 1:343 5:1 5:48 5:245 5:527 2:1 2:48 2:245 2:527 0:245"
-cfg() { echo "== $*"; env "$@" timeout 200 python tools/probe.py $S; }
-cfg X=1
-cfg TLT_GEMM_PAIR_SPLIT=0
+S="1:1 1:17 1:48 1:100 5:1 5:17 5:48"
+for c in 4 8 2; do echo "== qkv max splits $c"; TLT_QKV_MAX_SPLITS=$c timeout 200 python tools/probe.py $S; done
+for c in 8 4; do echo "== global max splits $c"; TLT_GEMM_MAX_SPLITS=$c timeout 200 python tools/probe.py 5:1 5:17 5:48 2:1 2:17 2:48; done
