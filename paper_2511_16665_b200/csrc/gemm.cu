@@ -342,14 +342,14 @@ __global__ void __launch_bounds__(192, 1)
         const int row = na + q * 32 + lane;
         const int n_even = row & ~1;
         if (ep.kind == EPI_TOPK) {
-            float* tr = align16f(tmem_holder + 4);  // [16 cols][128 vocab rows]
+            float* tr = reinterpret_cast<float*>(smem);  // [16 cols][128 vocab rows] over the drained ring
             const int tile = (blockIdx.y * PAIR + rank) * wm + a;
             if (ep.topk_k <= 1)
                 epi_topk_tile<1>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
             else
                 epi_topk_tile<kEpiTopkMax>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
         } else {
-            epi_tile_staged(ep, tm_a, q, lane, na, t0, bn, align16f(tmem_holder + 4));
+            epi_tile_staged(ep, tm_a, q, lane, na, t0, bn, reinterpret_cast<float*>(smem));
         }
         (void)n_even;
         }  // a
@@ -731,7 +731,9 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     static const int l2pf = env_knob("TLT_GEMM_L2PF", 0);
     g.l2pf = l2pf;
     g.kb_total = (k + kBlockK - 1) / kBlockK;
-    const int fixed = 1024 + 16 * 8 + 64 + 16 * 128 * 4;
+    // ring + barriers + alignment slack; the epilogue's 8 KB staging reuses
+    // the drained ring (all MMAs complete before the epilogue starts)
+    const int fixed = 1024 + 256;
     // Tensor-bound regime: CTA pairs (cta_group::2, 256 weight rows x up to
     // 256 tokens per pair), no split-K.
     static const int pair_min_m = env_knob("TLT_GEMM_PAIR_MIN_M", 192);

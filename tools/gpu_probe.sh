@@ -1,4 +1,3 @@
 #!/bin/bash
-S="1:1 1:17 1:48 1:100 5:1 5:17 5:48"
-for c in 4 8 2; do echo "== qkv max splits $c"; TLT_QKV_MAX_SPLITS=$c timeout 200 python tools/probe.py $S; done
-for c in 8 4; do echo "== global max splits $c"; TLT_GEMM_MAX_SPLITS=$c timeout 200 python tools/probe.py 5:1 5:17 5:48 2:1 2:17 2:48; done
+timeout 300 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_parity_tiny.py -x -q 2>&1 | tail -1
+timeout 200 python tools/probe.py 0:17 0:245 0:272 0:527 0:1040 2:17 2:245 2:527 5:245 1:245 3:240 3:496 4:17 4:272
