@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(192, 1)
             const int kc = (kb0 + i) * kBlockK;
             if (PAIR == 2) {
                 if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * (a_bytes + b_bytes));
-                tma_load_2d_pair(sA + i * a_bytes, &tmW, full_bar0 + 8u * i, kc, n0, pol_w);
+                for (int a = 0; a < wm; ++a)
+                    tma_load_2d_pair(sA + i * a_bytes + a * kABytes, &tmW, full_bar0 + 8u * i, kc, n0 + a * kBlockM,
+                                     pol_w);
             } else {
                 mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
                 for (int a = 0; a < wm; ++a)
@@ -272,7 +274,9 @@ __global__ void __launch_bounds__(192, 1)
                 mbar_wait(&empty[s], ph ^ 1);
                 if (PAIR == 2) {
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
-                    tma_load_2d_pair(sA + s * a_bytes, &tmW, full_bar0 + 8u * s, kc, n0, pol_w);
+                    for (int a = 0; a < wm; ++a)
+                        tma_load_2d_pair(sA + s * a_bytes + a * kABytes, &tmW, full_bar0 + 8u * s, kc,
+                                         n0 + a * kBlockM, pol_w);
                     tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows, pol_x);
                 } else {
                     mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(192, 1)
                             // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
                             if (ep.dbg & 1) continue;  // diagnostics: loads only
                             if (PAIR == 2)
-                                tc_mma_bf16_pair(tmem, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                                tc_mma_bf16_pair(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
                             else
                                 tc_mma_bf16(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
                         }
@@ -780,16 +784,27 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     if (pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas >= pair_min_ctas) {
         g.pair = 2;
         g.wm = 1;
+        static const int pair_wm2 = env_knob("TLT_GEMM_PAIR_WM2", 0);  // measured slower (exposed epilogue, 1 CTA/SM)
+        // two 256-row pair tiles per cluster (512 weight rows x bn tokens,
+        // 1 CTA/SM): halves the token-tile TMA traffic per FLOP, the bound of
+        // the 2-CTA/SM plan at mid M (chip TMA throughput)
+        if (pair_wm2 && m_tok >= 384 && (n_out + 4 * kBlockM - 1) / (4 * kBlockM) * 2 >= num_sms() / 2) g.wm = 2;
         const int n_tt = (m_tok + pair_bn_max - 1) / pair_bn_max;
         int bn = (m_tok + n_tt - 1) / n_tt;
         bn = std::max(32, (bn + 15) / 16 * 16);
         g.bn = bn;
         g.box_rows = bn / 2;
         g.n_ttiles = (m_tok + bn - 1) / bn;
-        g.n_wtiles = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
-        const int stage_bytes = kABytes + g.box_rows * kBlockK * 2;
+        g.n_wtiles = (n_out + 2 * kBlockM * g.wm - 1) / (2 * kBlockM * g.wm);
+        const int stage_bytes = g.wm * kABytes + g.box_rows * kBlockK * 2;
         g.kb_per_split = g.kb_total;
         g.splits = 1;
+        if (g.wm == 2) {
+            g.stages = std::max(2, std::min(8, (220 * 1024 - fixed) / stage_bytes));
+            g.smem = g.stages * stage_bytes + fixed;
+            g.tmem_cols = 2 * bn <= 256 ? 256 : 512;
+            return g;
+        }
         if (persist >= 1 && m_tok >= pair_persist_min_m) {
             // persistent: one pair per 2 SMs, full smem ring, 2 TMEM accumulators
             const int pfixed = 1024 + 32 * 8 + 16 + 16 * 128 * 4;
@@ -866,7 +881,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     }
     if (ep.kind == EPI_TOPK && g.splits > 1) throw CudaError("EPI_TOPK needs whole-K accumulators");
     if (g.splits > kMaxSplits) throw CudaError("split-K cluster larger than the portable cluster size");
-    if (g.pair == 2 && (g.wm != 1 || g.bn % 16 || g.bn < 32 || g.bn > 256 || (g.splits > 1 && g.bn > 128) ||
+    if (g.pair == 2 && ((g.wm != 1 && (g.splits != 1 || g.persist)) || g.bn % 16 || g.bn < 32 || g.bn > 256 || (g.splits > 1 && g.bn > 128) ||
                         2 * g.splits > kMaxSplits))
         throw CudaError("invalid CTA-pair GEMM plan");
     if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.box_rows * kBlockK * 2) < g.bn * kBlockM * 4))

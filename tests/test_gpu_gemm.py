@@ -15,6 +15,8 @@ SHAPES = [
     (192, 256, 256), (193, 512, 384), (2048, 3584, 1000), (700, 1024, 4608), (4096, 256, 512),
     # CTA pair + split-K across a (2, 1, splits) cluster (few weight tiles)
     (300, 4096, 512), (527, 3584, 3584), (272, 18944, 3584), (200, 2048, 1000),
+    # CTA pair with two 256-row sub-tiles per cluster (M >= 384, many weight tiles), ragged N
+    (400, 512, 38000), (1000, 256, 40000),
 ]
 
 

@@ -1,3 +1,3 @@
 #!/bin/bash
-timeout 300 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_parity_tiny.py -x -q 2>&1 | tail -1
-timeout 200 python tools/probe.py 0:17 0:245 0:272 0:527 0:1040 2:17 2:245 2:527 5:245 1:245 3:240 3:496 4:17 4:272
+timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -1
+for v in 0 1; do echo "== wm2 $v"; TLT_GEMM_PAIR_WM2=$v timeout 200 python tools/probe.py 0:384 0:496 0:527 0:768 0:1040 3:496 3:1040; done
