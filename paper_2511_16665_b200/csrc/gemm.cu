@@ -23,7 +23,8 @@ namespace tlt {
 constexpr int kBlockM = 128;  // weight rows per tile (MMA M)
 constexpr int kBlockK = 64;   // 64 bf16 = one 128-byte swizzle row
 constexpr int kABytes = kBlockM * kBlockK * 2;
-constexpr int kMaxSplits = 8;  // portable thread-block cluster size
+constexpr int kMaxSplits = 16;  // split-K cluster size (> 8 needs the non-portable cluster attribute)
+constexpr int kPeerBatch = 8;   // peers whose partials are loaded together in the DSMEM reduction
 
 // LM-head epilogue (EPI_TOPK) for one 128-vocab x bn-token accumulator tile.
 // Per 16-token chunk the 4 epilogue warps transpose the accumulators through
@@ -377,29 +378,28 @@ __global__ void __launch_bounds__(192, 1)
         const int per = (nunits + S - 1) / S;
         const int u0 = z * per, u1 = min(nunits, u0 + per);
         float* P = reinterpret_cast<float*>(smem);
-        const float4* peer[kMaxSplits];
-#pragma unroll
-        for (int zz = 0; zz < kMaxSplits; ++zz)
-            peer[zz] = zz < S ? reinterpret_cast<const float4*>(cluster.map_shared_rank(P, (int)rank + PAIR * zz))
-                              : nullptr;
         for (int u = u0 + (int)threadIdx.x; u < u1; u += (int)blockDim.x) {
             const int c = u / (kBlockM / 8);
             const int r8 = (u % (kBlockM / 8)) * 8;
             const int off4 = (c * kBlockM + r8) >> 2;
-            float4 va[kMaxSplits], vb[kMaxSplits];
-#pragma unroll
-            for (int zz = 0; zz < kMaxSplits; ++zz)
-                if (zz < S) {
-                    va[zz] = peer[zz][off4];
-                    vb[zz] = peer[zz][off4 + 1];
-                }
             float w[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int zb = 0; zb < S; zb += kPeerBatch) {
+                float4 va[kPeerBatch], vb[kPeerBatch];
 #pragma unroll
-            for (int zz = 0; zz < kMaxSplits; ++zz)  // fixed split order: deterministic
-                if (zz < S) {
-                    w[0] += va[zz].x; w[1] += va[zz].y; w[2] += va[zz].z; w[3] += va[zz].w;
-                    w[4] += vb[zz].x; w[5] += vb[zz].y; w[6] += vb[zz].z; w[7] += vb[zz].w;
-                }
+                for (int zz = 0; zz < kPeerBatch; ++zz)
+                    if (zb + zz < S) {
+                        const float4* pr = reinterpret_cast<const float4*>(
+                            cluster.map_shared_rank(P, (int)rank + PAIR * (zb + zz)));
+                        va[zz] = pr[off4];
+                        vb[zz] = pr[off4 + 1];
+                    }
+#pragma unroll
+                for (int zz = 0; zz < kPeerBatch; ++zz)  // fixed split order: deterministic
+                    if (zb + zz < S) {
+                        w[0] += va[zz].x; w[1] += va[zz].y; w[2] += va[zz].z; w[3] += va[zz].w;
+                        w[4] += vb[zz].x; w[5] += vb[zz].y; w[6] += vb[zz].z; w[7] += vb[zz].w;
+                    }
+            }
             epi_vec8(ep, t0 + c, n0 + r8, w);
         }
         cluster.sync();  // peers' smem stays alive until every remote read is done
@@ -763,7 +763,7 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
         bn = std::max(32, (bn + 15) / 16 * 16);
         const int n_wt = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
         const int ctas = 2 * n_wt * ((m_tok + bn - 1) / bn);
-        int splits = std::max(1, std::min({(2 * num_sms()) / ctas, g.kb_total / 4, kMaxSplits / 2}));
+        int splits = std::max(1, std::min({(2 * num_sms()) / ctas, g.kb_total / 4, 4}));
         const int stage_bytes = kABytes + (bn / 2) * kBlockK * 2;
         const int stages = std::max(2, std::min(8, (112 * 1024 - fixed) / stage_bytes));
         if (splits > 1 && stages * stage_bytes >= bn * kBlockM * 4) {
@@ -852,7 +852,7 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     if (tiles < slots) splits = std::max(1, std::min(slots / tiles, g.kb_total / 4));
     // split-K CTAs of a tile form one cluster (portable size <= 8) and park
     // their fp32 partial in the pipeline smem for the DSMEM reduction
-    static const int max_splits = env_knob("TLT_GEMM_MAX_SPLITS", kMaxSplits);
+    static const int max_splits = env_knob("TLT_GEMM_MAX_SPLITS", 8);
     splits = std::min({splits, kMaxSplits, std::max(1, max_splits)});
     if (g.wm != 1 || g.stages * stage_bytes < bn * kBlockM * 4) splits = 1;
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
@@ -876,6 +876,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     if (!attr_set) {
         // 226 KB: leaves room for the kernel's few static shared words
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         attr_set = true;
     }

@@ -1,3 +1,4 @@
 #!/bin/bash
 timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -1
-for v in 0 1; do echo "== wm2 $v"; TLT_GEMM_PAIR_WM2=$v timeout 200 python tools/probe.py 0:384 0:496 0:527 0:768 0:1040 3:496 3:1040; done
+TLT_GEMM_MAX_SPLITS=16 timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -1
+for v in 8 10 12 16; do echo "== max splits $v"; TLT_GEMM_MAX_SPLITS=$v timeout 200 python tools/probe.py 5:1 5:17 5:48 2:1 2:17 2:48 0:1 0:17; done
