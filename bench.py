@@ -271,12 +271,16 @@ def run_ours(a):
     world, rank, local, pg = dist_setup(a.gpus)
     import torch
     torch.cuda.set_device(local)
-    from paper_2511_16665_b200.engine import Engine, Mab
+    from paper_2511_16665_b200.engine import Engine, Mab, merge_bandit_stats
     peak_gbs, peak_tf, peak_kind = peaks()
     n = a.requests
     max_ctx = a.prompt + a.max_len + 8
     eng = Engine(a.model, max_slots=n, max_ctx=max_ctx, device=local)
     mab = Mab(DEFAULT_ARMS, THRESHOLDS, 0.1, 20)
+    # C1: with several ranks each rank's bandit records are all-gathered after
+    # every rollout and merged in rank order into a shared replica (NCCL; the
+    # only collective besides the timing reductions)
+    mab_shared = Mab(DEFAULT_ARMS, THRESHOLDS, 0.1, 20) if pg is not None else None
     V = eng.vocab
 
     def workload(step):
@@ -289,8 +293,11 @@ def run_ours(a):
 
     def rollout(step, enable_sd=True):
         ids, prompts, lens = workload(step)
-        return eng.run_rollout(prompts, lens, ids, enable_sd=enable_sd, elastic_threshold=a.elastic,
-                               mab=mab, seed=step, use_graphs=True)
+        r = eng.run_rollout(prompts, lens, ids, enable_sd=enable_sd, elastic_threshold=a.elastic,
+                            mab=mab, seed=step, use_graphs=True)
+        if mab_shared is not None and enable_sd:
+            r["c1_records"] = merge_bandit_stats(pg, mab, mab_shared)
+        return r
 
     for s in range(a.warmup):
         rollout(s)

@@ -175,6 +175,12 @@ TLT_API int tlt_mab_record(tlt_mab* m, const tlt_strategy* s, double elapsed, co
 TLT_API int tlt_mab_arm_stats(tlt_mab* m, int arm, double* median_reward, int64_t* selections, int32_t* n_rewards);
 /* Multi-GPU merge (C1): apply one foreign rank's record to this replica. */
 TLT_API int tlt_mab_apply_record(tlt_mab* m, int arm, double reward, double a_bar);
+/* C1 (cross-rank bandit statistics): return and clear the records this
+ * replica's beg_record logged since the last call (records applied through
+ * tlt_mab_apply_record are not logged). */
+TLT_API int tlt_mab_take_log(tlt_mab* m, int32_t* arm, double* reward, double* a_bar, int cap, int32_t* n);
+/* Copy the full bandit state (windows, selection counts) of src into dst. */
+TLT_API int tlt_mab_copy(tlt_mab* dst, const tlt_mab* src);
 /* Deterministic streams, reference RngStream (rng.hpp:34-86). */
 TLT_API int tlt_rng_create(uint64_t seed, uint64_t stream_id, tlt_rng** out);
 TLT_API int tlt_rng_fork(const tlt_rng* r, uint64_t label, tlt_rng** out);

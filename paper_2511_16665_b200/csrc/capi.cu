@@ -242,7 +242,30 @@ TLT_API int tlt_mab_apply_record(tlt_mab* m, int arm, double reward, double a_ba
     if (!m) return fail(TLT_ERR_STATE, "null argument");
     return guard([&] {
         if (arm < 0 || arm >= (int)m->m->arms.size()) throw tlt::ConfigErr("arm", "out of range");
-        m->m->push(m->m->arms[arm], reward, a_bar);
+        m->m->push(m->m->arms[arm], reward, a_bar, false);  // merged records are not re-logged
+    });
+}
+
+TLT_API int tlt_mab_take_log(tlt_mab* m, int32_t* arm, double* reward, double* a_bar, int cap, int32_t* n) {
+    if (!m || !n) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        auto& lg = m->m->log;
+        if ((int)lg.size() > cap) throw tlt::ConfigErr("cap", "record log larger than the output arrays");
+        for (size_t i = 0; i < lg.size(); ++i) {
+            arm[i] = lg[i].arm;
+            reward[i] = lg[i].reward;
+            a_bar[i] = lg[i].a_bar;
+        }
+        *n = (int32_t)lg.size();
+        lg.clear();
+    });
+}
+
+TLT_API int tlt_mab_copy(tlt_mab* dst, const tlt_mab* src) {
+    if (!dst || !src) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        *dst->m = *src->m;
+        dst->m->log.clear();
     });
 }
 

@@ -124,7 +124,15 @@ struct Mab {
         }
         throw ConfigErr("strategy", "not a configured strategy");
     }
-    void push(Arm& arm, double reward, double a_bar) {
+    // C1 log: every record pushed by beg_record on this replica since the last
+    // take (arm, reward, a_bar), for the cross-rank merge
+    struct LogRec {
+        int arm;
+        double reward, a_bar;
+    };
+    std::vector<LogRec> log;
+    void push(Arm& arm, double reward, double a_bar, bool logged = true) {
+        if (logged) log.push_back(LogRec{(int)(&arm - arms.data()), reward, a_bar});
         arm.rewards.push_back(reward);
         arm.accept_lens.push_back(a_bar);
         while (arm.rewards.size() > static_cast<size_t>(window)) arm.rewards.pop_front();

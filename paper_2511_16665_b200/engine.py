@@ -361,6 +361,40 @@ class Mab:
     def apply_record(self, arm, reward, a_bar):
         _check(self.L.tlt_mab_apply_record(self.h, arm, C.c_double(reward), C.c_double(a_bar)))
 
+    def take_log(self, cap: int = 1 << 16):
+        """Records this replica's beg_record logged since the last call: [(arm, reward, a_bar)]."""
+        arm = np.zeros(cap, np.int32)
+        rew = np.zeros(cap, np.float64)
+        ab = np.zeros(cap, np.float64)
+        n = C.c_int32()
+        _check(self.L.tlt_mab_take_log(self.h, _p(arm), rew.ctypes.data_as(C.c_void_p),
+                                       ab.ctypes.data_as(C.c_void_p), cap, C.byref(n)))
+        return [(int(arm[i]), float(rew[i]), float(ab[i])) for i in range(n.value)]
+
+    def copy_from(self, other: "Mab"):
+        _check(self.L.tlt_mab_copy(self.h, other.h))
+
+
+def merge_bandit_stats(dist, local: "Mab", shared: "Mab") -> int:
+    """C1: all-gather every rank's new BEG-MAB records and apply
+    them to the shared replica in rank order, so every rank's shared replica is
+    bit-identical; the local replica then restarts from it. With one rank this
+    is exactly the local beg_record sequence. Returns the records merged."""
+    mine = local.take_log()
+    world = dist.get_world_size() if dist is not None else 1
+    logs = [None] * world
+    if dist is not None:
+        dist.all_gather_object(logs, mine)
+    else:
+        logs = [mine]
+    n = 0
+    for recs in logs:  # rank order
+        for arm, reward, a_bar in recs:
+            shared.apply_record(arm, reward, a_bar)
+            n += 1
+    local.copy_from(shared)
+    return n
+
     def __del__(self):
         try:
             self.L.tlt_mab_destroy(self.h)

@@ -55,3 +55,51 @@ def test_gloo_allgather_merge_keeps_replicas_identical(world):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+def _rollout_worker(rank, world, port, q):
+    """bench.py's C1 path: per 'rollout' each rank records into its local
+    replica, then merge_bandit_stats all-gathers the logs and applies them in
+    rank order to the shared replica; shared replicas must be bit-identical
+    and equal to one sequential application of rank 0's then rank 1's records."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_16665_b200.engine import Mab, Rng, merge_bandit_stats
+    local, shared = Mab(ARMS, THR, 0.1, 20), Mab(ARMS, THR, 0.1, 20)
+    rng = Rng(99, 0x53454C + rank)
+    g = random.Random(7 + rank)
+    total = 0
+    all_logs = []
+    for rollout in range(3):
+        mine = []
+        for step in range(10 + rank):  # ranks run different numbers of SD steps
+            batch = g.choice([1, 4, 12, 25])
+            arm, s = local.select(batch, rng)
+            lens = [g.randrange(0, s[0] + 1) for _ in range(batch)]
+            local.record(s, 1.0 + g.random(), lens)
+        total += merge_bandit_stats(dist, local, shared)
+    stats = torch.tensor([v for i in range(len(ARMS)) for v in (shared.arm_stats(i)[0], shared.arm_stats(i)[2])],
+                         dtype=torch.float64)
+    gathered = [torch.zeros_like(stats) for _ in range(world)]
+    dist.all_gather(gathered, stats)
+    local_stats = torch.tensor([v for i in range(len(ARMS)) for v in (local.arm_stats(i)[0], local.arm_stats(i)[2])],
+                               dtype=torch.float64)
+    ok = all(torch.equal(gathered[0], t) for t in gathered) and torch.equal(local_stats, stats)
+    ok = ok and total == 3 * sum(10 + r for r in range(world))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_gloo_rollout_boundary_merge():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + random.randrange(1000, 2000)
+    procs = [ctx.Process(target=_rollout_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
