@@ -1,4 +1,6 @@
 #!/bin/bash
-timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -1
-TLT_GEMM_MAX_SPLITS=16 timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -1
-for v in 8 10 12 16; do echo "== max splits $v"; TLT_GEMM_MAX_SPLITS=$v timeout 200 python tools/probe.py 5:1 5:17 5:48 2:1 2:17 2:48 0:1 0:17; done
+S="1:245 1:527 5:245 5:527 2:527"
+echo "== default"; timeout 200 python tools/probe.py $S
+echo "== pure pair"; TLT_GEMM_PAIR_MIN_CTAS=1 TLT_GEMM_PAIR_SPLIT=0 timeout 200 python tools/probe.py $S
+echo "== pure pair persistent"; TLT_GEMM_PAIR_MIN_CTAS=1 TLT_GEMM_PAIR_SPLIT=0 TLT_GEMM_PAIR_PERSIST_MIN_M=200 timeout 200 python tools/probe.py $S
+echo "== 1cta bn256"; TLT_GEMM_PAIR_MIN_M=100000 TLT_GEMM_BN_MAX=256 timeout 200 python tools/probe.py $S
