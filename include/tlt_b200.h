@@ -79,6 +79,8 @@ typedef struct {
     float lm_alt;      /* relative gain of the second (alternative) successor */
     float lm_noise;    /* unstructured part of the LM head */
     float fc_noise;    /* drafter fc deviation from the embedding passthrough */
+    int32_t drafter_lm_fp8; /* 1: the drafter's LM head runs in e4m3 (per-row scales, kind::f8f6f4);
+                               the target's stays bf16. 0 = bf16 everywhere (struct padding slot) */
 } tlt_init_cfg;
 
 typedef struct tlt_engine tlt_engine;
@@ -278,6 +280,11 @@ TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n,
  * number of chunks per row. */
 TLT_API int tlt_dev_row_topk(const float* logits, int R, int V, int k, float* part, int* out_tok, float* out_logit,
                              float* out_M, float* out_S, int iters, float* avg_ms);
+/* e4m3 GEMM (kind::f8f6f4) through the production path: x [m][k] and w [n][k]
+ * bf16 quantised per row (scale = amax/448), y = (qx qw^T) * sx[t] * sw[n]
+ * fp32; the quantised operands / scales are returned for the reference. */
+TLT_API int tlt_dev_gemm_e4m3(const void* x, int m, int k, const void* w, int n, float* y, void* qx, float* sx,
+                              void* qw, float* sw);
 /* Tree-masked attention over explicit device buffers (q [R][H*hd], K/V
  * caches [slots][KV][cap][hd] bf16, row slots / 1024-bit tail masks, group
  * slot / committed length / tail start / tail length): kernel 0 = mma.sync

@@ -59,7 +59,8 @@ class ModelCfg(C.Structure):
 
 class InitCfg(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("layer_scale", C.c_float), ("lm_gain", C.c_float), ("lm_alt", C.c_float),
-                ("lm_noise", C.c_float), ("fc_noise", C.c_float)]
+                ("lm_noise", C.c_float), ("fc_noise", C.c_float),
+                ("drafter_lm_fp8", C.c_int32)]
 
 
 _orc = None

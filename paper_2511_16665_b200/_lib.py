@@ -48,6 +48,8 @@ def _declare(L: C.CDLL) -> None:
     L.tlt_dev_gemm.restype = C.c_int
     L.tlt_dev_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int]
+    L.tlt_dev_gemm_e4m3.restype = C.c_int
+    L.tlt_dev_gemm_e4m3.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int] + [C.c_void_p] * 5
     L.tlt_dev_attention.restype = C.c_int
     L.tlt_dev_attention.argtypes = [C.c_void_p] * 4 + [C.c_int] * 6 + [C.c_void_p] * 6 + [C.c_int] * 2
     L.tlt_dev_row_topk.restype = C.c_int

@@ -167,3 +167,32 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
         return -1;
     }
 }
+
+// e4m3 GEMM through the production path: x [m][k], w [n][k] bf16 are
+// quantised per row (launch_quant_rows_e4m3), then y = (qx qw^T) * sx * sw
+// (fp32) with the kind::f8f6f4 kernel. Also returns the quantised operands
+// and scales for the reference. Returns the CTA-pair factor used.
+extern "C" TLT_API int tlt_dev_gemm_e4m3(const void* x, int m, int k, const void* w, int n, float* y, void* qx,
+                                         float* sx, void* qw, float* sw) {
+    try {
+        launch_quant_rows_e4m3(static_cast<const __nv_bfloat16*>(x), m, k, k, qx, sx, 0);
+        launch_quant_rows_e4m3(static_cast<const __nv_bfloat16*>(w), n, k, k, qw, sw, 0);
+        GemmPlan g = plan_gemm_e4m3(m, n, k);
+        CUtensorMap tw = make_tmap_e4m3(qw, n, k, k, 128);
+        CUtensorMap tx = make_tmap_e4m3(qx, m, k, k, g.box_rows);
+        EpiParams ep{};
+        ep.kind = EPI_F32;
+        ep.n_out = n;
+        ep.m_tok = m;
+        ep.out_f32 = y;
+        ep.ld_f32 = n;
+        ep.row_scale = sw;
+        ep.tok_scale = sx;
+        launch_gemm(g, tw, tx, ep, nullptr, 0, 0);
+        CUDA_CHECK(cudaDeviceSynchronize());
+        return g.pair;
+    } catch (const std::exception& e) {
+        tlt_set_last_error(e.what());
+        return -1;
+    }
+}

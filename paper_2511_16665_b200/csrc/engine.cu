@@ -113,6 +113,7 @@ Engine::~Engine() {
         if (p) cudaFree(p);
     };
     f(embed_), f(lm_head_), f(final_norm_), f(fc_), f(rope_cos_), f(rope_sin_);
+    f(lm8_), f(lm8_s_), f(h8_), f(h8_s_);
     for (auto& L : layers_) f(L.attn_norm), f(L.qkv), f(L.qkv_b), f(L.o), f(L.mlp_norm), f(L.gu), f(L.down);
     f(drafter_.attn_norm), f(drafter_.qkv), f(drafter_.qkv_b), f(drafter_.o), f(drafter_.mlp_norm), f(drafter_.gu),
         f(drafter_.down);
@@ -139,7 +140,7 @@ Engine::~Engine() {
     cudaStreamDestroy(st_);
 }
 
-void Engine::alloc_weights(const tlt_init_cfg&) {
+void Engine::alloc_weights(const tlt_init_cfg& init) {
     const long long V = cfg.vocab, d = cfg.hidden, F = cfg.ffn;
     const long long nqkv = (long long)(cfg.heads + 2 * cfg.kv_heads) * cfg.head_dim;
     const long long nq = (long long)cfg.heads * cfg.head_dim;
@@ -171,6 +172,13 @@ void Engine::alloc_weights(const tlt_init_cfg&) {
     for (int l = 0; l < cfg.layers; ++l) layers_.push_back(mk_layer(l));
     drafter_ = mk_layer(TLT_DRAFTER_LAYER);
     tm_lm_ = make_tmap_bf16(lm_head_, (int)V, (int)d, d, 128);
+    drafter_fp8_ = init.drafter_lm_fp8 != 0 || env_int("TLT_DRAFTER_FP8", 0) != 0;
+    if (drafter_fp8_) {  // e4m3 copy of the LM head for the drafter, one scale per vocab row
+        lm8_ = dmalloc<uint8_t>((size_t)V * d);
+        lm8_s_ = dmalloc<float>((size_t)V);
+        launch_quant_rows_e4m3(lm_head_, (int)V, (int)d, d, lm8_, lm8_s_, st_);
+        tm_lm8_ = make_tmap_e4m3(lm8_, (int)V, (int)d, d, 128);
+    }
     tm_fc_ = make_tmap_bf16(fc_, (int)d, (int)(2 * d), 2 * d, 128);
     // RoPE table, computed in double exactly as the oracle does, stored fp32
     cap_ = cfg.max_ctx + kMaxT + 2;
@@ -457,10 +465,55 @@ void Engine::lm_head(const float* x, int n, float* logits, bool h_ready) {
 // Final norm + LM head with the fused top-k epilogue (EPI_TOPK) and the
 // per-row merge: writes tk_tok_/tk_logit_ [n][k], tk_M_, tk_S_. The fp32
 // logits are only materialized for the parity exports (want_logits).
-void Engine::lm_topk(const float* x, int n, int k, const int* live, bool want_logits, bool h_ready) {
+// Drafter LM head over h_ (normalised rows) -> logits_ [n][V] fp32: bf16
+// tcgen05 GEMM, or e4m3 (kind::f8f6f4) with per-token / per-vocab-row scales
+// when the drafter runs its LM head in FP8.
+void Engine::drafter_logits(int n) {
+    EpiParams f{};
+    f.kind = EPI_F32;
+    f.out_f32 = logits_;
+    f.ld_f32 = cfg.vocab;
+    if (!drafter_fp8_) {
+        gemm(h_, n, cfg.hidden, cfg.hidden, tm_lm_, cfg.vocab, f);
+        return;
+    }
+    const int d = cfg.hidden;
+    if (!h8_) {
+        h8_ = dmalloc<uint8_t>((size_t)std::max(R_, Rmeta_) * d);
+        h8_s_ = dmalloc<float>((size_t)std::max(R_, Rmeta_));
+    }
+    launch_quant_rows_e4m3(h_, n, d, d, h8_, h8_s_, st_);
+    count_launch();
+    GemmPlan g = plan_gemm_e4m3(n, cfg.vocab, d);
+    char key[96];
+    std::snprintf(key, sizeof key, "e4m3/%p/%d/%d", (void*)h8_, n, g.box_rows);
+    auto it = tmaps_.find(key);
+    if (it == tmaps_.end()) it = tmaps_.emplace(key, make_tmap_e4m3(h8_, n, d, d, g.box_rows)).first;
+    f.n_out = cfg.vocab;
+    f.m_tok = n;
+    f.row_scale = lm8_s_;
+    f.tok_scale = h8_s_;
+    launch_gemm(g, tm_lm8_, it->second, f, ws_, ws_elems_, st_);
+    count_launch();
+}
+
+void Engine::drafter_lm_head(const float* x, int n) {
+    launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
+    count_launch();
+    drafter_logits(n);
+}
+
+void Engine::lm_topk(const float* x, int n, int k, const int* live, bool want_logits, bool h_ready, bool drafter) {
     if (!h_ready) {
         launch_rmsnorm(x, n, cfg.hidden, final_norm_, cfg.rms_eps, h_, st_);
         count_launch();
+    }
+    if (drafter && drafter_fp8_) {
+        drafter_logits(n);
+        const int nch = launch_row_topk_chunked(logits_, n, cfg.vocab, live, k, topk_part_, st_);
+        launch_topk_merge(topk_part_, nch, n, k, live, tk_tok_, tk_logit_, tk_M_, tk_S_, st_);
+        count_launch(2);
+        return;
     }
     static const int fused_k = [] {
         const char* v = std::getenv("TLT_FUSED_TOPK_K");
@@ -533,9 +586,9 @@ void Engine::drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, i
         if (gather) {
             launch_gather_rows(x_, gather, n_lm, d, xg_, st_);
             count_launch();
-            lm_topk(xg_, n_lm, k, live, want_logits, false);
+            lm_topk(xg_, n_lm, k, live, want_logits, false, true);
         } else {
-            lm_topk(x_, n_lm, k, live, want_logits, true);
+            lm_topk(x_, n_lm, k, live, want_logits, true, true);
         }
     }
 }
@@ -770,6 +823,11 @@ float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* fl
                     N = cfg.vocab;
                     K = d;
                     break;
+                case 6:  // the drafter's LM head as configured (bf16 or e4m3 incl. activation quantisation)
+                    drafter_logits(M);
+                    N = cfg.vocab;
+                    K = d;
+                    break;
                 default:
                     ep.kind = EPI_TOPK;
                     ep.out_f32 = topk_part_;
@@ -786,7 +844,7 @@ float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* fl
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
     const double out_b = kind == 0 ? (double)M * N / 2 * 2 : kind == 1 ? (double)M * N * 2
-                         : (kind == 2 || kind == 5) ? (double)M * N * 8 : kind == 3 ? (double)M * N * 4 : (double)M * 16;
+                         : (kind == 2 || kind == 5) ? (double)M * N * 8 : kind == 6 ? (double)M * N * 4 : kind == 3 ? (double)M * N * 4 : (double)M * 16;
     if (bytes) *bytes = (double)N * K * 2 + (double)M * K * 2 + out_b;
     if (flops) *flops = 2.0 * M * N * K;
     return ms / iters;

@@ -96,7 +96,14 @@ private:
                         float* logits, bf16* feat);
     void drafter_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
                          const int* gather, int n_lm, int k, const int* live, bool want_logits, bf16* dfeat_out);
-    void lm_topk(const float* x, int n, int k, const int* live, bool want_logits, bool h_ready = false);
+    void lm_topk(const float* x, int n, int k, const int* live, bool want_logits, bool h_ready = false,
+                 bool drafter = false);
+    void drafter_logits(int n);  // h_ -> logits_ through the drafter's LM head (bf16 or e4m3)
+    void drafter_lm_head(const float* x, int n);  // final norm + drafter_logits
+    bool drafter_fp8_ = false;
+    uint8_t *lm8_ = nullptr, *h8_ = nullptr;
+    float *lm8_s_ = nullptr, *h8_s_ = nullptr;
+    CUtensorMap tm_lm8_;
     float* topk_part_ = nullptr;  // EPI_TOPK partials [vocab tiles][R][2 + 2k]
     void scatter_features(const Rows& rw, int R, const bf16* feat);
     void catchup_drafter(int b, const int32_t* slots);

@@ -28,6 +28,9 @@ void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc = 
 // test hooks: the mma.sync kernels + combine, and the combine alone
 void launch_attention_legacy(const AttnParams& p, cudaStream_t st);
 void launch_attn_combine_only(const AttnParams& p, cudaStream_t st);
+// e4m3 quantisation, one fp32 scale per row (q: [rows][cols] bytes)
+void launch_quant_rows_e4m3(const __nv_bfloat16* x, int rows, int cols, long long ld, void* q, float* scale,
+                            cudaStream_t st);
 bool attention_tc_eligible(const AttnParams& p);
 bool attention_tc_shape_ok(const AttnParams& p);
 void launch_attention_tc(const AttnParams& p, cudaStream_t st);

@@ -81,9 +81,9 @@ void Engine::stoch_device_sequence(int b_hi, int D, double temperature, bool dbg
         if (lv == 1) {
             launch_gather_rows(x_, root_row_, b_hi, d, xg_, st_);
             count_launch();
-            lm_head(xg_, b_hi, logits_, false);
+            drafter_lm_head(xg_, b_hi);
         } else {
-            lm_head(x_, b_hi, logits_, false);
+            drafter_lm_head(x_, b_hi);
         }
         launch_chain_sample(logits_, b_hi, V, lv == 1 ? dg_[1].slot : rw.slot, qrows_, lv, kMaxDepth, d_uni_, US,
                             tk_tok_, tk_logit_, tk_M_, tk_S_, st_);

@@ -164,7 +164,7 @@ __device__ __forceinline__ void epi_tile_staged(const EpiParams& ep, uint32_t ac
 // issues the MMAs, each CTA's TMEM holds the accumulators of its 128 rows for
 // all bn tokens. Per SM this halves the token-operand smem traffic and the
 // L2->SMEM re-reads of the activations (the tensor-bound regime, M >~ 256).
-template <int PAIR>
+template <int PAIR, int FP8 = 0>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_swapab(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                   int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, int wm, int l2pf,
@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* tfull = empty + stages;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
 
+    constexpr int kKel = FP8 ? 2 * kBlockK : kBlockK;  // elements per 128-byte k-block row
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // pair: rank = position in the CTA pair (cluster x); with split-K the
@@ -239,9 +240,9 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 0 && lane == 0) {
         // weight tiles beyond the smem ring: L2 prefetch l2pf k-blocks ahead
         for (int i = npre; i < min(nkb, npre + l2pf); ++i)
-            for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, (kb0 + i) * kBlockK, n0 + a * kBlockM);
+            for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, (kb0 + i) * kKel, n0 + a * kBlockM);
         for (int i = 0; i < npre; ++i) {
-            const int kc = (kb0 + i) * kBlockK;
+            const int kc = (kb0 + i) * kKel;
             if (PAIR == 2) {
                 if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * (a_bytes + b_bytes));
                 for (int a = 0; a < wm; ++a)
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % stages;
                 const uint32_t ph = (i / stages) & 1;
-                const int kc = (kb0 + i) * kBlockK;
+                const int kc = (kb0 + i) * kKel;
                 if (i < npre) {  // weight tile already in flight: activations only
                     if (PAIR == 2)
                         tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows, pol_x);
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(192, 1)
                     continue;
                 }
                 if (i + l2pf < nkb)
-                    for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, kc + l2pf * kBlockK, n0 + a * kBlockM);
+                    for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, kc + l2pf * kKel, n0 + a * kBlockM);
                 mbar_wait(&empty[s], ph ^ 1);
                 if (PAIR == 2) {
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(192, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer (single elected thread; pair: leader CTA only)
         if (PAIR == 1 || rank == 0) {
-            const uint32_t idesc = idesc_bf16_f32(kBlockM * PAIR, bn);
+            const uint32_t idesc = FP8 ? idesc_e4m3_f32(kBlockM * PAIR, bn) : idesc_bf16_f32(kBlockM * PAIR, bn);
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % stages;
                 const uint32_t ph = (i / stages) & 1;
@@ -304,10 +305,16 @@ __global__ void __launch_bounds__(192, 1)
                         for (int kk = 0; kk < kBlockK / 16; ++kk) {
                             // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
                             if (ep.dbg & 1) continue;  // diagnostics: loads only
-                            if (PAIR == 2)
+                            if (FP8) {
+                                if (PAIR == 2)
+                                    tc_mma_e4m3_pair(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                                else
+                                    tc_mma_e4m3(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                            } else if (PAIR == 2) {
                                 tc_mma_bf16_pair(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
-                            else
+                            } else {
                                 tc_mma_bf16(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                            }
                         }
                     }
                     if (PAIR == 2) {
@@ -697,6 +704,20 @@ CUtensorMap make_tmap_bf16(const void* base, int rows, int cols, long long row_s
     return m;
 }
 
+// 2D e4m3 (one-byte) K-major map: box = box_rows x 128 elements (128 bytes).
+CUtensorMap make_tmap_e4m3(const void* base, int rows, int cols, long long row_stride_elems, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_elems)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(2 * kBlockK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (e4m3) failed: " + std::to_string(r));
+    return m;
+}
+
 static int g_num_sms = 0;
 int num_sms() {
     if (!g_num_sms) {
@@ -868,6 +889,26 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     return g;
 }
 
+GemmPlan plan_gemm_e4m3(int m_tok, int n_out, int k) {
+    // one-byte operands: a k-block (128 bytes) holds 128 elements, i.e. the
+    // bf16 planner with k/2; single split (the large-N LM head fills the SMs)
+    GemmPlan g = plan_gemm(m_tok, n_out, (k + 1) / 2);
+    if (g.persist || g.splits != 1 || g.wm != 1) {
+        const int fixed = 1024 + 256;
+        const int stage_bytes = kABytes + g.box_rows * kBlockK * 2;
+        g.persist = 0;
+        g.wm = 1;
+        g.splits = 1;
+        g.kb_per_split = g.kb_total;
+        g.stages = std::max(2, std::min(8, ((g.pair == 2 || g.bn <= 128 ? 112 : 220) * 1024 - fixed) / stage_bytes));
+        g.smem = g.stages * stage_bytes + fixed;
+        const int cols = g.bn;
+        g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256;
+    }
+    g.fp8 = 1;
+    return g;
+}
+
 void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep,
                  float* workspace, size_t workspace_elems, cudaStream_t st) {
     (void)workspace;
@@ -878,6 +919,8 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         attr_set = true;
     }
     if (ep.kind == EPI_TOPK && g.splits > 1) throw CudaError("EPI_TOPK needs whole-K accumulators");
@@ -947,7 +990,10 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     ++na;
     cfg.attrs = at;
     cfg.numAttrs = na;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, g.pair == 2 ? k_gemm_swapab<2> : k_gemm_swapab<1>, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
+    auto kern = g.fp8 ? (g.pair == 2 ? k_gemm_swapab<2, 1> : k_gemm_swapab<1, 1>)
+                      : (g.pair == 2 ? k_gemm_swapab<2, 0> : k_gemm_swapab<1, 0>);
+    if (g.fp8 && (g.persist || g.splits != 1)) throw CudaError("e4m3 GEMM: only the single-split non-persistent plan");
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
                                        g.tmem_cols, g.wm, g.l2pf, epd);
     if (e != cudaSuccess) throw CudaError(std::string("gemm launch: ") + cudaGetErrorString(e));
 }

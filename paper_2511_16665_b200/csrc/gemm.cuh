@@ -59,6 +59,9 @@ struct EpiParams {
     __nv_bfloat16* norm_out;
     float norm_eps;
     int* norm_counter;
+    // e4m3 GEMM dequantisation: acc * row_scale[n] * tok_scale[t] (null: none)
+    const float* row_scale;
+    const float* tok_scale;
 };
 constexpr int kEpiTopkMax = 8;
 
@@ -68,6 +71,10 @@ __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)
 __device__ __forceinline__ void epi_pair(const EpiParams& p, int t, int n, float v0, float v1, int split) {
     if (t >= p.m_tok || n >= p.n_out) return;
     const bool has1 = (n + 1) < p.n_out;
+    if (p.row_scale && split >= 0) {
+        v0 *= p.row_scale[n] * p.tok_scale[t];
+        if (has1) v1 *= p.row_scale[n + 1] * p.tok_scale[t];
+    }
     switch (p.kind) {
         case EPI_F32: {
             float* o = p.out_f32 + (long long)t * p.ld_f32 + n;
@@ -126,11 +133,19 @@ __device__ __forceinline__ void epi_pair(const EpiParams& p, int t, int n, float
 // of token t, v[] = fp32 accumulators (rows interleaved exactly as the weight
 // rows). Rows >= n_out are dropped. One 16-byte (bf16) or 2x16-byte (fp32)
 // store per call where the layout allows it.
-__device__ __forceinline__ void epi_vec8(const EpiParams& p, int t, int n, const float (&v)[8]) {
+__device__ __forceinline__ void epi_vec8(const EpiParams& p, int t, int n, const float (&vin)[8]) {
     if (t >= p.m_tok || n >= p.n_out) return;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = vin[i];
+    if (p.row_scale) {
+        const float ts = p.tok_scale[t];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] *= p.row_scale[min(n + i, p.n_out - 1)] * ts;
+    }
     if (n + 8 > p.n_out) {  // ragged tail: scalar pairs
 #pragma unroll
-        for (int i = 0; i < 8; i += 2) epi_pair(p, t, n + i, v[i], v[i + 1], 0);
+        for (int i = 0; i < 8; i += 2) epi_pair(p, t, n + i, v[i], v[i + 1], -1);  // already scaled
         return;
     }
     switch (p.kind) {
@@ -207,7 +222,7 @@ __device__ __forceinline__ void epi_vec8(const EpiParams& p, int t, int n, const
         } break;
         default: {
 #pragma unroll
-            for (int i = 0; i < 8; i += 2) epi_pair(p, t, n + i, v[i], v[i + 1], 0);
+            for (int i = 0; i < 8; i += 2) epi_pair(p, t, n + i, v[i], v[i + 1], -1);  // already scaled
         } break;
     }
 }

@@ -3,6 +3,7 @@
 // row top-k / argmax, drafter tree select (K6), greedy accept (K7), KV
 // compaction + commit (K8), row-metadata builders. The GEMMs are in gemm.cu.
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <math_constants.h>
@@ -1312,4 +1313,31 @@ void launch_commit_ar(const StepIn* st, int b, const int* argmax, const bf16* fe
     if (b > 0) launch_pdl(k_commit_ar, b, 256, 0, s, st, b, argmax, feat, d, tok_hist, feat_hist, cap, out_tok);
 }
 
+}  // namespace tlt
+
+namespace tlt {
+// e4m3 quantisation with one fp32 scale per row (weights: per output
+// feature; activations: per token): scale = amax / 448 (1 for an all-zero
+// row), q = e4m3(x / scale), round-to-nearest-even, saturating. One warp per
+// row; the oracle (orc_neural.c) applies the identical arithmetic.
+__global__ void k_quant_rows_e4m3(const bf16* __restrict__ x, int rows, int cols, long long ld,
+                                  __nv_fp8_storage_t* __restrict__ q, float* __restrict__ scale) {
+    pdl_wait();
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= rows) return;
+    const bf16* xr = x + (long long)warp * ld;
+    float amax = 0.f;
+    for (int c = lane; c < cols; c += 32) amax = fmaxf(amax, fabsf(__bfloat162float(xr[c])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float s = amax > 0.f ? __fdiv_rn(amax, 448.0f) : 1.0f;  // IEEE division (the oracle computes the same)
+    __nv_fp8_storage_t* qr = q + (long long)warp * cols;
+    for (int c = lane; c < cols; c += 32)
+        qr[c] = __nv_cvt_float_to_fp8(__fdiv_rn(__bfloat162float(xr[c]), s), __NV_SATFINITE, __NV_E4M3);
+    if (lane == 0) scale[warp] = s;
+}
+void launch_quant_rows_e4m3(const bf16* x, int rows, int cols, long long ld, void* q, float* scale, cudaStream_t st) {
+    const int blocks = (rows * 32 + 255) / 256;
+    launch_pdl(k_quant_rows_e4m3, blocks, 256, 0, st, x, rows, cols, ld, static_cast<__nv_fp8_storage_t*>(q), scale);
+}
 }  // namespace tlt

@@ -42,11 +42,14 @@ struct GemmPlan {
     int box_rows = 16; // token rows per TMA box of the activation tensor map (bn / pair)
     int l2pf = 0;      // weight k-blocks prefetched into L2 ahead of the smem ring
     int persist = 0;   // 1: persistent kernel (double-buffered TMEM accumulators)
+    int fp8 = 0;       // 1: e4m3 operands (kind::f8f6f4), per-row / per-token scales in the epilogue
 };
 
 int num_sms();
 CUtensorMap make_tmap_bf16(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
 GemmPlan plan_gemm(int m_tok, int n_out, int k);
+GemmPlan plan_gemm_e4m3(int m_tok, int n_out, int k);
+CUtensorMap make_tmap_e4m3(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
 int* gemm_norm_counter();
 void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& tmX, const EpiParams& ep,
                  float* workspace, size_t workspace_elems, cudaStream_t st);

@@ -61,7 +61,7 @@ class ModelCfg(C.Structure):
 
 class InitCfg(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("layer_scale", C.c_float), ("lm_gain", C.c_float), ("lm_alt", C.c_float), ("lm_noise", C.c_float),
-                ("fc_noise", C.c_float)]
+                ("fc_noise", C.c_float), ("drafter_lm_fp8", C.c_int32)]
 
 
 class TreeOut(C.Structure):
@@ -138,7 +138,8 @@ class Engine:
         self.init = ini
         self.cfg = ModelCfg(m["vocab"], m["hidden"], m["layers"], m["heads"], m["kv_heads"], m["head_dim"], m["ffn"],
                             m["qkv_bias"], m["rope_theta"], m["rms_eps"], max_slots, max_ctx)
-        self.icfg = InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"], ini["fc_noise"])
+        self.icfg = InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"], ini["fc_noise"],
+                            int(ini.get("drafter_lm_fp8", 0)))
         self.L = lib()
         h = C.c_void_p()
         _check(self.L.tlt_engine_create(C.byref(self.cfg), C.byref(self.icfg), device, C.byref(h)))
