@@ -376,6 +376,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 tlt_strategy s = cfg->fixed_strategy;
                 if (cfg->use_mab) s = mab->m->arms[mab->m->select(batch, select_rng)].strategy;
                 const int D = s.draft_depth;
+                if (trace) std::fprintf(stderr, "[tlt] sd_begin b=%d (%d,%d,%d)\n", batch, D, s.top_k, s.tokens_to_verify);
                 acc_len.assign(batch, 0);
                 bonus.assign(batch, 0);
                 accepted.assign((size_t)batch * D, 0);

@@ -709,32 +709,69 @@ void Engine::release(int slot) {
 // Drafter catch-up (after plain-decode steps): committed positions [ld, lt)
 // with target features, chunked. The SD graph then sees exactly 1 + accepted
 // pending rows per request.
-void Engine::catchup_drafter(int b, const int32_t* slots) {
-    const int chunk = 256;
+float Engine::catchup_drafter(int b, const int32_t* slots) {
+    // Batched like prefill: several requests per drafter forward, each with a
+    // static stride of `chunk` rows; committed prefix [0, ld) + causal block.
+    // Returns the device time (CUDA events), counted in the step's elapsed.
+    std::vector<int> pend(b), from(b);
+    int longest = 1;
     for (int i = 0; i < b; ++i) {
-        const int s = slots[i];
-        while (lt_[s] - ld_[s] > 0) {
-            const int n = std::min(chunk, lt_[s] - ld_[s]);
-            const int c0 = ld_[s];
-            std::vector<int> tok(chunk, 0), pos(chunk, 0), slot(chunk, -1), cidx(chunk, 0), fk(chunk, 0);
-            std::vector<long long> fidx(chunk, 0);
-            std::vector<uint32_t> mask((size_t)chunk * kMaskWords, 0u);
-            std::vector<int32_t> htok(n);
-            CUDA_CHECK(cudaMemcpy(htok.data(), tok_hist_ + (size_t)s * cap_ + c0, sizeof(int32_t) * n,
-                                  cudaMemcpyDeviceToHost));
-            for (int j = 0; j < n; ++j) {
-                tok[j] = htok[j];
-                pos[j] = cidx[j] = c0 + j;
-                slot[j] = s;
-                fk[j] = c0 + j > 0 ? 1 : 0;
-                fidx[j] = (long long)s * cap_ + c0 + j - 1;
-                for (int t = 0; t <= j; ++t) mask[(size_t)j * kMaskWords + (t >> 5)] |= 1u << (t & 31);
+        from[i] = ld_[slots[i]];
+        pend[i] = lt_[slots[i]] - ld_[slots[i]];
+        longest = std::max(longest, pend[i]);
+    }
+    const int chunk = std::max(16, std::min({512, std::max(1, R_ / 2), (longest + 15) / 16 * 16}));
+    // all pending tokens in one D2H pass
+    std::vector<std::vector<int32_t>> htok(b);
+    for (int i = 0; i < b; ++i) {
+        htok[i].resize(std::max(1, pend[i]));
+        if (pend[i] > 0)
+            CUDA_CHECK(cudaMemcpyAsync(htok[i].data(), tok_hist_ + (size_t)slots[i] * cap_ + from[i],
+                                       sizeof(int32_t) * pend[i], cudaMemcpyDeviceToHost, st_));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    CUDA_CHECK(cudaEventRecord(ev0_, st_));
+    const int per_fwd = std::max(1, R_ / chunk);
+    for (int i0 = 0; i0 < b; i0 += per_fwd) {
+        const int nreq = std::min(per_fwd, b - i0);
+        int rows_max = 0;
+        for (int q = 0; q < nreq; ++q) rows_max = std::max(rows_max, pend[i0 + q]);
+        for (int c0 = 0; c0 < rows_max; c0 += chunk) {
+            const int R = nreq * chunk;
+            std::vector<int> tok(R, 0), pos(R, 0), slot(R, -1), cidx(R, 0), fk(R, 0), gs(nreq, -1), glc(nreq, 0),
+                gt0(nreq, 0), gnt(nreq, 0);
+            std::vector<long long> fidx(R, 0);
+            std::vector<uint32_t> mask((size_t)R * kMaskWords, 0u);
+            int max_keys = 1;
+            for (int q = 0; q < nreq; ++q) {
+                const int i = i0 + q, s = slots[i];
+                const int cn = std::max(0, std::min(chunk, pend[i] - c0));
+                const int base = from[i] + c0;
+                gs[q] = cn > 0 ? s : -1;
+                glc[q] = base;
+                gt0[q] = base;
+                gnt[q] = cn;
+                max_keys = std::max(max_keys, base + chunk);
+                for (int j = 0; j < cn; ++j) {
+                    const int r = q * chunk + j, p = base + j;
+                    tok[r] = htok[i][c0 + j];
+                    pos[r] = cidx[r] = p;
+                    slot[r] = s;
+                    fk[r] = p > 0 ? 1 : 0;
+                    fidx[r] = (long long)s * cap_ + p - 1;
+                    for (int t = 0; t <= j; ++t) mask[(size_t)r * kMaskWords + (t >> 5)] |= 1u << (t & 31);
+                }
             }
-            upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, {s}, {c0}, {c0}, {n});
-            drafter_forward(prows_, pg_, chunk, chunk, 1, c0 + chunk, nullptr, 0, 0, nullptr, false, nullptr);
-            ld_[s] += n;
+            upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, gs, glc, gt0, gnt);
+            drafter_forward(prows_, pg_, R, chunk, nreq, max_keys, nullptr, 0, 0, nullptr, false, nullptr);
         }
     }
+    CUDA_CHECK(cudaEventRecord(ev1_, st_));
+    CUDA_CHECK(cudaEventSynchronize(ev1_));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    for (int i = 0; i < b; ++i) ld_[slots[i]] += pend[i];
+    return ms;
 }
 
 int Engine::bucket_hi_for(int b, int T) const {
@@ -1087,11 +1124,13 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
         if (lt_[sl] + T + 2 > cap_ - 1 || lt_[sl] + 1 + (D - 1) * T + 2 > dcap_) throw ConfigErr("max_ctx", "context full");
     }
     // drafter catch-up for requests whose pending rows exceed the graph stride
+    // (after plain-decode steps); its device time is part of the step's
+    float catchup_ms = 0.f;
     {
         std::vector<int32_t> need;
         for (int i = 0; i < b; ++i)
             if (lt_[slots[i]] - ld_[slots[i]] + 1 > D + 1) need.push_back(slots[i]);
-        if (!need.empty()) catchup_drafter((int)need.size(), need.data());
+        if (!need.empty()) catchup_ms = catchup_drafter((int)need.size(), need.data());
     }
     const int b_hi = bucket_hi_for(b, T);
     for (int i = 0; i < b_hi; ++i) {
@@ -1121,6 +1160,7 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
     CUDA_CHECK(cudaEventSynchronize(ev1_));
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    ms += catchup_ms;
     // capture for the next replay (after a successful eager run)
     if (use_graphs && !dbg && it == graphs_.end()) {
         cudaGraph_t g;

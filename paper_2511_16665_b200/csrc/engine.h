@@ -106,7 +106,7 @@ private:
     CUtensorMap tm_lm8_;
     float* topk_part_ = nullptr;  // EPI_TOPK partials [vocab tiles][R][2 + 2k]
     void scatter_features(const Rows& rw, int R, const bf16* feat);
-    void catchup_drafter(int b, const int32_t* slots);
+    float catchup_drafter(int b, const int32_t* slots);
     void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real);
     void ar_device_sequence(int b_hi);
     void stoch_device_sequence(int b_hi, int D, double temperature, bool dbg, int b_real);

@@ -265,11 +265,12 @@ float Engine::sd_step_stochastic(int D, float temperature, int b, const int32_t*
     }
     const int US = 2 * kMaxDepth + 1;
     ensure_stoch_buffers();
+    float catchup_ms = 0.f;  // drafter catch-up after plain decode: part of the step's device time
     {
         std::vector<int32_t> need;
         for (int i = 0; i < b; ++i)
             if (lt_[slots[i]] - ld_[slots[i]] + 1 > D + 1) need.push_back(slots[i]);
-        if (!need.empty()) catchup_drafter((int)need.size(), need.data());
+        if (!need.empty()) catchup_ms = catchup_drafter((int)need.size(), need.data());
     }
     const int b_hi = b;
     for (int i = 0; i < b_hi; ++i) {
@@ -292,6 +293,7 @@ float Engine::sd_step_stochastic(int D, float temperature, int b, const int32_t*
     CUDA_CHECK(cudaEventSynchronize(ev1_));
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    ms += catchup_ms;
     if (use_graphs && !dbg && it == graphs_.end()) {
         cudaGraph_t g;
         launches_in_seq_ = 0;

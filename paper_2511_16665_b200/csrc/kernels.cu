@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(kTreeThreads) k_tree_level(TreeParams p) {
     for (int t = threadIdx.x; t < n_kept; t += blockDim.x) sc[t] = arena[kept[t]];
     for (int t = threadIdx.x; t < n_new; t += blockDim.x) sc[n_kept + t] = arena[count0 + t];
     int n_pad = 1;
-    while (n_pad < n_new) n_pad <<= 1;
+    while (n_pad < n_new && n_pad < (1 << 20)) n_pad <<= 1;
     for (int t = threadIdx.x; t < n_pad; t += blockDim.x) sidx[t] = t < n_new ? n_kept + t : -1;
     __syncthreads();
     if (n_new > 1) bitonic_rank_sort(sidx, n_pad, sc);
@@ -1081,7 +1081,7 @@ __global__ void __launch_bounds__(kTreeThreads) k_tree_level(TreeParams p) {
     if (active) {
         const int n_all = n_kept + n_new;
         int m_pad = 1;
-        while (m_pad < n_all) m_pad <<= 1;
+        while (m_pad < n_all && m_pad < (1 << 20)) m_pad <<= 1;
         // reuse sidx: kept then new (unsorted is fine: full sort)
         __syncthreads();
         for (int t = threadIdx.x; t < m_pad; t += blockDim.x) sidx[t] = t < n_all ? t : -1;
@@ -1144,7 +1144,9 @@ __global__ void k_tree_final(TreeParams p) {
                 const int nd = t - 1;
                 p.vrows.tok[r] = p.tree_tok[(long long)i * T + nd];
                 p.vrows.pos[r] = lt + p.tree_dep[(long long)i * T + nd];
-                for (int a = nd; a >= 0; a = s_par[a]) mk[(a + 1) >> 5] |= 1u << ((a + 1) & 31);
+                // bounded walk (a tree path has <= D nodes): malformed input cannot spin
+                for (int a = nd, g = 0; a >= 0 && a < T && g <= kMaxDepth; a = s_par[a], ++g)
+                    mk[(a + 1) >> 5] |= 1u << ((a + 1) & 31);
             }
             p.vrows.slot[r] = slot;
             p.vrows.cidx[r] = lt + t;
@@ -1199,7 +1201,10 @@ __global__ void k_accept_greedy(AcceptParams p) {
     const int* par = p.tree_par + (long long)i * T;
     int node = -1, a = 0;
     int want;
-    for (;;) {
+    // the accepted path is a root-to-leaf chain of the tree: at most D nodes
+    // (children always follow their parent in rank order, so `found` strictly
+    // increases); the bound also makes a malformed tree unable to spin
+    for (int depth = 0;; ++depth) {
         const int vrow = i * T1 + (node < 0 ? 0 : node + 1);
         want = p.argmax[vrow];
         int found = -1;
@@ -1209,7 +1214,7 @@ __global__ void k_accept_greedy(AcceptParams p) {
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
             if (bal) found = c0 + __ffs(bal) - 1;
         }
-        if (found < 0) break;
+        if (found < 0 || found <= node || depth >= p.maxD) break;
         if (lane == 0) {
             p.acc_nodes[(long long)i * p.maxD + a] = found;
             p.acc_tok[(long long)i * p.maxD + a] = want;
