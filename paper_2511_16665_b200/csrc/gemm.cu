@@ -952,7 +952,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         pc.stream = st;
         cudaLaunchAttribute pa[2];
         int npa = 0;
-        if (pdl_enabled()) {
+        if (pdl_enabled(1)) {
             pa[npa].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             pa[npa].val.programmaticStreamSerializationAllowed = 1;
             ++npa;
@@ -976,7 +976,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     int na = 0;
-    if (pdl_enabled()) {
+    if (pdl_enabled(1)) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;

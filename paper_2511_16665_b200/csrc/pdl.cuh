@@ -1,9 +1,9 @@
-// Programmatic dependent launch (PDL): every engine kernel is launched with
-// programmatic stream serialization, calls griddepcontrol.launch_dependents
+// Programmatic dependent launch (PDL): when enabled every engine kernel is
+// launched with programmatic stream serialization, calls griddepcontrol.launch_dependents
 // early and griddepcontrol.wait before touching its inputs, so the next
 // kernel's CTAs are scheduled and run their prologue (barrier init, TMEM
 // alloc, descriptor prefetch) while this kernel drains. Inside CUDA graphs the
-// edges become programmatic. TLT_PDL=0 disables it.
+// edges become programmatic.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -19,13 +19,24 @@ __device__ __forceinline__ void pdl_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-inline bool pdl_enabled() {
-    static int on = [] {
+// TLT_PDL: 0 = plain stream serialization (default), 1 = every engine
+// kernel, "gemm" = tcgen05 GEMM launches only, "other" = all but them.
+// Default off: with PDL on every kernel the 7B rollout bench wedged in
+// 3 of 26 runs on B200 (an SD step's first, eager, run of a new graph key;
+// no mbarrier watchdog fired), 0 of 18 with it off and 0 of 12 in each
+// single-class mode (tools/gpu_hang3.sh); the overlap is worth 1-3%.
+inline int pdl_mask() {
+    static int m = [] {
         const char* v = std::getenv("TLT_PDL");
-        return v ? std::atoi(v) : 1;
+        if (!v) return 0;
+        const std::string s(v);
+        if (s == "gemm") return 1;
+        if (s == "other") return 2;
+        return std::atoi(v) ? 3 : 0;
     }();
-    return on != 0;
+    return m;
 }
+inline bool pdl_enabled(int bit = 2) { return (pdl_mask() & bit) != 0; }
 
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
