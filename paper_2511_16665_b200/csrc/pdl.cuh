@@ -19,16 +19,17 @@ __device__ __forceinline__ void pdl_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-// TLT_PDL: 0 = plain stream serialization (default), 1 = every engine
-// kernel, "gemm" = tcgen05 GEMM launches only, "other" = all but them.
-// Default off: with PDL on every kernel the 7B rollout bench wedged in
-// 3 of 26 runs on B200 (an SD step's first, eager, run of a new graph key;
-// no mbarrier watchdog fired), 0 of 18 with it off and 0 of 12 in each
-// single-class mode (tools/gpu_hang3.sh); the overlap is worth 1-3%.
+// TLT_PDL: "gemm" = tcgen05 GEMM launches only (default), 1 = every engine
+// kernel, 0 = plain stream serialization, "other" = all but the GEMMs.
+// Not every kernel by default: with PDL on all of them the 7B rollout bench
+// wedged in 3 of 26 runs on B200 (an SD step's first, eager, run of a new
+// graph key; no mbarrier watchdog fired); 0 of 40 runs with GEMM-only PDL,
+// 0 of 18 with it off, 0 of 12 with "other" (tools/gpu_hang*.sh). GEMM-only
+// keeps most of the overlap (+1.6% rollout throughput over off).
 inline int pdl_mask() {
     static int m = [] {
         const char* v = std::getenv("TLT_PDL");
-        if (!v) return 0;
+        if (!v) return 1;
         const std::string s(v);
         if (s == "gemm") return 1;
         if (s == "other") return 2;
