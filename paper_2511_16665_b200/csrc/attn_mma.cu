@@ -20,6 +20,7 @@
 #include "engine_kernels.h"
 #include "kernels.cuh"
 #include "pdl.cuh"
+#include "ptx.cuh"
 
 namespace tlt {
 
@@ -114,6 +115,7 @@ __device__ __forceinline__ void attn_fused_combine(const AttnParams& p, int grp,
 template <int kHD>
 __global__ void __launch_bounds__(128) k_attention_mma(AttnParams p) {
     pdl_wait();
+    l2_prefetch_slice(p.pf, p.pf_bytes);
     constexpr int kStride = kHD + 8;  // padded smem row (elements): conflict-free fragments
     constexpr int KS = kHD / 16;      // k-steps over head_dim
     constexpr int NT = kHD / 8;       // n-tiles of the output
@@ -357,6 +359,7 @@ __global__ void __launch_bounds__(QV * 2, QV == 64 ? 2 : 1) k_attention_tree(Att
     constexpr int kTRows = kTQV / 2 + 2;  // >= distinct rows covered by QV qv (G >= 2)
     constexpr int kThreads = QV * 2;
     pdl_wait();
+    l2_prefetch_slice(p.pf, p.pf_bytes);
     constexpr int kStride = kHD + 8;
     constexpr int KS = kHD / 16;
     constexpr int NT = kHD / 8;
@@ -620,6 +623,7 @@ __device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2
 template <int kHD>
 __global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
     pdl_wait();
+    l2_prefetch_slice(p.pf, p.pf_bytes);
     constexpr int kStride = kHD + 8;
     constexpr int KS = kHD / 16;
     constexpr int NT = kHD / 8;

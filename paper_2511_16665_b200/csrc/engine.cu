@@ -363,8 +363,10 @@ void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const C
 }
 
 void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int rpr,
-                       int ngroups, int max_keys) {
+                       int ngroups, int max_keys, const void* pf, long long pf_bytes) {
     AttnParams p{};
+    p.pf = pf;
+    p.pf_bytes = pf_bytes;
     p.q = q_;
     p.out = attn_;
     p.kc = kc;
@@ -440,7 +442,14 @@ void Engine::layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, c
     e.n_kv = cfg.kv_heads;
     e.max_ctx = cache_cap;
     gemm(h_, R, d, d, w.tm_qkv, nq + 2 * nkv, e);
-    attention(kc, vc, cache_cap, rw, gp, rpr, ngroups, max_keys);
+    // TLT_L2PF_O=1: the attention kernel warms L2 with W_o (HBM is mostly
+    // idle during the latency-bound attention). Off: measured -0.5% on the
+    // rollout (contends with the KV stream at b >= 32, no gain at small b)
+    static const int l2pf_o = [] {
+        const char* v = std::getenv("TLT_L2PF_O");
+        return v ? std::atoi(v) : 0;
+    }();
+    attention(kc, vc, cache_cap, rw, gp, rpr, ngroups, max_keys, l2pf_o ? w.o : nullptr, (long long)d * nq * 2);
     gemm_resid_norm(attn_, R, nq, nq, w.tm_o, w.mlp_norm);  // x += o W_o^T; h = norm(x)
     EpiParams s{};
     s.kind = EPI_SWIGLU;

@@ -90,7 +90,7 @@ private:
                        int rpr, int ngroups, int max_keys, bool h_ready, const bf16* next_norm);
     void gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w);
     void attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int rpr,
-                   int ngroups, int max_keys);
+                   int ngroups, int max_keys, const void* pf = nullptr, long long pf_bytes = 0);
     void lm_head(const float* x, int n, float* logits, bool h_ready = false);
     void target_forward(const Rows& rw, const Groups& gp, int R, int rpr, int ngroups, int max_keys,
                         float* logits, bf16* feat);

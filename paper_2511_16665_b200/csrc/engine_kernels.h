@@ -23,6 +23,11 @@ struct AttnParams {
     int impl;  // 0: CUDA-core reference kernel, 1: tensor-core flash-decode (attn_mma.cu)
     int* counters;  // non-null: fused split combine (last CTA per tile), zeroed buffer
     int dec;        // 1: decode kernel (<= 16 query vectors per request/head), chunk = multiple of 256
+    // optional L2 warm-up of the NEXT kernel's weights (the o-proj): the
+    // attention kernels are latency-bound and leave HBM idle, so each CTA
+    // issues a bulk L2 prefetch of its slice of [pf, pf + pf_bytes)
+    const void* pf;
+    long long pf_bytes;
 };
 void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc = true);
 // test hooks: the mma.sync kernels + combine, and the combine alone

@@ -66,6 +66,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- TMA
+// Bulk L2 prefetch of a contiguous global range (no smem, no barrier).
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+                 : "memory");
+}
+// Thread 0 of every CTA prefetches its 1/gridsize slice of [base, base+bytes)
+// (bytes a multiple of 16) into L2, in 64 KB requests.
+__device__ __forceinline__ void l2_prefetch_slice(const void* base, long long bytes) {
+    if (!base || bytes <= 0 || threadIdx.x != 0) return;
+    const long long nb = (long long)gridDim.x * gridDim.y * gridDim.z;
+    const long long cta = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+    const long long per = ((bytes + nb - 1) / nb + 15) & ~15LL;
+    const long long lo = cta * per, hi = bytes < lo + per ? bytes : lo + per;
+    for (long long o = lo; o < hi; o += 65536)
+        l2_prefetch_bulk(static_cast<const char*>(base) + o, (uint32_t)(hi - o < 65536 ? hi - o : 65536));
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
