@@ -142,6 +142,14 @@ TLT_API int tlt_sd_step(tlt_engine* e, const tlt_strategy* s, int b, const int32
  * residual/bonus draw); `uniforms` is [b][2*draft_depth+1]. */
 TLT_API int tlt_sd_step_stochastic(tlt_engine* e, int draft_depth, float temperature, int b,
                                    const int32_t* slot_ids, const double* uniforms, tlt_accept_out* out);
+/* Greedy verify of host-proposed linear chains (the model-free n-gram
+ * branch of run_rollout, rollout.hpp:212-216): chain_from_tokens
+ * (spec_decode.hpp:228-240) of chains[i*draft_depth .. +chain_lens[i]]
+ * (0 <= len <= draft_depth; an empty chain is a plain step emitting the
+ * bonus), then the same tree-masked target verify, verify_greedy and KV
+ * compaction as tlt_sd_step. The drafter does not run. */
+TLT_API int tlt_sd_step_chain(tlt_engine* e, int draft_depth, int b, const int32_t* slot_ids, const int32_t* chains,
+                              const int32_t* chain_lens, tlt_accept_out* out);
 /* Plain autoregressive step (the 2x denominator): reference plain branch
  * (rollout.hpp:247-261) / generate_autoregressive (token_model.hpp:190-203). */
 TLT_API int tlt_ar_step(tlt_engine* e, int b, const int32_t* slot_ids, int32_t* out_tokens, float* elapsed_ms);
@@ -189,6 +197,22 @@ TLT_API int tlt_rng_fork(const tlt_rng* r, uint64_t label, tlt_rng** out);
 TLT_API void tlt_rng_destroy(tlt_rng* r);
 TLT_API uint64_t tlt_rng_next_u64(tlt_rng* r);
 TLT_API double tlt_rng_uniform01(tlt_rng* r);
+
+/* Model-free n-gram drafter, reference NgramIndex / ngram_insert /
+ * ngram_draft (ngram.hpp:13-103) and the per-request NgramTracker cursor
+ * (rollout.hpp:103-120). Opaque single-owner state. */
+typedef struct tlt_ngram tlt_ngram;
+TLT_API int tlt_ngram_create(int n, int continuation_len, tlt_ngram** out);
+TLT_API void tlt_ngram_destroy(tlt_ngram* g);
+/* ngram_insert (ngram.hpp:62-78): every n-gram of the response. */
+TLT_API int tlt_ngram_insert(tlt_ngram* g, const int32_t* response, int len, int64_t step_id);
+/* NgramTracker::extend (rollout.hpp:107-118): complete windows of the stream
+ * from the tracker cursor on. */
+TLT_API int tlt_ngram_extend(tlt_ngram* g, const int32_t* stream, int len, int64_t step_id);
+/* ngram_draft (ngram.hpp:83-101): writes up to depth tokens, *out_len = count. */
+TLT_API int tlt_ngram_draft(const tlt_ngram* g, const int32_t* ctx, int len, int depth, int32_t* out, int32_t* out_len);
+/* Number of stored (key, continuation) entries (NgramIndex::size, :34-38). */
+TLT_API int tlt_ngram_size(const tlt_ngram* g, int64_t* size);
 
 /* plan_captures (capture_plan.hpp:87-126) with BucketSpec (:42-45). Writes up
  * to max_entries entries; *n_entries = number produced. vanilla != 0 gives

@@ -383,4 +383,36 @@ int ref_generate_autoregressive(void* model, const int32_t* prompt, int plen, in
     return 0;
 }
 
+// ---- n-gram fallback drafter (ngram.hpp:13-103, NgramTracker rollout.hpp:103-120)
+void* ref_ngram_create(int n, int cont) {
+    try {
+        auto* t = new detail::NgramTracker;
+        t->index = NgramIndex(n, cont);
+        return t;
+    } catch (...) {
+        return nullptr;
+    }
+}
+void ref_ngram_destroy(void* t) { delete static_cast<detail::NgramTracker*>(t); }
+int ref_ngram_insert(void* t, const int32_t* r, int len, long long step) {
+    auto* tr = static_cast<detail::NgramTracker*>(t);
+    tr->index = ngram_insert(tr->index, std::span<const TokenId>(r, static_cast<std::size_t>(len)), step);
+    return 0;
+}
+int ref_ngram_extend(void* t, const int32_t* r, int len, long long step) {
+    static_cast<detail::NgramTracker*>(t)->extend(TokenSeq(r, r + len), step);
+    return 0;
+}
+int ref_ngram_draft(void* t, const int32_t* ctx, int len, int depth, int32_t* out) {
+    try {
+        auto v = ngram_draft(static_cast<detail::NgramTracker*>(t)->index,
+                             std::span<const TokenId>(ctx, static_cast<std::size_t>(len)), depth);
+        std::copy(v.begin(), v.end(), out);
+        return static_cast<int>(v.size());
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+long long ref_ngram_size(void* t) { return (long long)static_cast<detail::NgramTracker*>(t)->index.size(); }
+
 }  // extern "C"

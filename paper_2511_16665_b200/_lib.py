@@ -42,6 +42,8 @@ def _declare(L: C.CDLL) -> None:
     L.tlt_rng_destroy.argtypes = [C.c_void_p]
     L.tlt_engine_destroy.argtypes = [C.c_void_p]
     L.tlt_mab_destroy.argtypes = [C.c_void_p]
+    L.tlt_ngram_destroy.argtypes = [C.c_void_p]
+    L.tlt_ngram_draft.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     L.tlt_dev_time_gemm.restype = C.c_int
     L.tlt_dev_time_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_longlong, C.c_int, C.c_void_p]

@@ -878,9 +878,9 @@ int attention_dec_chunk(int n_groups, int kv, int max_keys) {
         return v ? std::atoi(v) : 296;
     }();
     const int chunks = std::max(1, (max_keys + kSplit - 1) / kSplit);
-    // >= one CTA per SM already: a single split (the kernel then writes the
-    // normalised output itself, no partials, no combine launch)
-    const int want_splits = n_groups * kv >= 148 ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
+    // (request, head) pairs alone reach the CTA target: a single split (the
+    // kernel then writes the normalised output itself, no partials, no combine)
+    const int want_splits = n_groups * kv >= target_ctas ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
     const int per = std::max(1, (chunks + want_splits - 1) / want_splits);
     return per * kSplit;
 }

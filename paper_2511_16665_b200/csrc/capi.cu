@@ -23,6 +23,9 @@ struct tlt_mab {
 struct tlt_rng {
     tlt::Rng r;
 };
+struct tlt_ngram {
+    tlt::Ngram g;
+};
 
 namespace {
 int fail(int code, const char* msg) {
@@ -86,6 +89,40 @@ TLT_API int tlt_sd_step(tlt_engine* e, const tlt_strategy* s, int b, const int32
                         tlt_accept_out* out) {
     if (!e || !s || !slot_ids) return fail(TLT_ERR_STATE, "null argument");
     return guard([&] { e->e->sd_step(*s, b, slot_ids, tree, out); });
+}
+
+TLT_API int tlt_sd_step_chain(tlt_engine* e, int draft_depth, int b, const int32_t* slot_ids, const int32_t* chains,
+                              const int32_t* chain_lens, tlt_accept_out* out) {
+    if (!e || !slot_ids || !chains || !chain_lens) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { e->e->sd_step_chain(draft_depth, b, slot_ids, chains, chain_lens, out); });
+}
+
+TLT_API int tlt_ngram_create(int n, int continuation_len, tlt_ngram** out) {
+    if (!out) return fail(TLT_ERR_CONFIG, "null argument");
+    return guard([&] { *out = new tlt_ngram{tlt::Ngram(n, continuation_len)}; });
+}
+TLT_API void tlt_ngram_destroy(tlt_ngram* g) { delete g; }
+TLT_API int tlt_ngram_insert(tlt_ngram* g, const int32_t* response, int len, int64_t step_id) {
+    if (!g || (len > 0 && !response) || len < 0) return fail(TLT_ERR_CONFIG, "bad argument");
+    return guard([&] { g->g.insert(response, (size_t)len, step_id); });
+}
+TLT_API int tlt_ngram_extend(tlt_ngram* g, const int32_t* stream, int len, int64_t step_id) {
+    if (!g || (len > 0 && !stream) || len < 0) return fail(TLT_ERR_CONFIG, "bad argument");
+    return guard([&] { g->g.extend(stream, (size_t)len, step_id); });
+}
+TLT_API int tlt_ngram_draft(const tlt_ngram* g, const int32_t* ctx, int len, int depth, int32_t* out,
+                            int32_t* out_len) {
+    if (!g || !out || !out_len || (len > 0 && !ctx) || len < 0) return fail(TLT_ERR_CONFIG, "bad argument");
+    return guard([&] {
+        auto v = g->g.draft(ctx, (size_t)len, depth);
+        std::copy(v.begin(), v.end(), out);
+        *out_len = (int32_t)v.size();
+    });
+}
+TLT_API int tlt_ngram_size(const tlt_ngram* g, int64_t* size) {
+    if (!g || !size) return fail(TLT_ERR_CONFIG, "null argument");
+    *size = (int64_t)g->g.size();
+    return 0;
 }
 
 TLT_API int tlt_sd_step_stochastic(tlt_engine* e, int draft_depth, float temperature, int b, const int32_t* slot_ids,

@@ -1041,7 +1041,14 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
     }
     launch_tree_final(tp, st_);
     count_launch();
-    // target verify over root + tree
+    verify_accept_commit(b_hi, T, dbg, b_real);
+}
+
+// Target verify over root + the final tree (rows written by k_tree_final),
+// argmax, verify_greedy, KV compaction, results into pinned host memory.
+void Engine::verify_accept_commit(int b_hi, int T, bool dbg, int b_real) {
+    const int d = cfg.hidden, V = cfg.vocab;
+    const int max_keys_t = cap_;
     const int T1 = T + 1, RV = b_hi * T1;
     target_forward(vrows_, vg_, RV, T1, b_hi, max_keys_t, nullptr, feat_);
     lm_topk(x_, RV, 1, vrows_.slot, dbg, true);  // argmax per verify row (fused epilogue + merge)
@@ -1216,6 +1223,106 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
         }
         ld_[sl] = lt_[sl] + 1;
         lt_[sl] = lt_[sl] + 1 + a;
+    }
+    if (out && out->elapsed_ms) out->elapsed_ms[0] = ms;
+    return ms;
+}
+
+// n-gram fallback branch of run_rollout (rollout.hpp:212-216): the host
+// proposes a linear chain per request (chain_from_tokens, spec_decode.hpp:
+// 228-240: parent i-1, depth i+1, prob = path_prob = 1); it is written into
+// the tree arena as the kept list, and k_tree_final + the common verify tail
+// do the rest. Eager (chains are data-dependent host input; one H2D of
+// b*D candidates per step).
+float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* chains, const int32_t* lens,
+                            tlt_accept_out* out) {
+    if (D < 1 || D > kMaxD - 1 || D > kMaxT) throw ConfigErr("draft_depth", "out of range (1..15)");
+    if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");
+    for (int i = 0; i < b; ++i) {
+        const int sl = slots[i];
+        if (sl < 0 || sl >= cfg.max_slots || !live_[sl]) throw ConfigErr("slot_ids", "slot not prefilled");
+        if (lens[i] < 0 || lens[i] > D) throw ConfigErr("chain_lens", "must be in [0, draft_depth]");
+        if (lt_[sl] + D + 2 > cap_ - 1) throw ConfigErr("max_ctx", "context full");
+        for (int j = 0; j < lens[i]; ++j)
+            if (chains[(size_t)i * D + j] < 0 || chains[(size_t)i * D + j] >= cfg.vocab)
+                throw ConfigErr("chains", "token out of range");
+    }
+    const int b_hi = b, T = D;
+    for (int i = 0; i < b_hi; ++i) h_step_[i] = StepIn{slots[i], lt_[slots[i]], ld_[slots[i]], 0};
+    std::vector<Cand> cand((size_t)b_hi * D);
+    std::vector<int> kept((size_t)b_hi * D), kept_n(b_hi);
+    for (int i = 0; i < b_hi; ++i) {
+        kept_n[i] = lens[i];
+        for (int j = 0; j < D; ++j) {
+            Cand c{};
+            c.pp = 1.0;
+            c.prob = 1.0;
+            c.token = j < lens[i] ? chains[(size_t)i * D + j] : 0;
+            c.parent = j - 1;
+            c.depth = j + 1;
+            c.birth = j;
+            c.row = -1;
+            c.eslot = -1;
+            cand[(size_t)i * D + j] = c;
+            kept[(size_t)i * D + j] = j;
+        }
+    }
+    CUDA_CHECK(cudaEventRecord(ev0_, st_));
+    launches_in_seq_ = 0;
+    CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpy2DAsync(arena_, sizeof(Cand) * arena_cap_, cand.data(), sizeof(Cand) * D, sizeof(Cand) * D,
+                                 b_hi, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(kept_, kept.data(), sizeof(int) * kept.size(), cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(kept_n_, kept_n.data(), sizeof(int) * b_hi, cudaMemcpyHostToDevice, st_));
+    TreeParams tp{};
+    tp.step = d_step_;
+    tp.b = b_hi;
+    tp.b_hi = b_hi;
+    tp.D = D;
+    tp.k = 1;
+    tp.T = T;
+    tp.arena = arena_;
+    tp.arena_cap = arena_cap_;
+    tp.arena_n = arena_n_;
+    tp.kept = kept_;
+    tp.kept_n = kept_n_;
+    tp.exp_n = exp_n_;
+    tp.done = done_;
+    tp.row_node = row_node_;
+    tp.root_row = root_row_;
+    tp.rows = drows_;
+    tp.tree_tok = tree_tok_;
+    tp.tree_par = tree_par_;
+    tp.tree_dep = tree_dep_;
+    tp.tree_prob = tree_prob_;
+    tp.tree_pp = tree_pp_;
+    tp.tree_n = tree_n_;
+    tp.vrows = vrows_;
+    tp.vg = vg_;
+    tp.tok_hist = tok_hist_;
+    tp.cap = cap_;
+    launch_tree_final(tp, st_);
+    count_launch();
+    verify_accept_commit(b_hi, T, false, b);
+    launches += launches_in_seq_;
+    CUDA_CHECK(cudaEventRecord(ev1_, st_));
+    CUDA_CHECK(cudaEventSynchronize(ev1_));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    for (int i = 0; i < b; ++i) {
+        const int sl = slots[i];
+        const int a = ho_.acc_len[i];
+        if (out) {
+            if (out->accept_len) out->accept_len[i] = a;
+            if (out->bonus) out->bonus[i] = ho_.bonus[i];
+            for (int j = 0; j < a; ++j) {
+                if (out->accepted) out->accepted[(size_t)i * D + j] = ho_.acc_tok[(size_t)i * kMaxD + j];
+                if (out->nodes) out->nodes[(size_t)i * D + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
+                if (out->kv_src) out->kv_src[(size_t)i * D + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
+            }
+            if (out->kv_len) out->kv_len[i] = lt_[sl] + 1 + a;
+        }
+        lt_[sl] = lt_[sl] + 1 + a;  // the drafter did not run: ld_ stays (catch-up on the next EAGLE step)
     }
     if (out && out->elapsed_ms) out->elapsed_ms[0] = ms;
     return ms;

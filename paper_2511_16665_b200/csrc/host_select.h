@@ -219,4 +219,76 @@ inline std::vector<tlt_capture_entry> plan_captures(const std::vector<tlt_strate
     return out;
 }
 
+// Model-free n-gram fallback drafter (reference ngram.hpp:13-103 and the
+// per-request NgramTracker, rollout.hpp:103-120). Keys are the last n tokens;
+// each key holds its distinct continuations in first-seen order with a
+// frequency and the latest step id. draft() picks (frequency desc, step id
+// desc, continuation lexicographically asc) and truncates to depth; the chain
+// it returns is verified on the GPU (Engine::sd_step_chain).
+struct Ngram {
+    struct Entry {
+        std::vector<int32_t> cont;
+        uint64_t freq = 0;
+        int64_t last_step = 0;
+    };
+    int n = 2, cont_len = 8;
+    size_t next_key_start = 0;  // tracker cursor over the request stream
+    std::map<std::vector<int32_t>, std::vector<Entry>> entries;
+
+    Ngram(int n_, int cont_len_) : n(n_), cont_len(cont_len_) {
+        if (n < 1) throw ConfigErr("n", "must be >= 1");
+        if (cont_len < 1) throw ConfigErr("continuation_len", "must be >= 1");
+    }
+    size_t size() const {
+        size_t t = 0;
+        for (auto& kv : entries) t += kv.second.size();
+        return t;
+    }
+    // ngram.hpp:40-51
+    void record(std::vector<int32_t> key, std::vector<int32_t> cont, int64_t step) {
+        auto& list = entries[std::move(key)];
+        for (auto& e : list)
+            if (e.cont == cont) {
+                e.freq += 1;
+                e.last_step = std::max(e.last_step, step);
+                return;
+            }
+        list.push_back(Entry{std::move(cont), 1, step});
+    }
+    // ngram_insert, ngram.hpp:62-78 (every n-gram of the response, truncated continuation)
+    void insert(const int32_t* r, size_t len, int64_t step) {
+        const size_t nn = (size_t)n;
+        if (len < nn + 1) return;
+        for (size_t s = 0; s + nn < len; ++s) {
+            const size_t ce = std::min(len, s + nn + (size_t)cont_len);
+            record(std::vector<int32_t>(r + s, r + s + nn), std::vector<int32_t>(r + s + nn, r + ce), step);
+        }
+    }
+    // NgramTracker::extend, rollout.hpp:107-118 (only complete windows)
+    void extend(const int32_t* stream, size_t len, int64_t step) {
+        const size_t nn = (size_t)n, c = (size_t)cont_len;
+        while (next_key_start + nn + c <= len) {
+            const int32_t* k = stream + next_key_start;
+            record(std::vector<int32_t>(k, k + nn), std::vector<int32_t>(k + nn, k + nn + c), step);
+            ++next_key_start;
+        }
+    }
+    // ngram_draft, ngram.hpp:83-101
+    std::vector<int32_t> draft(const int32_t* ctx, size_t len, int depth) const {
+        if (depth < 1) throw ConfigErr("depth", "must be >= 1");
+        const size_t nn = (size_t)n;
+        if (len < nn) return {};
+        auto it = entries.find(std::vector<int32_t>(ctx + len - nn, ctx + len));
+        if (it == entries.end()) return {};
+        const Entry* best = nullptr;
+        for (auto& e : it->second)
+            if (!best || e.freq > best->freq || (e.freq == best->freq && e.last_step > best->last_step) ||
+                (e.freq == best->freq && e.last_step == best->last_step && e.cont < best->cont))
+                best = &e;
+        std::vector<int32_t> out = best->cont;
+        if (out.size() > (size_t)depth) out.resize((size_t)depth);
+        return out;
+    }
+};
+
 }  // namespace tlt

@@ -254,6 +254,31 @@ class Engine:
                          [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
         return res, chains, consumed
 
+    def sd_step_chain(self, draft_depth, slots, chains):
+        """Greedy verify of host-proposed linear chains (n-gram fallback branch,
+        rollout.hpp:212-216; chain_from_tokens, spec_decode.hpp:228-240).
+        chains[i]: list of <= draft_depth tokens (may be empty)."""
+        slots = np.asarray(slots, np.int32)
+        b, D = len(slots), draft_depth
+        ch = np.zeros((b, D), np.int32)
+        lens = np.zeros(b, np.int32)
+        for i, c in enumerate(chains):
+            if len(c) > D:
+                raise ConfigError("chain_lens: must be in [0, draft_depth]")
+            ch[i, :len(c)] = c
+            lens[i] = len(c)
+        acc = np.zeros((b, D), np.int32)
+        nodes = np.zeros((b, D), np.int32)
+        alen = np.zeros(b, np.int32)
+        bonus = np.zeros(b, np.int32)
+        kvl = np.zeros(b, np.int32)
+        ms = np.zeros(1, np.float32)
+        ao = AcceptOut(acc.ctypes.data, nodes.ctypes.data, alen.ctypes.data, bonus.ctypes.data, None,
+                       kvl.ctypes.data, ms.ctypes.data)
+        _check(self.L.tlt_sd_step_chain(self.h, D, b, _p(slots), _p(ch), _p(lens), C.byref(ao)))
+        return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
+                          [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
+
     def debug_target_rows(self, i: int, max_rows: int = 32):
         out = np.zeros((max_rows, self.vocab), np.float64)
         n = C.c_int32()
@@ -328,6 +353,44 @@ class Rng:
     def __del__(self):
         try:
             self.L.tlt_rng_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Ngram:
+    """Model-free n-gram drafter index (reference NgramIndex / ngram_insert /
+    ngram_draft, ngram.hpp:13-103, plus the NgramTracker cursor,
+    rollout.hpp:103-120), host C++ behind the C-ABI."""
+
+    def __init__(self, n=2, continuation_len=8):
+        self.L = lib()
+        self.h = C.c_void_p()
+        _check(self.L.tlt_ngram_create(n, continuation_len, C.byref(self.h)))
+        self.n, self.continuation_len = n, continuation_len
+
+    def insert(self, response, step_id=0):
+        r = np.asarray(response, np.int32)
+        _check(self.L.tlt_ngram_insert(self.h, _p(r), len(r), C.c_int64(step_id)))
+
+    def extend(self, stream, step_id=0):
+        r = np.asarray(stream, np.int32)
+        _check(self.L.tlt_ngram_extend(self.h, _p(r), len(r), C.c_int64(step_id)))
+
+    def draft(self, ctx, depth):
+        c = np.asarray(ctx, np.int32)
+        out = np.zeros(max(depth, 1), np.int32)
+        n = C.c_int32()
+        _check(self.L.tlt_ngram_draft(self.h, _p(c), len(c), depth, _p(out), C.byref(n)))
+        return out[:n.value].tolist()
+
+    def size(self):
+        v = C.c_int64()
+        _check(self.L.tlt_ngram_size(self.h, C.byref(v)))
+        return v.value
+
+    def __del__(self):
+        try:
+            self.L.tlt_ngram_destroy(self.h)
         except Exception:
             pass
 

@@ -1,0 +1,161 @@
+"""Model-free n-gram fallback drafter.
+
+Host index (tlt_ngram_*, csrc/host_select.h `Ngram`) pinned bit-for-bit
+against the UNMODIFIED reference NgramIndex / ngram_insert / ngram_draft
+(ngram.hpp:13-103) and NgramTracker::extend (rollout.hpp:103-120) through
+oracle/_ref; the GPU chain verify (tlt_sd_step_chain) is checked against the
+same engine's greedy plain decode, which greedy SD must reproduce token for
+token (spec_decode.hpp:348-351 "token-identical to greedy autoregressive").
+"""
+import ctypes as C
+import random
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2511_16665_b200.engine import ConfigError, Engine, Ngram
+
+
+def _ref_lib():
+    R = O.ref()
+    R.ref_ngram_create.restype = C.c_void_p
+    R.ref_ngram_destroy.argtypes = [C.c_void_p]
+    R.ref_ngram_insert.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_longlong]
+    R.ref_ngram_extend.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_longlong]
+    R.ref_ngram_draft.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    R.ref_ngram_size.argtypes = [C.c_void_p]
+    R.ref_ngram_size.restype = C.c_longlong
+    return R
+
+
+def _a(x):
+    return np.ascontiguousarray(np.asarray(x, np.int32))
+
+
+def _ref_draft(R, h, ctx, depth):
+    c = _a(ctx)
+    out = np.zeros(max(depth, 1) + 64, np.int32)
+    n = R.ref_ngram_draft(h, c.ctypes.data, len(c), depth, out.ctypes.data)
+    return n, out[:max(n, 0)].tolist()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference bridge not built")
+@pytest.mark.parametrize("seed,n,cont,vocab", [(0, 1, 1, 3), (1, 2, 8, 5), (2, 3, 4, 4), (3, 2, 3, 50)])
+def test_ngram_index_matches_reference(seed, n, cont, vocab):
+    """Random insert/extend/draft sequences over a small vocabulary (many
+    frequency and recency ties), every draft compared with the reference."""
+    R = _ref_lib()
+    rnd = random.Random(seed)
+    h = R.ref_ngram_create(n, cont)
+    g = Ngram(n, cont)
+    stream = []
+    try:
+        for step in range(60):
+            op = rnd.random()
+            if op < 0.35:
+                resp = [rnd.randrange(vocab) for _ in range(rnd.randrange(0, 20))]
+                R.ref_ngram_insert(h, _a(resp).ctypes.data, len(resp), step)
+                g.insert(resp, step)
+            else:
+                stream += [rnd.randrange(vocab) for _ in range(rnd.randrange(1, 6))]
+                R.ref_ngram_extend(h, _a(stream).ctypes.data, len(stream), step)
+                g.extend(stream, step)
+            assert g.size() == R.ref_ngram_size(h)
+            for _ in range(4):
+                ctx = [rnd.randrange(vocab) for _ in range(rnd.randrange(0, 6))]
+                if rnd.random() < 0.5 and stream:
+                    ctx = stream[-rnd.randrange(1, len(stream) + 1):]
+                depth = rnd.randrange(1, 10)
+                rn, rtok = _ref_draft(R, h, ctx, depth)
+                assert rn >= 0
+                assert g.draft(ctx, depth) == rtok
+    finally:
+        R.ref_ngram_destroy(h)
+
+
+def test_ngram_tiebreaks_and_errors():
+    g = Ngram(2, 3)
+    g.insert([1, 2, 3, 4, 5], step_id=1)  # (1,2)->[3,4,5]
+    g.insert([1, 2, 9, 9], step_id=1)     # (1,2)->[9,9]  same freq, same step, larger
+    assert g.draft([7, 1, 2], 8) == [3, 4, 5]
+    assert g.draft([1, 2], 2) == [3, 4]
+    g.insert([1, 2, 9, 9], step_id=2)     # freq 2 wins
+    assert g.draft([1, 2], 8) == [9, 9]
+    assert g.draft([5], 3) == []          # context shorter than n
+    assert g.draft([4, 4], 3) == []       # unknown key
+    with pytest.raises(ConfigError):
+        g.draft([1, 2], 0)
+    with pytest.raises(ConfigError):
+        Ngram(0, 2)
+    with pytest.raises(ConfigError):
+        Ngram(2, 0)
+
+
+@pytest.mark.gpu
+def test_gpu_chain_verify_matches_greedy_decode():
+    """n-gram chains verified on the GPU emit exactly the greedy plain-decode
+    stream; a chain equal to that stream is accepted in full; a wrong first
+    token accepts nothing and emits the argmax as the bonus; KV lengths track."""
+    V = 4096
+    rng = np.random.default_rng(3)
+    prompts = [rng.integers(2, V, 16).tolist() for _ in range(3)]
+    steps = 24
+    ar = Engine("tiny", max_slots=3, max_ctx=512, device=0)
+    ar.prefill(range(3), prompts)
+    ref = [[] for _ in range(3)]
+    for _ in range(steps * 3):
+        toks, _ = ar.ar_step([0, 1, 2])
+        for i in range(3):
+            ref[i].append(int(toks[i]))
+    ar.close()
+
+    D = 4
+    eng = Engine("tiny", max_slots=3, max_ctx=512, device=0)
+    eng.prefill(range(3), prompts)
+    out = [[] for _ in range(3)]
+    trackers = [Ngram(2, D) for _ in range(3)]
+    perfect = wrong = 0
+    for step in range(steps):
+        chains = []
+        for i in range(3):
+            ctx = prompts[i] + out[i]
+            mode = (step + i) % 3
+            if mode == 0:       # oracle-perfect chain: the next D greedy tokens
+                c = ref[i][len(out[i]):len(out[i]) + D]
+            elif mode == 1:     # wrong first token
+                c = [(ref[i][len(out[i])] + 1) % V, 5, 6][:D]
+            else:               # the reference n-gram drafter over the request stream
+                trackers[i].extend(ctx, step)
+                c = trackers[i].draft(ctx, D)
+            chains.append(c)
+        kv0 = [len(prompts[i]) - 1 + len(out[i]) for i in range(3)]
+        r = eng.sd_step_chain(D, [0, 1, 2], chains)
+        for i in range(3):
+            a = int(r.accept_len[i])
+            emitted = r.accepted[i] + [int(r.bonus[i])]
+            mode = (step + i) % 3
+            if mode == 0 and len(chains[i]) == D:
+                assert a == D
+                perfect += 1
+            if mode == 1:
+                assert a == 0
+                wrong += 1
+            assert r.accepted[i] == chains[i][:a]
+            assert r.nodes[i] == list(range(a))
+            assert int(r.kv_len[i]) == kv0[i] + 1 + a
+            out[i] += emitted
+    for i in range(3):
+        n = min(len(out[i]), len(ref[i]))
+        assert n >= steps
+        assert out[i][:n] == ref[i][:n]
+    assert perfect > 0 and wrong > 0
+    # the EAGLE path still works after chain steps (drafter catch-up)
+    r = eng.sd_step((4, 4, 16), [0, 1, 2])
+    for i in range(3):
+        emitted = r.accepted[i] + [int(r.bonus[i])]
+        pos = len(out[i])
+        assert emitted == ref[i][pos:pos + len(emitted)]
+    with pytest.raises(ConfigError):
+        eng.sd_step_chain(D, [0], [[1, 2, 3, 4, 5]])
+    eng.close()
