@@ -232,6 +232,14 @@ typedef struct {
     int32_t use_mab;           /* 1: BEG-MAB select/record with measured elapsed */
     uint64_t seed;             /* RngStream seed of the rollout (fork labels as rollout.hpp:151,153) */
     int32_t use_graphs;        /* replay the CUDA-graph pool */
+    /* Drafter freshness (rollout.hpp:142-144, 209-216): 0 = the EAGLE snapshot
+     * is fresh (target step - snapshot step <= drafter_staleness_bound); 1 =
+     * stale or absent, SD steps draft with the per-request model-free n-gram
+     * tracker instead (greedy mode). Zero-initialised callers keep EAGLE. */
+    int32_t drafter_stale;
+    int32_t ngram_n;                /* reference default 2 */
+    int32_t ngram_continuation_len; /* reference default 8 */
+    int64_t target_step_id;         /* recency stamp of n-gram records (target.step_id()) */
 } tlt_rollout_cfg;
 
 /* Reference RolloutResult (rollout.hpp:79-97) flattened. generated: [n][max_len]. */

@@ -368,6 +368,16 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         std::vector<tlt::Rng> req_rng;
         for (int i = 0; i < n; ++i) req_rng.push_back(root.fork(0x52515254ULL + (uint64_t)request_ids[i]));
         tlt::Rng select_rng = root.fork(0x53454CULL);
+        const bool via_ngram = cfg->drafter_stale != 0;  // rollout.hpp:209 `via_ngram = !adaptive_fresh`
+        if (via_ngram && stoch) throw tlt::ConfigErr("mode", "n-gram fallback is wired for greedy_tree only");
+        std::vector<tlt::Ngram> trackers;
+        if (via_ngram)
+            for (int i = 0; i < n; ++i) trackers.emplace_back(cfg->ngram_n, cfg->ngram_continuation_len);
+        std::vector<std::vector<int32_t>> ctxs;  // prompt ++ generated, for the trackers
+        if (via_ngram)
+            for (int i = 0, off = 0; i < n; off += prompt_lens[i], ++i)
+                ctxs.emplace_back(prompts + off, prompts + off + prompt_lens[i]);
+        std::vector<int32_t> chains, chain_lens;
         E.prefill(n, slots.data(), prompt_lens, prompts);
         if (std::getenv("TLT_TRACE")) std::fprintf(stderr, "[tlt] prefill_ms %.3f n=%d\n", E.last_prefill_ms, n);
         std::vector<int> running(n, 1), glen(n, 0);
@@ -402,6 +412,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
             auto emit = [&](int i, int32_t t) {
                 out->generated[(size_t)i * max_len_stride + glen[i]] = t;
                 glen[i] += 1;
+                if (via_ngram) ctxs[i].push_back(t);
                 out->emitted_total += 1;
                 if (t == TLT_EOS_TOKEN || glen[i] >= max_lens[i]) {
                     running[i] = 0;
@@ -425,6 +436,18 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                     for (int j = 0; j < batch; ++j) take(act[j], U, ubuf.data() + (size_t)j * U);
                     E.sd_step_stochastic(D, cfg->temperature, batch, act.data(), ubuf.data(), &ao);
                     for (int j = 0; j < batch; ++j) pop(act[j], E.last_consumed[j]);
+                } else if (via_ngram) {
+                    // rollout.hpp:214-216: tracker.extend(ctx), chain_from_tokens(ngram_draft(ctx, D))
+                    chains.assign((size_t)batch * D, 0);
+                    chain_lens.assign(batch, 0);
+                    for (int j = 0; j < batch; ++j) {
+                        const int i = act[j];
+                        trackers[i].extend(ctxs[i].data(), ctxs[i].size(), cfg->target_step_id);
+                        auto c = trackers[i].draft(ctxs[i].data(), ctxs[i].size(), D);
+                        std::copy(c.begin(), c.end(), chains.begin() + (size_t)j * D);
+                        chain_lens[j] = (int32_t)c.size();
+                    }
+                    E.sd_step_chain(D, batch, act.data(), chains.data(), chain_lens.data(), &ao);
                 } else {
                     E.sd_step(s, batch, act.data(), nullptr, &ao);
                 }

@@ -83,7 +83,8 @@ class CaptureEntry(C.Structure):
 class RolloutCfg(C.Structure):
     _fields_ = [("enable_sd", C.c_int32), ("elastic_threshold", C.c_int32), ("mode", C.c_int32),
                 ("temperature", C.c_float), ("fixed_strategy", Strategy), ("use_mab", C.c_int32),
-                ("seed", C.c_uint64), ("use_graphs", C.c_int32)]
+                ("seed", C.c_uint64), ("use_graphs", C.c_int32), ("drafter_stale", C.c_int32),
+                ("ngram_n", C.c_int32), ("ngram_continuation_len", C.c_int32), ("target_step_id", C.c_int64)]
 
 
 class RolloutResult(C.Structure):
@@ -310,7 +311,7 @@ class Engine:
     # ---------------------------------------------------------- rollout
     def run_rollout(self, prompts, max_lens, request_ids=None, *, enable_sd=True, elastic_threshold=32,
                     strategy=(4, 4, 16), mab: "Mab | None" = None, seed=0, use_graphs=True, mode="greedy",
-                    temperature=0.0):
+                    temperature=0.0, drafter_stale=False, ngram_n=2, ngram_continuation_len=8, target_step_id=0):
         n = len(prompts)
         rid = np.asarray(request_ids if request_ids is not None else range(n), np.int32)
         plen = np.asarray([len(p) for p in prompts], np.int32)
@@ -321,7 +322,8 @@ class Engine:
         glen = np.zeros(n, np.int32)
         cfg = RolloutCfg(1 if enable_sd else 0, elastic_threshold, 1 if mode == "stochastic" else 0,
                          float(temperature), Strategy(*strategy),
-                         1 if mab is not None else 0, seed, 1 if use_graphs else 0)
+                         1 if mab is not None else 0, seed, 1 if use_graphs else 0, 1 if drafter_stale else 0,
+                         ngram_n, ngram_continuation_len, target_step_id)
         res = RolloutResult(gen.ctypes.data, glen.ctypes.data)
         _check(self.L.tlt_run_rollout(self.h, C.byref(cfg), mab.h if mab is not None else None, n, _p(rid),
                                       _p(plen), _p(toks), _p(ml), stride, C.byref(res)))

@@ -159,3 +159,34 @@ def test_gpu_chain_verify_matches_greedy_decode():
     with pytest.raises(ConfigError):
         eng.sd_step_chain(D, [0], [[1, 2, 3, 4, 5]])
     eng.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D", [3, 8])
+def test_gpu_rollout_ngram_branch_is_lossless(D):
+    """tlt_run_rollout with a stale drafter (rollout.hpp:142-144) drafts with
+    the per-request n-gram tracker (rollout.hpp:212-216) and must emit the
+    same greedy stream as plain decode; repetitive greedy streams of the
+    random-init model give the tracker real acceptances."""
+    V = 4096
+    rng = np.random.default_rng(11)
+    prompts = [rng.integers(2, V, 12).tolist() for _ in range(4)]
+    max_lens = [96, 64, 80, 48]
+    eng = Engine("tiny", max_slots=4, max_ctx=512, device=0)
+    ng = eng.run_rollout(prompts, max_lens, enable_sd=True, elastic_threshold=64, strategy=(D, 1, D),
+                         drafter_stale=True, ngram_n=2, ngram_continuation_len=8, target_step_id=3)
+    ar = eng.run_rollout(prompts, max_lens, enable_sd=False)
+    eng.close()
+    assert ng["tokens"] == ar["tokens"]
+    assert ng["sd_steps"] > 0 and ng["plain_steps"] == 0
+    assert ng["emitted_total"] == sum(len(t) for t in ar["tokens"])
+    assert ng["accepted_total"] > 0
+    assert ng["sd_steps"] <= ar["plain_steps"]
+    assert ng["verify_events"] >= ng["emitted_total"] - ng["accepted_total"]
+
+
+def test_rollout_cfg_ngram_fields():
+    """The ctypes mirror appends the n-gram fields in the C struct's order."""
+    import paper_2511_16665_b200.engine as E
+    assert [f[0] for f in E.RolloutCfg._fields_][-4:] == ["drafter_stale", "ngram_n", "ngram_continuation_len",
+                                                          "target_step_id"]
