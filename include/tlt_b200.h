@@ -150,6 +150,14 @@ TLT_API int tlt_sd_step_stochastic(tlt_engine* e, int draft_depth, float tempera
  * compaction as tlt_sd_step. The drafter does not run. */
 TLT_API int tlt_sd_step_chain(tlt_engine* e, int draft_depth, int b, const int32_t* slot_ids, const int32_t* chains,
                               const int32_t* chain_lens, tlt_accept_out* out);
+/* Stochastic mode of the same branch: verify_stochastic (spec_decode.hpp:
+ * 275-313) of host chains with an empty draft_dist (q one-hot at the drafted
+ * token), temperature t > 0. uniforms: [b][draft_depth+1] RngStream draws in
+ * consumption order (one per tested node, then one residual/bonus draw);
+ * tlt_debug_chain reports how many each request consumed. */
+TLT_API int tlt_sd_step_chain_stochastic(tlt_engine* e, int draft_depth, float temperature, int b,
+                                         const int32_t* slot_ids, const int32_t* chains, const int32_t* chain_lens,
+                                         const double* uniforms, tlt_accept_out* out);
 /* Plain autoregressive step (the 2x denominator): reference plain branch
  * (rollout.hpp:247-261) / generate_autoregressive (token_model.hpp:190-203). */
 TLT_API int tlt_ar_step(tlt_engine* e, int b, const int32_t* slot_ids, int32_t* out_tokens, float* elapsed_ms);

@@ -97,6 +97,14 @@ TLT_API int tlt_sd_step_chain(tlt_engine* e, int draft_depth, int b, const int32
     return guard([&] { e->e->sd_step_chain(draft_depth, b, slot_ids, chains, chain_lens, out); });
 }
 
+TLT_API int tlt_sd_step_chain_stochastic(tlt_engine* e, int draft_depth, float temperature, int b,
+                                         const int32_t* slot_ids, const int32_t* chains, const int32_t* chain_lens,
+                                         const double* uniforms, tlt_accept_out* out) {
+    if (!e || !slot_ids || !chains || !chain_lens || !uniforms) return fail(TLT_ERR_STATE, "null argument");
+    if (!(temperature > 0.f)) return fail(TLT_ERR_CONFIG, "temperature: stochastic mode requires t > 0");
+    return guard([&] { e->e->sd_step_chain(draft_depth, b, slot_ids, chains, chain_lens, out, temperature, uniforms); });
+}
+
 TLT_API int tlt_ngram_create(int n, int continuation_len, tlt_ngram** out) {
     if (!out) return fail(TLT_ERR_CONFIG, "null argument");
     return guard([&] { *out = new tlt_ngram{tlt::Ngram(n, continuation_len)}; });
@@ -369,7 +377,6 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         for (int i = 0; i < n; ++i) req_rng.push_back(root.fork(0x52515254ULL + (uint64_t)request_ids[i]));
         tlt::Rng select_rng = root.fork(0x53454CULL);
         const bool via_ngram = cfg->drafter_stale != 0;  // rollout.hpp:209 `via_ngram = !adaptive_fresh`
-        if (via_ngram && stoch) throw tlt::ConfigErr("mode", "n-gram fallback is wired for greedy_tree only");
         std::vector<tlt::Ngram> trackers;
         if (via_ngram)
             for (int i = 0; i < n; ++i) trackers.emplace_back(cfg->ngram_n, cfg->ngram_continuation_len);
@@ -430,13 +437,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 accepted.assign((size_t)batch * D, 0);
                 float ms = 0.f;
                 tlt_accept_out ao{accepted.data(), nullptr, acc_len.data(), bonus.data(), nullptr, nullptr, &ms};
-                if (stoch) {
-                    const int U = 2 * D + 1;
-                    ubuf.assign((size_t)batch * U, 0.0);
-                    for (int j = 0; j < batch; ++j) take(act[j], U, ubuf.data() + (size_t)j * U);
-                    E.sd_step_stochastic(D, cfg->temperature, batch, act.data(), ubuf.data(), &ao);
-                    for (int j = 0; j < batch; ++j) pop(act[j], E.last_consumed[j]);
-                } else if (via_ngram) {
+                if (via_ngram) {
                     // rollout.hpp:214-216: tracker.extend(ctx), chain_from_tokens(ngram_draft(ctx, D))
                     chains.assign((size_t)batch * D, 0);
                     chain_lens.assign(batch, 0);
@@ -447,7 +448,21 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                         std::copy(c.begin(), c.end(), chains.begin() + (size_t)j * D);
                         chain_lens[j] = (int32_t)c.size();
                     }
-                    E.sd_step_chain(D, batch, act.data(), chains.data(), chain_lens.data(), &ao);
+                    if (stoch) {
+                        ubuf.assign((size_t)batch * (D + 1), 0.0);
+                        for (int j = 0; j < batch; ++j) take(act[j], D + 1, ubuf.data() + (size_t)j * (D + 1));
+                        E.sd_step_chain(D, batch, act.data(), chains.data(), chain_lens.data(), &ao, cfg->temperature,
+                                        ubuf.data());
+                        for (int j = 0; j < batch; ++j) pop(act[j], E.last_consumed[j]);
+                    } else {
+                        E.sd_step_chain(D, batch, act.data(), chains.data(), chain_lens.data(), &ao);
+                    }
+                } else if (stoch) {
+                    const int U = 2 * D + 1;
+                    ubuf.assign((size_t)batch * U, 0.0);
+                    for (int j = 0; j < batch; ++j) take(act[j], U, ubuf.data() + (size_t)j * U);
+                    E.sd_step_stochastic(D, cfg->temperature, batch, act.data(), ubuf.data(), &ao);
+                    for (int j = 0; j < batch; ++j) pop(act[j], E.last_consumed[j]);
                 } else {
                     E.sd_step(s, batch, act.data(), nullptr, &ao);
                 }

@@ -956,7 +956,6 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
         base[lv] = base[lv - 1] + b_hi * Fd[lv - 1];
     }
     if (D >= 2 && base[D] + b_hi * Fd[D] > Rmeta_) throw ConfigErr("strategy", "draft rows exceed TLT_MAX_DRAFT_ROWS");
-    const int max_keys_t = cap_;
     const int max_keys_d = dcap_;
     launch_rows_level1(d_step_, b_hi, b_hi, D1, drows_, dg_[1], root_row_, tok_hist_, cap_, st_);
     count_launch();
@@ -1235,8 +1234,11 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
 // do the rest. Eager (chains are data-dependent host input; one H2D of
 // b*D candidates per step).
 float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* chains, const int32_t* lens,
-                            tlt_accept_out* out) {
+                            tlt_accept_out* out, float temperature, const double* uniforms) {
     if (D < 1 || D > kMaxD - 1 || D > kMaxT) throw ConfigErr("draft_depth", "out of range (1..15)");
+    const bool stoch = temperature != 0.f;
+    if (stoch && !(temperature > 0.f)) throw ConfigErr("temperature", "must be > 0");
+    if (stoch && !uniforms) throw ConfigErr("uniforms", "required");
     if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");
     for (int i = 0; i < b; ++i) {
         const int sl = slots[i];
@@ -1249,6 +1251,12 @@ float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* c
     }
     const int b_hi = b, T = D;
     for (int i = 0; i < b_hi; ++i) h_step_[i] = StepIn{slots[i], lt_[slots[i]], ld_[slots[i]], 0};
+    const int US = 2 * kMaxDepth + 1;
+    if (stoch) {
+        ensure_stoch_buffers();
+        for (int i = 0; i < b_hi; ++i)
+            for (int j = 0; j < US; ++j) h_uni_[(size_t)i * US + j] = j < D + 1 ? uniforms[(size_t)i * (D + 1) + j] : 2.0;
+    }
     std::vector<Cand> cand((size_t)b_hi * D);
     std::vector<int> kept((size_t)b_hi * D), kept_n(b_hi);
     for (int i = 0; i < b_hi; ++i) {
@@ -1274,6 +1282,8 @@ float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* c
                                  b_hi, cudaMemcpyHostToDevice, st_));
     CUDA_CHECK(cudaMemcpyAsync(kept_, kept.data(), sizeof(int) * kept.size(), cudaMemcpyHostToDevice, st_));
     CUDA_CHECK(cudaMemcpyAsync(kept_n_, kept_n.data(), sizeof(int) * b_hi, cudaMemcpyHostToDevice, st_));
+    if (stoch)
+        CUDA_CHECK(cudaMemcpyAsync(d_uni_, h_uni_, sizeof(double) * b_hi * US, cudaMemcpyHostToDevice, st_));
     TreeParams tp{};
     tp.step = d_step_;
     tp.b = b_hi;
@@ -1303,7 +1313,10 @@ float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* c
     tp.cap = cap_;
     launch_tree_final(tp, st_);
     count_launch();
-    verify_accept_commit(b_hi, T, false, b);
+    if (stoch)
+        stoch_verify_commit(b_hi, D, (double)temperature, debug_, b, nullptr, 0);
+    else
+        verify_accept_commit(b_hi, T, false, b);
     launches += launches_in_seq_;
     CUDA_CHECK(cudaEventRecord(ev1_, st_));
     CUDA_CHECK(cudaEventSynchronize(ev1_));
@@ -1321,6 +1334,12 @@ float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* c
                 if (out->kv_src) out->kv_src[(size_t)i * D + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
             }
             if (out->kv_len) out->kv_len[i] = lt_[sl] + 1 + a;
+        }
+        if (stoch) {
+            last_consumed.resize(b);
+            last_chain.resize(b);
+            last_consumed[i] = h_consumed_[i];
+            last_chain[i].assign(chains + (size_t)i * D, chains + (size_t)i * D + lens[i]);
         }
         lt_[sl] = lt_[sl] + 1 + a;  // the drafter did not run: ld_ stays (catch-up on the next EAGLE step)
     }

@@ -56,8 +56,9 @@ public:
     float sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out);
     float ar_step(int b, const int32_t* slots, int32_t* out_tokens);
     // greedy verify of host-proposed chains (n-gram fallback drafter)
+    // temperature > 0: verify_stochastic with one-hot q and uniforms [b][D+1]
     float sd_step_chain(int D, int b, const int32_t* slots, const int32_t* chains, const int32_t* lens,
-                        tlt_accept_out* out);
+                        tlt_accept_out* out, float temperature = 0.f, const double* uniforms = nullptr);
     // rejection-sampling SD over a drafter-sampled chain (stochastic.cu);
     // uniforms [b][2D+1] in RngStream consumption order
     float sd_step_stochastic(int D, float temperature, int b, const int32_t* slots, const double* uniforms,
@@ -112,6 +113,7 @@ private:
     float catchup_drafter(int b, const int32_t* slots);
     void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real);
     void verify_accept_commit(int b_hi, int T, bool dbg, int b_real);
+    void stoch_verify_commit(int b_hi, int D, double temperature, bool dbg, int b_real, const double* q, int cur0);
     void ar_device_sequence(int b_hi);
     void stoch_device_sequence(int b_hi, int D, double temperature, bool dbg, int b_real);
     void ar_sample_sequence(int b_hi, double temperature);

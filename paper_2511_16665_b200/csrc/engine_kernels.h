@@ -119,7 +119,7 @@ void launch_chain_sample(const float* logits, int R, int V, const int* live, dou
 void launch_accept_stochastic(const StepIn* step, int b, int D, int V, double temperature, const float* vlogits,
                               const double* q, const int* chain, const int* chain_n, const double* uni,
                               int uni_stride, double* pbuf, int* acc_nodes, int* acc_tok, int* acc_len, int* bonus,
-                              int* consumed, int maxD, int chain_stride, cudaStream_t st);
+                              int* consumed, int maxD, int chain_stride, int cur0, cudaStream_t st);
 void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int R, int d, float* x,
                               const __nv_bfloat16* g, float eps, __nv_bfloat16* out, cudaStream_t st);
 void launch_attention(const AttnParams& p, cudaStream_t st);

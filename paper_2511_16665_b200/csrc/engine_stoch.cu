@@ -117,12 +117,21 @@ void Engine::stoch_device_sequence(int b_hi, int D, double temperature, bool dbg
     }
     launch_tree_final(tp, st_);
     count_launch();
+    stoch_verify_commit(b_hi, D, temperature, dbg, b_real, qrows_, D);
+}
+
+// Target verify over root + chain (rows from k_tree_final), verify_stochastic
+// with draft rows q (nullptr = one-hot, host n-gram chains) starting at
+// uniform cur0, KV commit, results into pinned host memory.
+void Engine::stoch_verify_commit(int b_hi, int D, double temperature, bool dbg, int b_real, const double* q,
+                                 int cur0) {
+    const int d = cfg.hidden, V = cfg.vocab, D1 = D + 1, US = 2 * kMaxDepth + 1;
     // target verify over root + chain: full fp32 logits of every row
     const int RV = b_hi * D1;
     target_forward(vrows_, vg_, RV, D1, b_hi, cap_, nullptr, feat_);
     lm_head(x_, RV, logits_, true);
-    launch_accept_stochastic(d_step_, b_hi, D, V, temperature, logits_, qrows_, tree_tok_, tree_n_, d_uni_, US, pbuf_,
-                             acc_nodes_, acc_tok_, acc_len_, bonus_, consumed_, kMaxD, D, st_);
+    launch_accept_stochastic(d_step_, b_hi, D, V, temperature, logits_, q, tree_tok_, tree_n_, d_uni_, US, pbuf_,
+                             acc_nodes_, acc_tok_, acc_len_, bonus_, consumed_, kMaxD, D, cur0, st_);
     count_launch();
     if (dbg) {
         // raw target rows along the chain, computed by the accept kernel's own

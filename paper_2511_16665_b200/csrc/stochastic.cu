@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kST) k_accept_stochastic(const StepIn* __restr
                                                            double* __restrict__ pbuf, int* __restrict__ acc_nodes,
                                                            int* __restrict__ acc_tok, int* __restrict__ acc_len,
                                                            int* __restrict__ bonus, int* __restrict__ consumed,
-                                                           int maxD, int chain_stride) {
+                                                           int maxD, int chain_stride, int cur0) {
     pdl_wait();
     __shared__ float fsh[kST + 2];
     __shared__ double dsh[kST + 1];
@@ -244,7 +244,9 @@ __global__ void __launch_bounds__(kST) k_accept_stochastic(const StepIn* __restr
     if (i >= b || step[i].slot < 0) return;
     const int n = chain_n[i];
     const double* ur = uni + (long long)i * uni_stride;
-    int cur = D;  // chain draws come first (D of them)
+    int cur = cur0;  // sampled chains: the D chain draws come first; n-gram chains draw none
+    // q == nullptr: host-proposed (n-gram) chain, empty draft_dist -> q is
+    // one-hot at the drafted token (spec_decode.hpp:282, 296-298)
     double* p = pbuf + (long long)i * V;
     int a = 0;
     for (int j = 0; j <= n; ++j) {
@@ -257,9 +259,9 @@ __global__ void __launch_bounds__(kST) k_accept_stochastic(const StepIn* __restr
             break;
         }
         const int x = chain[(long long)i * chain_stride + j];
-        const double* qr = q + ((long long)i * kMaxDepth + j) * V;  // layout of k_chain_sample
+        const double* qr = q ? q + ((long long)i * kMaxDepth + j) * V : nullptr;  // layout of k_chain_sample
         if (threadIdx.x == 0) {
-            const double qx = qr[x], px = p[x];
+            const double qx = qr ? qr[x] : 1.0, px = p[x];
             const double ap = qx > 0.0 ? (px / qx < 1.0 ? px / qx : 1.0) : 0.0;
             s_dec = ur[cur] < ap ? 1 : 0;  // spec_decode.hpp:285
         }
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(kST) k_accept_stochastic(const StepIn* __restr
         const int per = (V + kST - 1) / kST;
         const int a0 = threadIdx.x * per, b0 = min(V, a0 + per);
         for (int k = a0; k < b0; ++k) {
-            const double diff = p[k] - qr[k];
+            const double diff = p[k] - (qr ? qr[k] : (k == x ? 1.0 : 0.0));
             const double v = diff > 0.0 ? diff : 0.0;
             p[k] = v;  // tentatively the residual
             s += v;
@@ -306,9 +308,9 @@ __global__ void __launch_bounds__(kST) k_accept_stochastic(const StepIn* __restr
 void launch_accept_stochastic(const StepIn* step, int b, int D, int V, double temperature, const float* vlogits,
                               const double* q, const int* chain, const int* chain_n, const double* uni,
                               int uni_stride, double* pbuf, int* acc_nodes, int* acc_tok, int* acc_len, int* bonus,
-                              int* consumed, int maxD, int chain_stride, cudaStream_t st) {
+                              int* consumed, int maxD, int chain_stride, int cur0, cudaStream_t st) {
     launch_pdl(k_accept_stochastic, b, kST, 0, st, step, b, D, V, temperature, vlogits, q, chain, chain_n, uni,
-               uni_stride, pbuf, acc_nodes, acc_tok, acc_len, bonus, consumed, maxD, chain_stride);
+               uni_stride, pbuf, acc_nodes, acc_tok, acc_len, bonus, consumed, maxD, chain_stride, cur0);
 }
 
 }  // namespace tlt

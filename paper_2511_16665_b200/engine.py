@@ -280,6 +280,37 @@ class Engine:
         return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
                           [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
 
+    def sd_step_chain_stochastic(self, draft_depth, temperature, slots, chains, uniforms):
+        """verify_stochastic of host chains with one-hot q (n-gram branch,
+        stochastic mode). uniforms: [b][D+1]; returns (StepResult, consumed)."""
+        slots = np.asarray(slots, np.int32)
+        b, D = len(slots), draft_depth
+        ch = np.zeros((b, D), np.int32)
+        lens = np.zeros(b, np.int32)
+        for i, c in enumerate(chains):
+            ch[i, :len(c)] = c
+            lens[i] = len(c)
+        uni = np.ascontiguousarray(np.asarray(uniforms, np.float64).reshape(b, D + 1))
+        acc = np.zeros((b, D), np.int32)
+        nodes = np.zeros((b, D), np.int32)
+        alen = np.zeros(b, np.int32)
+        bonus = np.zeros(b, np.int32)
+        kvl = np.zeros(b, np.int32)
+        ms = np.zeros(1, np.float32)
+        ao = AcceptOut(acc.ctypes.data, nodes.ctypes.data, alen.ctypes.data, bonus.ctypes.data, None,
+                       kvl.ctypes.data, ms.ctypes.data)
+        _check(self.L.tlt_sd_step_chain_stochastic(self.h, D, C.c_float(temperature), b, _p(slots), _p(ch), _p(lens),
+                                                   _p(uni), C.byref(ao)))
+        consumed = []
+        for i in range(b):
+            tmp = np.zeros(max(D, 1), np.int32)
+            n, cons = C.c_int32(), C.c_int32()
+            _check(self.L.tlt_debug_chain(self.h, i, _p(tmp), C.byref(n), C.byref(cons)))
+            consumed.append(cons.value)
+        res = StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
+                         [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
+        return res, consumed
+
     def debug_target_rows(self, i: int, max_rows: int = 32):
         out = np.zeros((max_rows, self.vocab), np.float64)
         n = C.c_int32()

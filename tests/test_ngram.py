@@ -190,3 +190,111 @@ def test_rollout_cfg_ngram_fields():
     import paper_2511_16665_b200.engine as E
     assert [f[0] for f in E.RolloutCfg._fields_][-4:] == ["drafter_stale", "ngram_n", "ngram_continuation_len",
                                                           "target_step_id"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D,temperature,scale", [(4, 0.9, 1.0), (6, 0.7, 0.02), (3, 1.0, 0.2)])
+def test_gpu_chain_stochastic_oracle_in_the_loop(D, temperature, scale):
+    """Stochastic n-gram branch: verify_stochastic with empty draft_dist (q
+    one-hot, spec_decode.hpp:282,296-298) on the GPU vs the C restatement
+    (pinned to the reference) fed the GPU's raw target rows and the SAME
+    uniforms. Bars: accept length, accepted tokens, bonus and uniform
+    consumption bit-exact; KV length = root + accepted. `scale` < 1 shrinks
+    the uniforms so drafted tokens are also accepted."""
+    L = O.orc()
+    L.orc_verify_stochastic.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                                        C.c_void_p, C.c_void_p, C.c_void_p]
+    V = 4096
+    eng = Engine("tiny", max_slots=4, max_ctx=512, device=0)
+    eng.set_debug(True)
+    rng = np.random.default_rng(5)
+    prompts = [rng.integers(2, V, 16).tolist() for _ in range(4)]
+    eng.prefill(range(4), prompts)
+    ctxs = [list(p) for p in prompts]
+    trackers = [Ngram(1, D) for _ in range(4)]
+    lens = [eng.slot_len(i) for i in range(4)]
+    accepted_any = 0
+    for step in range(8):
+        # greedy continuation of every context from a twin engine (likely-accepted chains)
+        twin = Engine("tiny", max_slots=4, max_ctx=512, device=0)
+        twin.prefill(range(4), ctxs)
+        greedy = [[] for _ in range(4)]
+        for _ in range(D):
+            toks, _ = twin.ar_step([0, 1, 2, 3])
+            for i in range(4):
+                greedy[i].append(int(toks[i]))
+        twin.close()
+        chains = []
+        for i in range(4):
+            mode = (step + i) % 4
+            if mode == 0:
+                c = []
+            elif mode == 1:
+                c = rng.integers(2, V, D).tolist()
+            elif mode == 3:
+                c = greedy[i]
+            else:
+                trackers[i].extend(ctxs[i], step)
+                c = trackers[i].draft(ctxs[i], D)
+            chains.append(c)
+        uni = np.array([[u * scale for u in _uniforms_o(700 + step, 0x52515254 + i, D + 1)] for i in range(4)])
+        res, consumed = eng.sd_step_chain_stochastic(D, temperature, [0, 1, 2, 3], chains, uni)
+        for i in range(4):
+            n = len(chains[i])
+            rows = eng.debug_target_rows(i, max_rows=D + 1)
+            table = {tuple(chains[i][:j]): rows[j] for j in range(n + 1)}
+
+            def target_cb(user, path, k, out, table=table):
+                row = table.get(tuple(path[j] for j in range(k)))
+                if row is None:
+                    return -1
+                C.memmove(out, row.ctypes.data, V * 8)
+                return 0
+
+            tfn = O.ROW_FN(target_cb)
+            ubuf = (C.c_double * (D + 1))(*uni[i].tolist())
+            us = O.USrc(None, C.cast(ubuf, O.f64p), D + 1, 0)
+            nodes = (O.Node * max(n, 1))()
+            for j, t in enumerate(chains[i]):
+                nodes[j].token, nodes[j].parent, nodes[j].depth = t, j - 1, j + 1
+                nodes[j].prob = nodes[j].path_prob = 1.0
+            acc = O.Accept()
+            assert L.orc_verify_stochastic(C.cast(tfn, C.c_void_p), None, V, temperature, nodes, n, None,
+                                           C.byref(us), C.byref(acc)) == 0
+            a = acc.accept_length
+            assert (a, acc.bonus) == (int(res.accept_len[i]), int(res.bonus[i])), (step, i)
+            assert list(acc.accepted[:a]) == res.accepted[i] == chains[i][:a]
+            assert consumed[i] == us.cursor
+            assert int(res.kv_len[i]) == lens[i] + 1 + a
+            lens[i] = int(res.kv_len[i])
+            ctxs[i] += res.accepted[i] + [int(res.bonus[i])]
+            accepted_any += a
+    if scale < 0.1:
+        assert accepted_any > 0
+    eng.close()
+
+
+def _uniforms_o(seed, stream, n):
+    r = O.Rng(seed, stream)
+    return [r.uniform01() for _ in range(n)]
+
+
+@pytest.mark.gpu
+def test_gpu_rollout_ngram_stochastic_deterministic():
+    """Stochastic rollout through the n-gram branch: seeded, reproducible,
+    terminates at max_len/EOS, all steps SD (batch below the gate)."""
+    V = 4096
+    rng = np.random.default_rng(17)
+    prompts = [rng.integers(2, V, 10).tolist() for _ in range(3)]
+    max_lens = [40, 24, 33]
+    eng = Engine("tiny", max_slots=3, max_ctx=512, device=0)
+    kw = dict(enable_sd=True, elastic_threshold=64, strategy=(4, 1, 4), mode="stochastic", temperature=0.9,
+              drafter_stale=True, ngram_n=1, ngram_continuation_len=4, seed=9)
+    r1 = eng.run_rollout(prompts, max_lens, **kw)
+    r2 = eng.run_rollout(prompts, max_lens, **kw)
+    eng.close()
+    assert r1["tokens"] == r2["tokens"]
+    assert r1["plain_steps"] == 0 and r1["sd_steps"] > 0
+    for t, m in zip(r1["tokens"], max_lens):
+        assert 1 <= len(t) <= m
+        assert len(t) == m or t[-1] == 0
