@@ -103,6 +103,14 @@ TLT_API int tlt_prefill(tlt_engine* e, int b, const int32_t* slot_ids, const int
 TLT_API int tlt_release(tlt_engine* e, int slot_id);
 /* Committed target KV length of a slot (positions 0..len-1 hold KV). */
 TLT_API int tlt_slot_len(tlt_engine* e, int slot_id, int32_t* len);
+/* C2 (drafter training samples; the reference hands finished
+ * sequences to DataBuffer, data_buffer.hpp:48-68): copies a live slot's
+ * committed tokens [0, len] (len = tlt_slot_len; token len is the pending
+ * root) and its target features [0, len) as bf16 [len][hidden] into caller
+ * memory, host or device (cudaMemcpyDefault). Either pointer may be NULL.
+ * Call before tlt_release. */
+TLT_API int tlt_export_sequence(tlt_engine* e, int slot_id, int32_t* tokens, int max_tokens, void* features,
+                                size_t features_bytes, int32_t* len);
 
 /* ---- one engine step ---------------------------------------------------- */
 /* Tree produced by the drafter, reference DraftTree (spec_decode.hpp:50-70),

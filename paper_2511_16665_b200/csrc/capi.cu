@@ -77,6 +77,12 @@ TLT_API int tlt_release(tlt_engine* e, int slot_id) {
     return guard([&] { e->e->release(slot_id); });
 }
 
+TLT_API int tlt_export_sequence(tlt_engine* e, int slot_id, int32_t* tokens, int max_tokens, void* features,
+                                size_t features_bytes, int32_t* len) {
+    if (!e || !len) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { *len = e->e->export_sequence(slot_id, tokens, max_tokens, features, features_bytes); });
+}
+
 TLT_API int tlt_slot_len(tlt_engine* e, int slot_id, int32_t* len) {
     if (!e || !len) return fail(TLT_ERR_STATE, "null argument");
     return guard([&] {

@@ -715,6 +715,24 @@ void Engine::release(int slot) {
     lt_[slot] = ld_[slot] = 0;
 }
 
+int Engine::export_sequence(int slot, int32_t* tokens, int max_tokens, void* features, size_t features_bytes) {
+    if (slot < 0 || slot >= cfg.max_slots || !live_[slot]) throw ConfigErr("slot_id", "slot not live");
+    const int n = lt_[slot];  // positions with committed KV / target features; token n is the pending root
+    if (tokens) {
+        if (max_tokens < n + 1) throw ConfigErr("max_tokens", "buffer smaller than slot_len + 1");
+        CUDA_CHECK(cudaMemcpyAsync(tokens, tok_hist_ + (size_t)slot * cap_, sizeof(int32_t) * (n + 1),
+                                   cudaMemcpyDefault, st_));
+    }
+    if (features) {
+        const size_t bytes = sizeof(bf16) * (size_t)n * cfg.hidden;
+        if (features_bytes < bytes) throw ConfigErr("features_bytes", "buffer smaller than slot_len x hidden x 2");
+        CUDA_CHECK(cudaMemcpyAsync(features, feat_hist_ + (size_t)slot * cap_ * cfg.hidden, bytes, cudaMemcpyDefault,
+                                   st_));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    return n;
+}
+
 // Drafter catch-up (after plain-decode steps): committed positions [ld, lt)
 // with target features, chunked. The SD graph then sees exactly 1 + accepted
 // pending rows per request.

@@ -52,6 +52,9 @@ public:
 
     void prefill(int b, const int32_t* slots, const int32_t* lens, const int32_t* tokens);
     void release(int slot);
+    // C2 (drafter training samples): committed tokens [0, lt] and target
+    // features [0, lt) of a live slot into caller memory (host or device)
+    int export_sequence(int slot, int32_t* tokens, int max_tokens, void* features, size_t features_bytes);
     // greedy tree SD step; returns device ms
     float sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out);
     float ar_step(int b, const int32_t* slots, int32_t* out_tokens);

@@ -146,6 +146,8 @@ class Engine:
         _check(self.L.tlt_engine_create(C.byref(self.cfg), C.byref(self.icfg), device, C.byref(h)))
         self.h = h
         self.vocab = m["vocab"]
+        self.hidden = m["hidden"]
+        self.device = device
 
     def close(self):
         if getattr(self, "h", None):
@@ -310,6 +312,23 @@ class Engine:
         res = StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
                          [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
         return res, consumed
+
+    def export_sequence(self, slot: int, device: bool = True):
+        """C2 payload of a live slot (tlt_export_sequence): committed tokens
+        [0, len] (int32) and target features [0, len) as bf16 [len][hidden],
+        copied by the engine straight into a torch tensor (CUDA when device)."""
+        import torch
+        n = C.c_int32()
+        _check(self.L.tlt_slot_len(self.h, slot, C.byref(n)))
+        L = n.value
+        toks = np.zeros(L + 1, np.int32)
+        feats = torch.empty((L, self.hidden), dtype=torch.bfloat16,
+                            device=f"cuda:{self.device}" if device else "cpu")
+        if not device:
+            feats = feats.pin_memory() if torch.cuda.is_available() else feats
+        _check(self.L.tlt_export_sequence(self.h, slot, _p(toks), L + 1, C.c_void_p(feats.data_ptr()),
+                                          C.c_size_t(feats.numel() * 2), C.byref(n)))
+        return toks, feats
 
     def debug_target_rows(self, i: int, max_rows: int = 32):
         out = np.zeros((max_rows, self.vocab), np.float64)
@@ -497,6 +516,46 @@ def merge_bandit_stats(dist, local: "Mab", shared: "Mab") -> int:
             self.L.tlt_mab_destroy(self.h)
         except Exception:
             pass
+
+
+def handback_samples(dist, samples, trainer_rank: int = 0):
+    """C2: every rank hands its finished sequences
+    [(tokens int32 [L+1], features bf16 [L][d]), ...] to the trainer rank,
+    which returns them as [(rank, tokens, features), ...] in rank order (its
+    own first at its rank position); other ranks return []. Point-to-point
+    over the process group's backend (NCCL with CUDA tensors, gloo on CPU);
+    off the decode critical path (called at rollout boundaries)."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = samples[0][1].device if samples else (torch.device("cuda", torch.cuda.current_device())
+                                                 if dist.get_backend() == "nccl" else torch.device("cpu"))
+    cnt = torch.tensor([len(samples)], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt)
+    out = []
+    if rank != trainer_rank:
+        for toks, feats in samples:
+            t = torch.as_tensor(np.asarray(toks, np.int32)).to(dev)
+            hdr = torch.tensor([t.numel(), feats.shape[0], feats.shape[1] if feats.dim() == 2 else 0],
+                               dtype=torch.int64, device=dev)
+            dist.send(hdr, trainer_rank)
+            dist.send(t, trainer_rank)
+            dist.send(feats.contiguous().view(torch.int16), trainer_rank)  # bf16 bits
+        return out
+    for r in range(world):
+        if r == trainer_rank:
+            out += [(r, torch.as_tensor(np.asarray(t, np.int32)).to(dev), f) for t, f in samples]
+            continue
+        for _ in range(int(counts[r].item())):
+            hdr = torch.zeros(3, dtype=torch.int64, device=dev)
+            dist.recv(hdr, r)
+            nt, L, d = (int(x) for x in hdr.tolist())
+            t = torch.zeros(nt, dtype=torch.int32, device=dev)
+            dist.recv(t, r)
+            f = torch.zeros((L, d), dtype=torch.int16, device=dev)
+            dist.recv(f, r)
+            out.append((r, t, f.view(torch.bfloat16)))
+    return out
 
 
 def plan_captures(strategies, thresholds, max_batch=32, vanilla=False):
