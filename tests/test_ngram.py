@@ -298,3 +298,42 @@ def test_gpu_rollout_ngram_stochastic_deterministic():
     for t, m in zip(r1["tokens"], max_lens):
         assert 1 <= len(t) <= m
         assert len(t) == m or t[-1] == 0
+
+
+@pytest.mark.gpu
+def test_gpu_chain_verify_7b_shape_lossless():
+    """Qwen2.5-7B shape (V=152064, 28 layers): greedy chain verification of
+    perfect / wrong / partially right chains reproduces plain decode."""
+    rng = np.random.default_rng(21)
+    prompts = [rng.integers(2, 152064, 40).tolist() for _ in range(2)]
+    D, steps = 5, 6
+    eng = Engine("qwen2.5-7b", max_slots=2, max_ctx=256, device=0)
+    eng.prefill([0, 1], prompts)
+    ref = [[], []]
+    for _ in range(steps * (D + 1)):
+        toks, _ = eng.ar_step([0, 1])
+        for i in range(2):
+            ref[i].append(int(toks[i]))
+    eng.close()
+    eng = Engine("qwen2.5-7b", max_slots=2, max_ctx=256, device=0)
+    eng.prefill([0, 1], prompts)
+    out = [[], []]
+    for step in range(steps):
+        chains = []
+        for i in range(2):
+            nxt = ref[i][len(out[i]):len(out[i]) + D]
+            mode = (step + i) % 3
+            if mode == 1:
+                nxt = nxt[:2] + [(nxt[2] + 7) % 152064] + nxt[3:]  # wrong third token
+            elif mode == 2:
+                nxt = [(nxt[0] + 1) % 152064]
+            chains.append(nxt)
+        r = eng.sd_step_chain(D, [0, 1], chains)
+        for i in range(2):
+            a = int(r.accept_len[i])
+            mode = (step + i) % 3
+            assert a == {0: D, 1: 2, 2: 0}[mode], (step, i, a)
+            out[i] += r.accepted[i] + [int(r.bonus[i])]
+    eng.close()
+    for i in range(2):
+        assert out[i] == ref[i][:len(out[i])]
