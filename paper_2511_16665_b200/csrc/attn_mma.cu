@@ -877,12 +877,27 @@ int attention_dec_chunk(int n_groups, int kv, int max_keys) {
         const char* v = std::getenv("TLT_ATTN_DEC_CTAS");
         return v ? std::atoi(v) : 296;
     }();
-    const int chunks = std::max(1, (max_keys + kSplit - 1) / kSplit);
+    // split granularity (keys): any multiple of the 64-key tile works for this
+    // kernel. 64-key granularity balances the splits (b = 16: 4 x 320 keys
+    // instead of 2 x 512 + 1; 26.7 -> 22.6 us per layer), and a 256-key floor
+    // keeps the long-tail shapes from fragmenting into many tiny splits whose
+    // combine costs more than it saves (b = 1: 16.5 us vs 18.5 us at 64 keys;
+    // profiles/r1_attn_dec_granularity.txt)
+    static const int gran = [] {
+        const char* v = std::getenv("TLT_ATTN_DEC_GRAN");
+        const int g = v ? std::atoi(v) : kDKeys;
+        return std::max(kDKeys, (g / kDKeys) * kDKeys);
+    }();
+    static const int min_chunk = [] {
+        const char* v = std::getenv("TLT_ATTN_DEC_MIN_CHUNK");
+        return v ? std::max(kDKeys, std::atoi(v)) : 256;
+    }();
+    const int chunks = std::max(1, (max_keys + gran - 1) / gran);
     // (request, head) pairs alone reach the CTA target: a single split (the
     // kernel then writes the normalised output itself, no partials, no combine)
     const int want_splits = n_groups * kv >= target_ctas ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
     const int per = std::max(1, (chunks + want_splits - 1) / want_splits);
-    return per * kSplit;
+    return std::max(min_chunk, per * gran);
 }
 
 template <int kHD>
