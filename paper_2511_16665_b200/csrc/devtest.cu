@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <vector>
 #include "../../include/tlt_b200.h"
 
 using namespace tlt;
@@ -153,6 +154,29 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
             if (!attention_tc_shape_ok(p)) throw ConfigErr("kernel", "shape not eligible for the tcgen05 kernel");
             launch_attention_tc(p, 0);
             launch_attn_combine_only(p, 0);
+        } else if (kernel == 2 || kernel == 3) {
+            // flash-decode kernel as the engine sizes it (<= 16 query vectors per
+            // request and KV head); 3 = split combine fused into the last CTA
+            int* ctr = nullptr;
+            if (rows_per_req * (H / KV) > 16) throw ConfigErr("kernel", "decode kernel needs <= 16 query vectors");
+            p.chunk = attention_dec_chunk(n_groups, KV, max_keys);
+            if (p.chunk <= 0) throw ConfigErr("kernel", "decode kernel disabled (TLT_ATTN_DEC=0)");
+            p.dec = 1;
+            p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+            if (kernel == 3) {
+                CUDA_CHECK(cudaMalloc(&ctr, sizeof(int) * n_groups * KV));
+                CUDA_CHECK(cudaMemset(ctr, 0, sizeof(int) * n_groups * KV));
+                p.counters = ctr;
+            }
+            launch_attention(p, 0);
+            CUDA_CHECK(cudaDeviceSynchronize());
+            if (ctr) {  // the last CTA must have reset every counter (graph-replay invariant)
+                std::vector<int> h(n_groups * KV);
+                CUDA_CHECK(cudaMemcpy(h.data(), ctr, sizeof(int) * h.size(), cudaMemcpyDeviceToHost));
+                cudaFree(ctr);
+                for (int v : h)
+                    if (v != 0) throw ConfigErr("counters", "fused combine left a non-zero counter");
+            }
         } else {
             p.impl = 1;
             launch_attention_legacy(p, 0);

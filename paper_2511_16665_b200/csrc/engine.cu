@@ -398,12 +398,17 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
     p.ws_l = aws_l_;
     p.ws_o = aws_o_;
     static const int fused_combine = [] {
-        // off by default: the electing CTA's serial merge measured slower than
-        // the separate combine launch (rollout 5072 vs 5604 tok/s)
+        // -1 (auto): only for flash-decode with >= 128 (request, KV head)
+        // pairs — there the last CTA's merge beats the separate combine
+        // launch (b=32: 28.7 -> 27.1 us per layer), while at b <= 8 and on the
+        // tree kernels the serial merge is slower (b=1: 16.7 -> 18.5 us;
+        // rollout 5072 vs 5604 tok/s with it on everywhere;
+        // profiles/r1_attn_dec_fused_combine_sweep.txt). 1 = always, 0 = never.
         const char* v = std::getenv("TLT_ATTN_FUSED_COMBINE");
-        return v ? std::atoi(v) : 0;
+        return v ? std::atoi(v) : -1;
     }();
-    if (fused_combine && p.impl == 1) {
+    const bool use_fc = fused_combine > 0 || (fused_combine < 0 && p.dec && ngroups * cfg.kv_heads >= 128);
+    if (use_fc && p.impl == 1) {
         if (!attn_counters_) {
             attn_counters_ = dmalloc<int>(1 << 16);
             CUDA_CHECK(cudaMemset(attn_counters_, 0, sizeof(int) << 16));

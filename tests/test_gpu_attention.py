@@ -79,3 +79,18 @@ def test_tree_attention(n_groups, rpr, lc, remap, kernel):
     got = run(c, kernel)
     err = (got - ref).abs()
     assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+@pytest.mark.parametrize("n_groups,lc", [(1, 1000), (5, 700), (33, 1500), (40, 300)])
+def test_decode_attention_fused_combine(n_groups, lc):
+    """Flash-decode kernel (1 row x 7 q-heads per request, balanced key splits)
+    with the separate combine launch (kernel 2) and with the combine fused into
+    the last CTA (kernel 3): both within bf16 tolerance of torch fp32, and
+    bit-identical to each other (same merge arithmetic, fixed split order)."""
+    c = make_case(n_groups, 1, lc, seed=7 * n_groups + lc)
+    ref = reference(c)
+    sep = run(c, 2)
+    fused = run(c, 3)
+    err = (sep - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+    assert torch.equal(sep, fused)
