@@ -72,7 +72,8 @@ __device__ __forceinline__ void attn_fused_combine(const AttnParams& p, int grp,
     __syncthreads();
     const int n_qt = gridDim.x;
     const long long cidx = ((long long)grp * p.KV + kvh) * n_qt + qtile;
-    const int n_active = min(p.max_splits, (p.g.lc[grp] + p.g.ntail[grp] + p.chunk - 1) / p.chunk);
+    const int tk = p.g.lc[grp] + p.g.ntail[grp], ch = split_chunk(p, tk);
+    const int n_active = min(p.max_splits, (tk + ch - 1) / ch);
     if (threadIdx.x == 0) s_last = atomicAdd(p.counters + cidx, 1) == n_active - 1;
     __syncthreads();
     if (!s_last) return;
@@ -81,7 +82,8 @@ __device__ __forceinline__ void attn_fused_combine(const AttnParams& p, int grp,
     const int nqv = p.rows_per_req * G;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int total_keys = p.g.lc[grp] + p.g.ntail[grp];
-    const int nsplit = min(p.max_splits, (total_keys + p.chunk - 1) / p.chunk);
+    const int nsplit = n_active;
+    (void)total_keys;
     constexpr int DPL = kHD / 32;
     for (int gqv = qv_lo + warp; gqv < min(qv_hi, nqv); gqv += nw) {
         const int row = grp * p.rows_per_req + gqv / G;
@@ -646,9 +648,10 @@ __global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
     const int slot = p.g.slot[grp];
     const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
     const int total = slot >= 0 ? lc + ntail : 0;
-    const int k0 = split * p.chunk;
+    const int chunk = split_chunk(p, total);
+    const int k0 = split * chunk;
     if (k0 >= total) return;  // empty split
-    const int k1 = min(total, k0 + p.chunk);
+    const int k1 = min(total, k0 + chunk);
     const int ntiles = (k1 - k0 + kDKeys - 1) / kDKeys;
     const long long slot_base = ((long long)slot * p.KV + kvh) * p.cap;
 
@@ -866,6 +869,21 @@ void launch_attention_dec_t(const AttnParams& p, cudaStream_t st) {
     launch_pdl(k_attention_dec<kHD>, grid, 128, smem, st, p);
 }
 
+// Target split count per (request, KV head) for the per-request split sizing
+// (split_chunk); 0 = per-request sizing off (TLT_ATTN_DEC_DYN=0).
+int attention_dec_target_splits(int n_groups, int kv) {
+    static const int dyn = [] {
+        const char* v = std::getenv("TLT_ATTN_DEC_DYN");
+        return v ? std::atoi(v) : 1;
+    }();
+    if (!dyn) return 0;
+    static const int target_ctas = [] {
+        const char* v = std::getenv("TLT_ATTN_DEC_CTAS");
+        return v ? std::atoi(v) : 296;
+    }();
+    return n_groups * kv >= target_ctas ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
+}
+
 int attention_dec_chunk(int n_groups, int kv, int max_keys) {
     // chunk (multiple of 256 keys) so that (groups x KV heads x splits) ~ 2 CTAs per SM
     static const int off = [] {
@@ -896,6 +914,18 @@ int attention_dec_chunk(int n_groups, int kv, int max_keys) {
     // (request, head) pairs alone reach the CTA target: a single split (the
     // kernel then writes the normalised output itself, no partials, no combine)
     const int want_splits = n_groups * kv >= target_ctas ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
+    static const int even = [] {
+        const char* v = std::getenv("TLT_ATTN_DEC_EVEN");
+        return v ? std::atoi(v) : 1;
+    }();
+    if (even && max_keys <= min_chunk + min_chunk / 2) {
+        // short contexts (<= 384 keys) run as ONE split: no remainder split,
+        // no partials, no combine launch (b=1 ctx 257: 14.4 -> 13.1 us; b=4:
+        // 16.5 -> 14.4 us). Longer contexts keep 256-key-floored splits: the
+        // per-CTA tile count is the critical path there (b=1 ctx 1025: 5 x 256
+        // beats 4 x 320, 16.5 vs 18.5 us; profiles/r1_attn_dec_even.txt)
+        return std::max(gran, (max_keys + gran - 1) / gran * gran);
+    }
     const int per = std::max(1, (chunks + want_splits - 1) / want_splits);
     return std::max(min_chunk, per * gran);
 }

@@ -162,7 +162,9 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
             p.chunk = attention_dec_chunk(n_groups, KV, max_keys);
             if (p.chunk <= 0) throw ConfigErr("kernel", "decode kernel disabled (TLT_ATTN_DEC=0)");
             p.dec = 1;
+            p.dyn_splits = attention_dec_target_splits(n_groups, KV);
             p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+            if (p.dyn_splits > 0) p.max_splits = std::max(1, std::min(p.dyn_splits, (max_keys + 255) / 256));
             if (kernel == 3) {
                 CUDA_CHECK(cudaMalloc(&ctr, sizeof(int) * n_groups * KV));
                 CUDA_CHECK(cudaMemset(ctr, 0, sizeof(int) * n_groups * KV));

@@ -387,9 +387,12 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
         if (ch > 0) {
             p.chunk = ch;
             p.dec = 1;
+            p.dyn_splits = attention_dec_target_splits(ngroups, cfg.kv_heads);
         }
     }
     p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+    // per-request split sizing: the grid covers the bound split_chunk can reach
+    if (p.dyn_splits > 0) p.max_splits = std::max(1, std::min(p.dyn_splits, (max_keys + 255) / 256));
     p.qv_cap = rpr * (cfg.heads / cfg.kv_heads);
     const size_t need = (size_t)ngroups * p.max_splits * p.qv_cap * cfg.kv_heads;
     if (need * cfg.head_dim > aws_elems_ || need > aws_elems_ / 32)
@@ -949,7 +952,7 @@ float Engine::probe_attention(int b, int ctx, int rpr, int iters, double* bytes)
         CUDA_CHECK(cudaEventRecord(ev0_, st_));
         for (int it = 0; it < iters; ++it) {
             const int l = it % cfg.layers;
-            attention(kc_[l], vc_[l], cap_, prows_, pg_, rpr, b, ctx + rpr);
+            attention(kc_[l], vc_[l], cap_, prows_, pg_, rpr, b, cap_);  // grid sized as in the engine
         }
         CUDA_CHECK(cudaEventRecord(ev1_, st_));
         CUDA_CHECK(cudaEventSynchronize(ev1_));

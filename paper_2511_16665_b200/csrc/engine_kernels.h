@@ -23,12 +23,28 @@ struct AttnParams {
     int impl;  // 0: CUDA-core reference kernel, 1: tensor-core flash-decode (attn_mma.cu)
     int* counters;  // non-null: fused split combine (last CTA per tile), zeroed buffer
     int dec;        // 1: decode kernel (<= 16 query vectors per request/head), chunk = multiple of 256
+    int dyn_splits; // > 0 (decode only): split size chosen per request from its ACTUAL key count
+                    // (split_chunk below) for this many target splits; 0 = fixed p.chunk
     // optional L2 warm-up of the NEXT kernel's weights (the o-proj): the
     // attention kernels are latency-bound and leave HBM idle, so each CTA
     // issues a bulk L2 prefetch of its slice of [pf, pf + pf_bytes)
     const void* pf;
     long long pf_bytes;
 };
+
+// Keys per split for a request with `total` keys. Fixed p.chunk unless
+// dyn_splits > 0 (flash-decode inside CUDA graphs, whose grid is sized for the
+// cache capacity): then the request's own key count is cut into <= dyn_splits
+// splits of whole 64-key tiles, never shorter than 256 keys (the per-CTA tile
+// count is the critical path: 5 x 64-key tiles in one CTA is slower than
+// 4 + 1 in two plus the combine). Number of active splits <= min(dyn_splits,
+// ceil(total / 256)), which is what the host sizes max_splits for.
+__host__ __device__ __forceinline__ int split_chunk(const AttnParams& p, int total) {
+    if (p.dyn_splits <= 0) return p.chunk;
+    const int tiles = (total + 63) / 64;
+    const int per = (tiles + p.dyn_splits - 1) / p.dyn_splits;
+    return per * 64 < 256 ? 256 : per * 64;
+}
 void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc = true);
 // test hooks: the mma.sync kernels + combine, and the combine alone
 void launch_attention_legacy(const AttnParams& p, cudaStream_t st);
@@ -41,6 +57,7 @@ bool attention_tc_shape_ok(const AttnParams& p);
 void launch_attention_tc(const AttnParams& p, cudaStream_t st);
 int attention_mma_split();
 int attention_dec_chunk(int n_groups, int kv, int max_keys);
+int attention_dec_target_splits(int n_groups, int kv);
 
 struct TreeParams {
     const StepIn* step;

@@ -361,7 +361,8 @@ __global__ void k_attn_combine(AttnParams p) {
     const int head = kvh * G + gqv % G;
     if (p.rows.slot[row] < 0) return;
     const int total_keys = p.g.lc[grp] + p.g.ntail[grp];
-    const int nsplit = min(p.max_splits, (total_keys + p.chunk - 1) / p.chunk);
+    const int ch = split_chunk(p, total_keys);
+    const int nsplit = min(p.max_splits, (total_keys + ch - 1) / ch);
     constexpr int DPL = HD / 32;
     float M = -CUDART_INF_F;
     for (int s = 0; s < nsplit; ++s) {
