@@ -149,6 +149,10 @@ static void free_layer(orc_layer* L) {
     free(L->gu);
     free(L->down);
 }
+void orc_model_set_threads(orc_model* m, int n_threads) {
+    m->n_threads = n_threads < 1 ? 1 : (n_threads > 256 ? 256 : n_threads);
+}
+
 void orc_model_destroy(orc_model* m) {
     if (!m) return;
     free(m->embed);
@@ -514,6 +518,13 @@ int orc_drafter_row(orc_seq* s, const int32_t* path, int n, double* probs, float
     }
     if (logits_out) memcpy(logits_out, lg, sizeof(float) * (size_t)m->c.vocab);
     if (probs) softmax64(lg, m->c.vocab, probs);
+    return 0;
+}
+
+int orc_seq_features(orc_seq* s, int from, int n, uint16_t* out) {
+    if (from < 0 || n < 0 || ensure_target(s) || from + n > s->tgt_kv_len) return -1;
+    const size_t d = (size_t)s->m->c.hidden;
+    memcpy(out, s->feat + (size_t)from * d, sizeof(uint16_t) * (size_t)n * d);
     return 0;
 }
 

@@ -178,6 +178,7 @@ typedef struct {
 
 typedef struct orc_model orc_model;
 orc_model* orc_model_create(const orc_model_cfg* cfg, const orc_init_cfg* init, int n_threads);
+void orc_model_set_threads(orc_model* m, int n_threads);
 void orc_model_destroy(orc_model* m);
 /* Raw bf16 bits of a named weight (test access): tensor ids as in DESIGN.md. */
 int orc_model_weight(orc_model* m, int tensor_id, int layer, const uint16_t** ptr, int64_t* n);
@@ -201,6 +202,9 @@ int orc_target_logits_path(orc_seq* s, const int32_t* path, int n, float* logits
  * target features), then the distribution of the next token after
  * committed ++ path, with EAGLE self-feeding along path. fp64 softmax. */
 int orc_drafter_row(orc_seq* s, const int32_t* path, int n, double* probs, float* logits);
+/* Target hidden states (final residual stream, bf16 bits) of committed
+ * positions [from, from + n): the drafter's input features. */
+int orc_seq_features(orc_seq* s, int from, int n, uint16_t* out);
 /* Truncate the committed state (target and drafter) to len tokens. */
 int orc_seq_truncate(orc_seq* s, int len);
 

@@ -214,8 +214,7 @@ TLT_API int tlt_debug_expansions(tlt_engine* e, int i, int max_exp, int32_t* n_e
     if (!e) return fail(TLT_ERR_STATE, "null engine");
     return guard([&] {
         auto& E = *e->e;
-        if (i < 0 || i >= (int)E.dbg_exp.size()) throw tlt::ConfigErr("i", "no debug data for request");
-        const auto& ex = E.dbg_exp[i];
+        const auto& ex = E.debug_expansions(i);
         const int n = std::min<int>(max_exp, (int)ex.size());
         *n_exp = (int32_t)ex.size();
         const int V = E.cfg.vocab;
@@ -231,8 +230,7 @@ TLT_API int tlt_debug_verify_logits(tlt_engine* e, int i, float* logits, int max
     if (!e) return fail(TLT_ERR_STATE, "null engine");
     return guard([&] {
         auto& E = *e->e;
-        if (i < 0 || i >= (int)E.dbg_vlogits.size()) throw tlt::ConfigErr("i", "no debug data for request");
-        const auto& v = E.dbg_vlogits[i];
+        const auto v = E.debug_verify_logits(i);
         const int V = E.cfg.vocab;
         const int rows = (int)(v.size() / V);
         *n_rows = rows;

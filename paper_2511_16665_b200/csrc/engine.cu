@@ -83,6 +83,24 @@ int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
 }
+// Drafter levels of a (b_hi, D, k, T) tree step: rows per request Fd[lv]
+// (level 1: pending + root; level lv >= 2: min(T, k^(lv-1)) frontier rows),
+// drafter row base[lv], and lmoff[lv] = LM-head row offset of the level in a
+// level-concatenated array (level 1 has one LM row per request).
+void level_plan(int b_hi, int D, int k, int T, std::vector<int>& base, std::vector<int>& Fd,
+                std::vector<int>& lmoff) {
+    base.assign(D + 2, 0);
+    Fd.assign(D + 2, 0);
+    lmoff.assign(D + 2, 0);
+    Fd[1] = D + 1;
+    long long kp = 1;
+    for (int lv = 2; lv <= D; ++lv) {
+        kp = std::min<long long>(kp * k, 1 << 20);
+        Fd[lv] = (int)std::min<long long>(T, kp);
+        base[lv] = base[lv - 1] + b_hi * Fd[lv - 1];
+    }
+    for (int lv = 1; lv <= D; ++lv) lmoff[lv + 1] = lmoff[lv] + (lv == 1 ? b_hi : b_hi * Fd[lv]);
+}
 }  // namespace
 
 Engine::Engine(const tlt_model_cfg& c, const tlt_init_cfg& init, int device) : cfg(c), dev_(device) {
@@ -127,6 +145,7 @@ Engine::~Engine() {
     for (auto& g : dg_) free_groups(g);
     free_groups(vg_), free_groups(pg_);
     f(root_row_), f(row_node_), f(tk_tok_), f(tk_logit_), f(tk_M_), f(tk_S_), f(argmax_), f(dbg_probs_);
+    free_debug_buffers();
     f(arena_), f(arena_n_), f(kept_), f(kept_n_), f(exp_n_), f(done_);
     f(tree_tok_), f(tree_par_), f(tree_dep_), f(tree_n_), f(tree_prob_), f(tree_pp_);
     f(acc_nodes_), f(acc_tok_), f(acc_len_), f(bonus_), f(kv_len_), f(ar_tok_), f(d_step_);
@@ -969,18 +988,11 @@ float Engine::probe_attention(int b, int ctx, int rpr, int iters, double* bytes)
 // commit. All shapes static in (b_hi, D, k, T); per-step data lives on the
 // device (StepIn uploaded first), so the sequence is graph-capturable.
 void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real) {
+    (void)b_real;
     const int d = cfg.hidden, V = cfg.vocab, D1 = D + 1;
     CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
-    // level bases
-    std::vector<int> base(D + 2, 0), Fd(D + 2, 0);
-    base[1] = 0;
-    Fd[1] = D1;  // rows per request at level 1 (pending + root)
-    long long kp = 1;
-    for (int lv = 2; lv <= D; ++lv) {
-        kp = std::min<long long>(kp * k, 1 << 20);
-        Fd[lv] = (int)std::min<long long>(T, kp);
-        base[lv] = base[lv - 1] + b_hi * Fd[lv - 1];
-    }
+    std::vector<int> base, Fd, lmoff;
+    level_plan(b_hi, D, k, T, base, Fd, lmoff);
     if (D >= 2 && base[D] + b_hi * Fd[D] > Rmeta_) throw ConfigErr("strategy", "draft rows exceed TLT_MAX_DRAFT_ROWS");
     const int max_keys_d = dcap_;
     launch_rows_level1(d_step_, b_hi, b_hi, D1, drows_, dg_[1], root_row_, tok_hist_, cap_, st_);
@@ -1016,10 +1028,9 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
     tp.vg = vg_;
     tp.tok_hist = tok_hist_;
     tp.cap = cap_;
-    if (dbg) {
-        dbg_exp.assign(b_real, {});
-        if (!dbg_probs_) dbg_probs_ = dmalloc<double>((size_t)std::max(R_, 256) * V);
-    }
+    auto d2d = [&](void* dst, const void* src, size_t bytes) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st_));
+    };
     for (int lv = 1; lv <= D; ++lv) {
         const int R = b_hi * Fd[lv];
         const Rows rw = sub(drows_, base[lv]);
@@ -1027,33 +1038,12 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
         drafter_forward(rw, dg_[lv], R, Fd[lv], b_hi, max_keys_d, lv == 1 ? root_row_ : nullptr, n_lm, k,
                         lv == 1 ? dg_[1].slot : rw.slot, dbg, dfeat_ + (size_t)base[lv] * d);
         if (dbg) {
-            // full fp64 rows of every live expansion (parity export)
-            launch_row_probs(logits_, n_lm, V, tk_M_, tk_S_, dbg_probs_, st_);
-            std::vector<int> live(n_lm), node(n_lm);
-            std::vector<double> rowsbuf((size_t)n_lm * V);
-            CUDA_CHECK(cudaMemcpyAsync(live.data(), lv == 1 ? dg_[1].slot : rw.slot, sizeof(int) * n_lm,
-                                       cudaMemcpyDeviceToHost, st_));
-            if (lv > 1)
-                CUDA_CHECK(cudaMemcpyAsync(node.data(), row_node_ + base[lv], sizeof(int) * n_lm,
-                                           cudaMemcpyDeviceToHost, st_));
-            CUDA_CHECK(cudaMemcpyAsync(rowsbuf.data(), dbg_probs_, sizeof(double) * n_lm * V, cudaMemcpyDeviceToHost,
-                                       st_));
-            std::vector<Cand> ar((size_t)b_real * arena_cap_);
-            CUDA_CHECK(cudaMemcpyAsync(ar.data(), arena_, sizeof(Cand) * ar.size(), cudaMemcpyDeviceToHost, st_));
-            CUDA_CHECK(cudaStreamSynchronize(st_));
-            for (int r = 0; r < n_lm; ++r) {
-                if (live[r] < 0) continue;
-                const int i = lv == 1 ? r : r / Fd[lv];
-                if (i >= b_real) continue;
-                DebugExp ex;
-                if (lv > 1) {
-                    for (int a = node[r]; a >= 0; a = ar[(size_t)i * arena_cap_ + a].parent)
-                        ex.path.push_back(ar[(size_t)i * arena_cap_ + a].token);
-                    std::reverse(ex.path.begin(), ex.path.end());
-                }
-                ex.row.assign(rowsbuf.begin() + (size_t)r * V, rowsbuf.begin() + (size_t)(r + 1) * V);
-                dbg_exp[i].push_back(std::move(ex));
-            }
+            // parity export: this level's fp32 logits, row max / normaliser and
+            // liveness, copied on the stream (graph-capturable, no host sync)
+            d2d(dbg_lg_ + (size_t)lmoff[lv] * V, logits_, sizeof(float) * (size_t)n_lm * V);
+            d2d(dbg_M_ + lmoff[lv], tk_M_, sizeof(float) * n_lm);
+            d2d(dbg_S_ + lmoff[lv], tk_S_, sizeof(float) * n_lm);
+            d2d(dbg_live_ + lmoff[lv], lv == 1 ? dg_[1].slot : rw.slot, sizeof(int) * n_lm);
         }
         tp.level = lv;
         tp.lvl_base = base[lv];
@@ -1066,6 +1056,10 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
     }
     launch_tree_final(tp, st_);
     count_launch();
+    if (dbg) {
+        d2d(dbg_arena_, arena_, sizeof(Cand) * (size_t)b_hi * arena_cap_);
+        d2d(dbg_node_, row_node_, sizeof(int) * (size_t)(base[D] + b_hi * Fd[D]));
+    }
     verify_accept_commit(b_hi, T, dbg, b_real);
 }
 
@@ -1077,14 +1071,9 @@ void Engine::verify_accept_commit(int b_hi, int T, bool dbg, int b_real) {
     const int T1 = T + 1, RV = b_hi * T1;
     target_forward(vrows_, vg_, RV, T1, b_hi, max_keys_t, nullptr, feat_);
     lm_topk(x_, RV, 1, vrows_.slot, dbg, true);  // argmax per verify row (fused epilogue + merge)
-    if (dbg) {
-        dbg_vlogits.assign(b_real, {});
-        std::vector<float> lg((size_t)RV * V);
-        CUDA_CHECK(cudaMemcpyAsync(lg.data(), logits_, sizeof(float) * lg.size(), cudaMemcpyDeviceToHost, st_));
-        CUDA_CHECK(cudaStreamSynchronize(st_));
-        for (int i = 0; i < b_real; ++i)
-            dbg_vlogits[i].assign(lg.begin() + (size_t)i * T1 * V, lg.begin() + (size_t)(i + 1) * T1 * V);
-    }
+    if (dbg)  // verify logits (fp32, from the same LM-head GEMM) for the parity export
+        CUDA_CHECK(cudaMemcpyAsync(dbg_vlg_, logits_, sizeof(float) * (size_t)RV * V, cudaMemcpyDeviceToDevice, st_));
+    (void)b_real;
     AcceptParams ap{};
     ap.step = d_step_;
     ap.b = b_hi;
@@ -1186,10 +1175,13 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
         }
     }
     const bool dbg = debug_;
+    if (dbg) ensure_debug_buffers(b_hi, D, k, T);  // may drop debug graphs: before the lookup
     CUDA_CHECK(cudaEventRecord(ev0_, st_));
-    auto key = std::make_tuple(b_hi, D, k, T, 0);
+    // debug steps replay their own graphs (the production sequence plus the
+    // parity-export copy nodes), keyed apart from the production ones
+    auto key = std::make_tuple(b_hi, D, k, T, dbg ? 4 : 0);
     auto it = graphs_.find(key);
-    if (use_graphs && !dbg && it != graphs_.end()) {
+    if (use_graphs && it != graphs_.end()) {
         CUDA_CHECK(cudaGraphLaunch(it->second.first, st_));
         launches += it->second.second;
     } else {
@@ -1202,14 +1194,24 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
     ms += catchup_ms;
+    if (dbg) {
+        level_plan(b_hi, D, k, T, dbgs_.base, dbgs_.Fd, dbgs_.lmoff);
+        dbgs_.valid = dbgs_.greedy = true;
+        dbgs_.b_hi = b_hi;
+        dbgs_.b_real = b;
+        dbgs_.D = D;
+        dbgs_.T = T;
+        dbgs_.meta_rows = dbgs_.base[D] + b_hi * dbgs_.Fd[D];
+        dbg_cache_.clear();
+    }
     // capture for the next replay (after a successful eager run)
-    if (use_graphs && !dbg && it == graphs_.end()) {
+    if (use_graphs && it == graphs_.end()) {
         cudaGraph_t g;
         launches_in_seq_ = 0;
         CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
         // the captured sequence must not change device state: capture only
         try {
-            sd_device_sequence(b_hi, D, k, T, false, b);
+            sd_device_sequence(b_hi, D, k, T, dbg, b);
         } catch (...) {
             cudaStreamEndCapture(st_, &g);
             throw;
@@ -1434,6 +1436,107 @@ float Engine::ar_step(int b, const int32_t* slots, int32_t* out_tokens) {
         lt_[slots[i]] += 1;
     }
     return ms;
+}
+
+// ------------------------------------------------------------ debug export
+void Engine::free_debug_buffers() {
+    auto f = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    f(dbg_lg_), f(dbg_M_), f(dbg_S_), f(dbg_vlg_), f(dbg_live_), f(dbg_node_), f(dbg_arena_);
+    dbg_lg_ = dbg_M_ = dbg_S_ = dbg_vlg_ = nullptr;
+    dbg_live_ = dbg_node_ = nullptr;
+    dbg_arena_ = nullptr;
+    dbg_lg_rows_ = dbg_vlg_rows_ = dbg_meta_rows_ = dbg_arena_reqs_ = 0;
+}
+
+void Engine::ensure_debug_buffers(int b_hi, int D, int k, int T) {
+    std::vector<int> base, Fd, lmoff;
+    level_plan(b_hi, D, k, T, base, Fd, lmoff);
+    const size_t lg = lmoff[D + 1], vlg = (size_t)b_hi * (T + 1), meta = base[D] + b_hi * Fd[D];
+    if (lg <= dbg_lg_rows_ && vlg <= dbg_vlg_rows_ && meta <= dbg_meta_rows_ && (size_t)b_hi <= dbg_arena_reqs_) return;
+    // growing: debug graphs hold the old addresses
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    for (auto it = graphs_.begin(); it != graphs_.end();) {
+        if (std::get<4>(it->first) == 4) {
+            cudaGraphExecDestroy(it->second.first);
+            it = graphs_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    const size_t nlg = std::max(lg, dbg_lg_rows_), nv = std::max(vlg, dbg_vlg_rows_),
+                 nm = std::max(meta, dbg_meta_rows_), na = std::max((size_t)b_hi, dbg_arena_reqs_);
+    free_debug_buffers();
+    const size_t V = cfg.vocab;
+    dbg_lg_ = dmalloc<float>(nlg * V);
+    dbg_M_ = dmalloc<float>(nlg);
+    dbg_S_ = dmalloc<float>(nlg);
+    dbg_live_ = dmalloc<int>(nlg);
+    dbg_vlg_ = dmalloc<float>(nv * V);
+    dbg_node_ = dmalloc<int>(nm);
+    dbg_arena_ = dmalloc<Cand>(na * arena_cap_);
+    dbg_lg_rows_ = nlg;
+    dbg_vlg_rows_ = nv;
+    dbg_meta_rows_ = nm;
+    dbg_arena_reqs_ = na;
+}
+
+// Expansions of request i in the last debug sd_step, in the order the
+// eager export used (level by level, row order): the path from the root
+// (arena parents) and the full fp64 drafter row p = exp((double)(l - M)) / S
+// computed by k_row_probs from the copied fp32 logits.
+const std::vector<DebugExp>& Engine::debug_expansions(int i) {
+    if (!dbgs_.valid || !dbgs_.greedy) {
+        if (i < 0 || i >= (int)dbg_exp.size()) throw ConfigErr("i", "no debug data for request");
+        return dbg_exp[i];
+    }
+    if (i < 0 || i >= dbgs_.b_real) throw ConfigErr("i", "no debug data for request");
+    auto hit = dbg_cache_.find(i);
+    if (hit != dbg_cache_.end()) return hit->second;
+    const int V = cfg.vocab, D = dbgs_.D;
+    std::vector<Cand> ar(arena_cap_);
+    CUDA_CHECK(cudaMemcpy(ar.data(), dbg_arena_ + (size_t)i * arena_cap_, sizeof(Cand) * arena_cap_,
+                          cudaMemcpyDeviceToHost));
+    const int maxF = *std::max_element(dbgs_.Fd.begin() + 1, dbgs_.Fd.begin() + D + 1);
+    if (!dbg_probs_) dbg_probs_ = dmalloc<double>((size_t)std::max(R_, 256) * V);
+    std::vector<double> rows((size_t)maxF * V);
+    std::vector<DebugExp> out;
+    for (int lv = 1; lv <= D; ++lv) {
+        const int F = lv == 1 ? 1 : dbgs_.Fd[lv];
+        const int r0 = lv == 1 ? i : i * F;  // LM rows of request i within the level
+        std::vector<int> live(F), node(F, -1);
+        CUDA_CHECK(cudaMemcpy(live.data(), dbg_live_ + dbgs_.lmoff[lv] + r0, sizeof(int) * F, cudaMemcpyDeviceToHost));
+        if (lv > 1)
+            CUDA_CHECK(cudaMemcpy(node.data(), dbg_node_ + dbgs_.base[lv] + r0, sizeof(int) * F,
+                                  cudaMemcpyDeviceToHost));
+        const size_t lr = dbgs_.lmoff[lv] + r0;
+        launch_row_probs(dbg_lg_ + lr * V, F, V, dbg_M_ + lr, dbg_S_ + lr, dbg_probs_, st_);
+        CUDA_CHECK(cudaGetLastError());
+        CUDA_CHECK(cudaMemcpyAsync(rows.data(), dbg_probs_, sizeof(double) * (size_t)F * V, cudaMemcpyDeviceToHost,
+                                   st_));
+        CUDA_CHECK(cudaStreamSynchronize(st_));
+        for (int r = 0; r < F; ++r) {
+            if (live[r] < 0) continue;
+            DebugExp ex;
+            if (lv > 1) {
+                for (int a = node[r]; a >= 0; a = ar[a].parent) ex.path.push_back(ar[a].token);
+                std::reverse(ex.path.begin(), ex.path.end());
+            }
+            ex.row.assign(rows.begin() + (size_t)r * V, rows.begin() + (size_t)(r + 1) * V);
+            out.push_back(std::move(ex));
+        }
+    }
+    return dbg_cache_.emplace(i, std::move(out)).first->second;
+}
+
+std::vector<float> Engine::debug_verify_logits(int i) {
+    if (!dbgs_.valid || !dbgs_.greedy || i < 0 || i >= dbgs_.b_real)
+        throw ConfigErr("i", "no debug data for request");
+    const size_t V = cfg.vocab, T1 = dbgs_.T + 1;
+    std::vector<float> v(T1 * V);
+    CUDA_CHECK(cudaMemcpy(v.data(), dbg_vlg_ + (size_t)i * T1 * V, sizeof(float) * v.size(), cudaMemcpyDeviceToHost));
+    return v;
 }
 
 size_t Engine::graph_pool_build(const std::vector<tlt_capture_entry>& entries) {

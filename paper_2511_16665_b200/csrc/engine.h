@@ -80,9 +80,13 @@ public:
     float probe_attention(int b, int ctx, int rpr, int iters, double* bytes);
 
     // parity exports
-    std::vector<std::vector<DebugExp>> dbg_exp;  // [request i] expansions of the last sd_step
-    std::vector<std::vector<float>> dbg_vlogits; // [request i] [(T+1)*V]
+    std::vector<std::vector<DebugExp>> dbg_exp;  // [request i] expansions of the last stochastic step
     std::vector<float> dbg_ar_logits;            // [b*V]
+    // greedy tree step: expansions / verify logits of request i of the last
+    // debug sd_step, extracted after the step from the device copies the
+    // step's own (graph-captured) sequence made
+    const std::vector<DebugExp>& debug_expansions(int i);
+    std::vector<float> debug_verify_logits(int i);
 
     const tlt_model_cfg cfg;
     long long launches = 0;
@@ -177,6 +181,24 @@ private:
     float *tk_logit_ = nullptr, *tk_M_ = nullptr, *tk_S_ = nullptr;
     int* argmax_ = nullptr;
     double* dbg_probs_ = nullptr;
+    // Debug export of the greedy tree step. The sequence itself enqueues
+    // device-to-device copies (per drafter level: fp32 logits rows, M, S,
+    // row liveness; at the end: arena, row->node map, verify logits), so a
+    // debug step replays a CUDA graph exactly like a production step (same
+    // kernels, plus copy nodes). Host extraction is lazy, per request.
+    struct DbgStep {
+        bool valid = false, greedy = false;
+        int b_hi = 0, b_real = 0, D = 0, T = 0;
+        std::vector<int> Fd, base, lmoff;  // per level: rows/request, drafter row base, logits row offset
+        int meta_rows = 0;                 // drafter rows of the step (row_node / slot copies)
+    } dbgs_;
+    std::map<int, std::vector<DebugExp>> dbg_cache_;
+    float *dbg_lg_ = nullptr, *dbg_M_ = nullptr, *dbg_S_ = nullptr, *dbg_vlg_ = nullptr;
+    int *dbg_live_ = nullptr, *dbg_node_ = nullptr;
+    Cand* dbg_arena_ = nullptr;
+    size_t dbg_lg_rows_ = 0, dbg_vlg_rows_ = 0, dbg_meta_rows_ = 0, dbg_arena_reqs_ = 0;
+    void ensure_debug_buffers(int b_hi, int D, int k, int T);
+    void free_debug_buffers();
     // tree + accept
     Cand* arena_ = nullptr;
     int arena_cap_ = 16384;

@@ -70,7 +70,11 @@ void Engine::stoch_device_sequence(int b_hi, int D, double temperature, bool dbg
     tp.vg = vg_;
     tp.tok_hist = tok_hist_;
     tp.cap = cap_;
-    if (dbg) dbg_exp.assign(b_real, {});
+    if (dbg) {
+        dbg_exp.assign(b_real, {});
+        dbgs_.valid = true;
+        dbgs_.greedy = false;  // tlt_debug_expansions reads dbg_exp (q rows of the chain)
+    }
     // chain levels: one drafter row per request per level (k = 1)
     for (int lv = 1; lv <= D; ++lv) {
         const int base = lv == 1 ? 0 : b_hi * D1 + (lv - 2) * b_hi;

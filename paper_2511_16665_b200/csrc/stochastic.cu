@@ -10,8 +10,9 @@
 // path exports; tempering (token_model.hpp:161-173) is applied in double.
 // Inverse CDF (token_model.hpp:83-91) uses a fixed blocked double scan: each
 // thread owns a contiguous segment, segments are prefix-summed in thread
-// order. It equals the reference's sequential sum except when u falls within
-// double rounding of a CDF boundary.
+// order; when u falls within a rigorous rounding bound of a CDF boundary the
+// pick is redone with the reference's sequential sum, so the result is the
+// reference's pick by construction (inverse_cdf_block).
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -40,8 +41,21 @@ __device__ double block_sum_fixed(double v, double* sh) {
 }
 
 // inverse CDF over a probability row held in global memory (double):
-// min{t : u < cum(t)}, fallback V-1 (token_model.hpp:83-91)
+// min{t : u < cum(t)}, fallback V-1 (token_model.hpp:83-91), bit-exact with
+// the reference's SEQUENTIAL cumulative sum.
+//
+// Fast path: a blocked scan (each thread owns a contiguous segment, segment
+// sums exclusive-scanned in thread order) picks t*. The blocked prefix sums
+// cumB and the reference's sequential ones cumR are both sums of <= V
+// non-negative doubles totalling ~1, so each is within V * 2^-53 * (1 + tiny)
+// of the exact prefix and |cumB(t) - cumR(t)| < delta = V * 2^-51 (2x
+// margin). cumR is monotone (adding p >= 0 never decreases a double), so
+// t* is the reference's pick whenever u >= cumB(t*-1) + delta and
+// u < cumB(t*) - delta. Otherwise u sits within rounding of a CDF boundary
+// and one thread replays the reference's sequential sum exactly (rare: the
+// window is ~1e-10 wide).
 __device__ int inverse_cdf_block(const double* p, int V, double u, double* sh, int* ish) {
+    __shared__ double s_lo, s_hi;
     const int per = (V + kST - 1) / kST;
     const int a = threadIdx.x * per, b = min(V, a + per);
     double seg = 0.0;
@@ -58,20 +72,50 @@ __device__ int inverse_cdf_block(const double* p, int V, double u, double* sh, i
         ish[0] = V - 1;
     }
     __syncthreads();
-    double cum = sh[threadIdx.x];
+    double cum = sh[threadIdx.x], lo = cum, hi = cum;
     int found = 0x7fffffff;
     for (int i = a; i < b && i < V - 1; ++i) {
+        lo = cum;
         cum += p[i];
         if (u < cum) {
             found = i;
+            hi = cum;
             break;
         }
     }
     if (found != 0x7fffffff) atomicMin(ish, found);
     __syncthreads();
     const int r = ish[0];
+    if (found == r) {  // the winning thread: cumB(t*-1), cumB(t*)
+        s_lo = lo;
+        s_hi = hi;
+    }
+    if (r == V - 1 && a <= V - 2 && V - 2 < b) {  // no pick below V-1: cumB(V-2) bounds it
+        s_lo = cum;
+        s_hi = CUDART_INF;
+    }
     __syncthreads();
-    return r;
+    if (threadIdx.x == 0) {
+        const double delta = (double)V * 0x1p-51;
+        const bool lo_ok = r == 0 || u - s_lo >= delta;
+        const bool hi_ok = r == V - 1 || s_hi - u > delta;
+        if (!(lo_ok && hi_ok)) {  // boundary window: the reference's own loop
+            double c = 0.0;
+            int t = V - 1;
+            for (int i = 0; i < V - 1; ++i) {
+                c += p[i];
+                if (u < c) {
+                    t = i;
+                    break;
+                }
+            }
+            ish[0] = t;
+        }
+    }
+    __syncthreads();
+    const int res = ish[0];
+    __syncthreads();
+    return res;
 }
 
 // raw row from logits into dst (double), returns nothing; M/S via block reductions

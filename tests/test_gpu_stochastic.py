@@ -9,11 +9,21 @@ import numpy as np
 import pytest
 
 import oracle as O
-from paper_2511_16665_b200.engine import Engine
+from paper_2511_16665_b200.engine import INITS, MODELS, Engine
 
 pytestmark = pytest.mark.gpu
 
 V = 4096
+# config 4 at V = 152064: the Qwen2.5-32B shape truncated to 2 of its 64
+# layers (the discrete rejection-sampling logic does not depend on depth;
+# the full 64-layer model runs in tools/config4.py / bench configs)
+MODEL_32B_TRUNC = dict(MODELS["qwen2.5-32b"], layers=2)
+
+
+def _engine(model, max_slots, max_ctx):
+    if model == "32b-trunc":
+        return Engine(MODEL_32B_TRUNC, max_slots=max_slots, max_ctx=max_ctx, init=INITS["qwen2.5-32b"])
+    return Engine(model, max_slots=max_slots, max_ctx=max_ctx)
 
 
 def _uniforms(seed, stream, n):
@@ -21,14 +31,16 @@ def _uniforms(seed, stream, n):
     return [r.uniform01() for _ in range(n)]
 
 
-@pytest.mark.parametrize("D,temperature", [(4, 0.9), (3, 1.0), (6, 0.7)])
-def test_stochastic_step_oracle_in_the_loop(D, temperature):
+@pytest.mark.parametrize("model,D,temperature", [("tiny", 4, 0.9), ("tiny", 3, 1.0), ("tiny", 6, 0.7),
+                                                 ("32b-trunc", 4, 0.9), ("32b-trunc", 6, 0.9)])
+def test_stochastic_step_oracle_in_the_loop(model, D, temperature):
     L = O.orc()
     L.orc_build_sampled_chain.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                           C.c_void_p]
     L.orc_verify_stochastic.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_int,
                                         C.c_void_p, C.c_void_p, C.c_void_p]
-    eng = Engine("tiny", max_slots=4, max_ctx=512)
+    eng = _engine(model, 4, 512)
+    V = eng.vocab
     eng.set_debug(True)
     rng = np.random.default_rng(11)
     prompts = [rng.integers(2, V, 16).tolist() for _ in range(4)]
@@ -134,4 +146,64 @@ def test_stochastic_first_token_marginal_is_target():
         p = p0[tok]
         sigma = np.sqrt(p * (1 - p) / n)
         assert abs(counts[tok] / n - p) < 5 * sigma + 1e-3, (int(tok), counts[tok] / n, p)
+    eng.close()
+
+
+def _blocked_prefix(p, nthreads=256):
+    """The GPU fast path's blocked prefix sums (inverse_cdf_block, stochastic.cu):
+    contiguous segments per thread, segment sums exclusive-scanned in order."""
+    V = len(p)
+    per = (V + nthreads - 1) // nthreads
+    seg = [float(np.cumsum(p[a:a + per])[-1]) if a < V else 0.0 for a in range(0, per * nthreads, per)]
+    out = np.zeros(V)
+    c = 0.0
+    for j in range(nthreads):
+        a = j * per
+        cum = c
+        for t in range(a, min(V, a + per)):
+            cum += p[t]
+            out[t] = cum
+        c += seg[j]
+    return out
+
+
+def _ref_pick(p, u):
+    """inverse_cdf_pick (token_model.hpp:83-91): sequential cumulative sum."""
+    cum = 0.0
+    for t in range(len(p) - 1):
+        cum += p[t]
+        if u < cum:
+            return t
+    return len(p) - 1
+
+
+@pytest.mark.parametrize("model", ["tiny", "32b-trunc"])
+def test_inverse_cdf_exact_at_cdf_boundaries(model):
+    """The chain draw equals the reference's sequential inverse CDF even when
+    u sits exactly on, or within rounding of, a CDF boundary (the blocked scan
+    and the sequential sum round differently there)."""
+    eng = _engine(model, 1, 256)
+    V = eng.vocab
+    eng.set_debug(True)
+    prompt = np.random.default_rng(7).integers(2, V, 12).tolist()
+    eng.prefill([0], [prompt])
+    eng.sd_step_stochastic(1, 1.0, [0], np.full((1, 3), 0.5))
+    q0 = eng.debug_expansions(0)[0][1]  # drafter root row (fp64) the chain draw used
+    seq = np.cumsum(q0)  # numpy accumulate: the reference's sequential order
+    blk = _blocked_prefix(q0)
+    us = []
+    top = np.argsort(-q0)[:6]
+    for t in top:  # exact boundaries of the heaviest tokens and their neighbours
+        us += [float(seq[t]), float(np.nextafter(seq[t], 0.0)), float(np.nextafter(seq[t], 1.0))]
+    diff = np.nonzero(seq[:-1] != blk[:-1])[0]
+    for t in diff[:6]:  # boundaries where the blocked and sequential sums disagree
+        lo, hi = sorted((float(seq[t]), float(blk[t])))
+        us += [lo, hi, (lo + hi) / 2]
+    us = [u for u in us if 0.0 <= u < 1.0]
+    assert us
+    for u in us:
+        eng.release(0)
+        eng.prefill([0], [prompt])
+        _, chains, _ = eng.sd_step_stochastic(1, 1.0, [0], np.array([[u, 0.5, 0.5]]))
+        assert chains[0][0] == _ref_pick(q0, u), (u, chains[0][0])
     eng.close()
