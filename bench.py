@@ -43,12 +43,60 @@ THRESHOLDS = [1, 2, 8, 16]
 
 
 def peaks():
+    """(HBM GB/s, dense bf16 TFLOP/s burst, sustained, source): the driver-measured
+    MEASURED_PEAKS.json, else the B200_PROFILING.md fallback."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+        return (float(p["hbm_gbs"]), float(p["bf16_tflops"]),
+                float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured")
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, 1373.0, "fallback"
+
+
+def model_costs(m):
+    """Algorithmic bytes / flops of the Qwen-shaped target and the EAGLE drafter
+    (SURVEY.md 8(d)): weights streamed per forward (the embedding is a row
+    gather), KV bytes per token, matmul flops per row."""
+    d, L, H, KV, hd, F, V = (m[k] for k in ("hidden", "layers", "heads", "kv_heads", "head_dim", "ffn", "vocab"))
+    nqkv = (H + 2 * KV) * hd
+    mat_layer = d * nqkv + H * hd * d + 2 * d * F + F * d
+    layer_b = (mat_layer + nqkv + 2 * d) * 2
+    return dict(
+        target_w=L * layer_b + V * d * 2 + d * 2,
+        drafter_w=(2 * d * d) * 2 + layer_b + V * d * 2 + d * 2,
+        kv_tok=L * 2 * KV * hd * 2, dkv_tok=2 * KV * hd * 2,
+        fl_row_t=2 * (L * mat_layer + V * d), fl_row_d=2 * (2 * d * d + mat_layer + V * d),
+        attn_fl=4 * H * hd, layers=L)
+
+
+def step_roofline(m, b, ctx, strategy, bw_gbs, tflops):
+    """t_roof of one engine step = sum over phases of max(bytes / BW, flops /
+    peak) (SURVEY.md 8(d)). strategy None = plain AR decode (R = b rows);
+    else (D, k, T): D drafter levels (level 1: b LM rows, level l: b *
+    min(T, k^(l-1)) rows) + one verify forward over b (T + 1) rows."""
+    c = model_costs(m)
+    bw, pk = bw_gbs * 1e9, tflops * 1e12
+
+    def phase(w, rows, kv_read, kv_write, attn_rows_keys, fl_row, layers):
+        byts = w + kv_read + kv_write
+        fl = rows * fl_row + c["attn_fl"] * layers * attn_rows_keys
+        return max(byts / bw, fl / pk), byts, fl
+
+    if strategy is None:
+        t, byts, fl = phase(c["target_w"], b, b * ctx * c["kv_tok"], b * c["kv_tok"], b * (ctx + 1), c["fl_row_t"],
+                            c["layers"])
+        return dict(t_roof_ms=t * 1e3, bytes=byts, flops=fl)
+    D, k, T = strategy
+    tot_t, tot_b, tot_f = 0.0, 0.0, 0.0
+    for lv in range(1, D + 1):
+        rows = b if lv == 1 else b * min(T, k ** (lv - 1))
+        t, byts, fl = phase(c["drafter_w"], rows, b * ctx * c["dkv_tok"], rows * c["dkv_tok"], rows * (ctx + lv), c["fl_row_d"], 1)
+        tot_t, tot_b, tot_f = tot_t + t, tot_b + byts, tot_f + fl
+    R = b * (T + 1)
+    t, byts, fl = phase(c["target_w"], R, b * ctx * c["kv_tok"], R * c["kv_tok"], R * (ctx + (T + 1) / 2),
+                        c["fl_row_t"], c["layers"])
+    return dict(t_roof_ms=(tot_t + t) * 1e3, bytes=tot_b + byts, flops=tot_f + fl)
 
 
 def response_lengths(n, mu, sigma, max_len, seed):
@@ -180,6 +228,59 @@ def cpu_rollout_sample(model_name, n_threads, gen_tokens, prompt_len, strategy, 
                 mean_accept=float(np.mean(list(acc[:max(steps, 1)]))))
 
 
+def cpu_rows(model_name, prompt_len, strategy):
+    """CPU baseline: the oracle port of the reference hot path
+    (C restatement of spec_generate over the neural CPU leaves) on this host.
+    b = 1 with 1 thread and with all cores; b in {8, 32} with all cores, each
+    request run to one SD step (max_len 2) as the reference's per-request loop
+    does (rollout.hpp:191 is sequential over requests)."""
+    import ctypes as C
+
+    import oracle as O
+    from paper_2511_16665_b200.engine import INITS, MODELS
+    m, ini = MODELS[model_name], INITS[model_name]
+    L = O.orc()
+    cfg = O.ModelCfg(m["vocab"], m["hidden"], m["layers"], m["heads"], m["kv_heads"], m["head_dim"], m["ffn"],
+                     m["qkv_bias"], m["rope_theta"], m["rms_eps"], prompt_len + 64)
+    icfg = O.InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"],
+                     ini["fc_noise"])
+    cores = os.cpu_count() or 1
+    om = L.orc_model_create(C.byref(cfg), C.byref(icfg), cores)
+    L.orc_neural_spec_generate.argtypes = [C.c_void_p] * 11
+    L.orc_model_set_threads.argtypes = [C.c_void_p, C.c_int]
+    rng = np.random.default_rng(0)
+
+    def run(b, threads):
+        L.orc_model_set_threads(om, threads)
+        toks, t0 = 0, time.time()
+        for _ in range(b):
+            prompt = (C.c_int32 * prompt_len)(*rng.integers(2, m["vocab"], prompt_len).tolist())
+            out = (C.c_int32 * 64)()
+            n = C.c_int()
+            acc = (C.c_int32 * 64)()
+            L.orc_neural_spec_generate(om, prompt, prompt_len, 2, C.byref(O.Strategy(*strategy)), out, C.byref(n),
+                                       acc, None, None, 64)
+            toks += n.value
+        dt = time.time() - t0
+        return {"b": b, "threads": threads, "tokens": toks, "seconds": round(dt, 2),
+                "tokens_per_s": round(toks / dt, 4)}
+
+    rows = [run(1, 1), run(1, cores), run(8, cores), run(32, cores)]
+    L.orc_model_destroy(om)
+    return rows, cores
+
+
+def lscpu_model():
+    try:
+        o = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in o.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def run_reference(a):
     world, rank, local, pg = dist_setup(a.gpus)
     if rank != 0:
@@ -267,12 +368,116 @@ def kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind):
     return out
 
 
+# Per-bucket fixed-step rows (the 2x bar is about b < 32): the reference
+# default arms of each BEG-MAB bucket (T = 64 / 48 / 32 / 16 for buckets
+# [1,1] / [2,7] / [8,15] / [16,32], experiment.hpp:87-95, beg_mab.hpp:95-105).
+BUCKET_ROWS = [(1, [(10, 8, 64), (6, 8, 64)]), (4, [(10, 8, 48), (6, 8, 48)]), (8, [(10, 8, 32), (6, 8, 32)]),
+               (16, [(10, 8, 16), (6, 8, 16)]), (31, [(10, 8, 16), (6, 8, 16)])]
+
+
+def bucket_rows(eng, a, peak_gbs, peak_tf_sus):
+    """b requests: prefill (prompt a.prompt), `warm_ar` untimed plain steps
+    (generated context), then `steps` timed AR steps and, per default arm, 2
+    warm SD steps (drafter catch-up + graph capture) and `steps` timed SD
+    steps. Tokens/s are device time (CUDA events per step); the step
+    roofline is t_roof / t_measured."""
+    rows = []
+    V = eng.vocab
+    steps, warm_ar = a.bucket_steps, a.bucket_ctx
+    for b, arms in BUCKET_ROWS:
+        rng = np.random.default_rng(77 + b)
+        prompts = [rng.integers(2, V, a.prompt).tolist() for _ in range(b)]
+        slots = list(range(b))
+        for s in slots:
+            eng.release(s)
+        eng.prefill(slots, prompts)
+        for _ in range(warm_ar):
+            eng.ar_step(slots)
+        ctx = a.prompt - 1 + warm_ar
+        ar_ms = 0.0
+        for _ in range(steps):
+            ar_ms += eng.ar_step(slots)[1]
+        ctx += steps
+        ar_tps = b * steps / (ar_ms / 1e3)
+        ar_roof = step_roofline(eng.model, b, ctx, None, peak_gbs, peak_tf_sus)["t_roof_ms"]
+        row = {"b": b, "ctx": ctx, "ar_tok_s": round(ar_tps, 1), "ar_ms_per_step": round(ar_ms / steps, 3),
+               "ar_step_roofline_frac": round(ar_roof / (ar_ms / steps), 3), "arms": []}
+        for arm in arms:
+            for _ in range(2):
+                eng.sd_step(arm, slots, want_tree=False)
+            ms, emitted, acc = 0.0, 0, 0
+            L0 = [eng.slot_len(s) for s in slots]
+            for _ in range(steps):
+                r = eng.sd_step(arm, slots, want_tree=False)
+                ms += r.elapsed_ms
+                emitted += int(r.accept_len.sum()) + b
+                acc += int(r.accept_len.sum())
+            ctx_sd = int(np.mean(L0))
+            roof = step_roofline(eng.model, b, ctx_sd, arm, peak_gbs, peak_tf_sus)["t_roof_ms"]
+            tps = emitted / (ms / 1e3)
+            row["arms"].append({"strategy": list(arm), "sd_tok_s": round(tps, 1), "speedup_vs_ar": round(tps / ar_tps, 3),
+                                "ms_per_step": round(ms / steps, 3), "mean_accept_len": round(acc / (b * steps), 3),
+                                "step_roofline_frac": round(roof / (ms / steps), 3), "ctx": ctx_sd})
+        row["best_speedup_vs_ar"] = max(x["speedup_vs_ar"] for x in row["arms"])
+        rows.append(row)
+        print(f"[bench] bucket b={b}: {row}", file=sys.stderr, flush=True)
+    return rows
+
+
+GEMM_SITES = [(1, "qkv (+bias, RoPE, KV write)"), (5, "o-proj (+residual)"), (0, "gate_up (+SwiGLU)"),
+              (2, "down (+residual)")]
+
+
+def gemm_class(eng, M, bound, peak_gbs, peak_tf):
+    """The dominant kernel class over one target forward at M rows: every
+    tcgen05 GEMM site of a layer (each timed over successive layers' weights,
+    tlt_probe_kernel, CUDA events on the engine stream) x layers + the LM
+    head with the fused top-1 epilogue. achieved = summed algorithmic bytes
+    (or flops) / summed launch time."""
+    L = eng.model["layers"]
+    t = byts = fl = 0.0
+    parts = []
+    for kind, name in GEMM_SITES:
+        ms, b_, f_ = eng.probe_kernel(kind, M, 56)
+        t, byts, fl = t + ms * L, byts + b_ * L, fl + f_ * L
+        parts.append({"site": name, "avg_launch_us": round(ms * 1e3, 2), "bytes": int(b_), "flops": int(f_)})
+    ms, b_, f_ = eng.probe_kernel(4, M, 8)
+    t, byts, fl = t + ms, byts + b_, fl + f_
+    parts.append({"site": "LM head (+fused top-1)", "avg_launch_us": round(ms * 1e3, 2), "bytes": int(b_),
+                  "flops": int(f_)})
+    if bound == "hbm":
+        ach = byts / (t * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
+                "frac": round(ach / peak_gbs, 3), "traffic": None, "M": M, "forward_gemm_ms": round(t, 3),
+                "algorithmic_bytes": int(byts), "sites": parts}
+    ach = fl / (t * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": round(ach / peak_tf, 3), "traffic": None, "M": M, "forward_gemm_ms": round(t, 3),
+            "flops": int(fl), "sites": parts}
+
+
+def token_match(sd_tokens, ar_tokens):
+    """Greedy SD is lossless vs plain decode (spec_decode.hpp:349-350): compare
+    the SD rollout's tokens with the AR rollout's on the same workload."""
+    same, tot, first_div, identical = 0, 0, [], 0
+    for s, r in zip(sd_tokens, ar_tokens):
+        n = min(len(s), len(r))
+        k = next((j for j in range(n) if s[j] != r[j]), n)
+        same += k
+        tot += max(len(s), len(r))
+        identical += int(s == r)
+        if s != r:
+            first_div.append(k)
+    return {"requests": len(sd_tokens), "identical_requests": identical,
+            "prefix_match_rate": round(same / max(1, tot), 6), "first_divergence_positions": first_div[:16]}
+
+
 def run_ours(a):
     world, rank, local, pg = dist_setup(a.gpus)
     import torch
     torch.cuda.set_device(local)
     from paper_2511_16665_b200.engine import Engine, Mab, merge_bandit_stats
-    peak_gbs, peak_tf, peak_kind = peaks()
+    peak_gbs, peak_tf, peak_tf_sus, peak_kind = peaks()
     n = a.requests
     max_ctx = a.prompt + a.max_len + 8
     eng = Engine(a.model, max_slots=n, max_ctx=max_ctx, device=local)
@@ -327,19 +532,28 @@ def run_ours(a):
     ar = rollout(a.warmup, enable_sd=False) if a.ar_baseline else None
     ar_tok_s = ar["emitted_total"] / (ar["device_ms"] / 1e3) if ar else None
     sd_same = res[0] if res else None
+    match = token_match(sd_same["tokens"], ar["tokens"]) if (ar and sd_same) else None
     out = None
     if rank == 0:
         print("[bench] probes", file=sys.stderr, flush=True)
         kernels = kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind)
-        roof = kernels[0]
+        roof = gemm_class(eng, 17, "hbm", peak_gbs, peak_tf)
+        roof["kernel"] = ("tcgen05 GEMM class, one long-tail verify forward (b=1, T=16: M=17): qkv+o+gate_up+down "
+                          "x layers + LM head/top-1")
+        roof_tc = gemm_class(eng, 527, "tensor", peak_gbs, peak_tf)
+        roof_tc["kernel"] = "tcgen05 GEMM class, one verify forward at b=31, T=16 (M=527)"
+        buckets = bucket_rows(eng, a, peak_gbs, peak_tf_sus) if a.bucket_steps > 0 else None
         cpu = None
-        if a.cpu_gen > 0:
-            threads = os.cpu_count() or 1
-            c = cpu_rollout_sample(a.model, threads, a.cpu_gen, a.cpu_prompt, (6, 8, 16))
-            cpu = {"value": round(c["tokens"] / c["seconds"], 4), "unit": "tokens/s", "cores": threads, "kind": "port",
-                   "sample": f"{a.model} CPU oracle port (C restatement of spec_generate + neural leaves), 1 request, "
-                             f"prompt {a.cpu_prompt}, {a.cpu_gen} tokens, greedy tree SD (6,8,16); "
-                             f"{c['seconds']:.1f}s"}
+        if a.cpu_rows:
+            rows_c, cores = cpu_rows(a.model, a.cpu_prompt, (6, 8, 16))
+            allc = [r for r in rows_c if r["threads"] == cores]
+            tps = sum(r["tokens"] for r in allc) / sum(r["seconds"] for r in allc)
+            cpu = {"value": round(tps, 4), "unit": "tokens/s", "cores": cores, "kind": "port",
+                   "cpu_model": lscpu_model(), "rows": rows_c,
+                   "sample": f"{a.model} CPU oracle port (C restatement of spec_generate over the neural leaves), "
+                             f"prompt {a.cpu_prompt}, greedy tree SD (6,8,16), each request to its first SD step "
+                             f"(max_len 2); rows b=1 at 1 thread and all cores, b=8 and b=32 at all cores; value = "
+                             f"all-core tokens / all-core seconds"}
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(mx[0] * 1e3 / max(1, a.steps), 2), "higher_is_better": True,
@@ -359,6 +573,8 @@ def run_ours(a):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": roof,
+            "roofline_tensor_class": roof_tc,
+            "per_bucket": buckets,
             "kernels": kernels,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
@@ -368,7 +584,8 @@ def run_ours(a):
                                   "sd_rollout_same_workload": round(sd_same["emitted_total"] /
                                                                     (sd_same["device_ms"] / 1e3), 2),
                                   "speedup": round((sd_same["emitted_total"] / (sd_same["device_ms"] / 1e3)) /
-                                                   ar_tok_s, 3)}
+                                                   ar_tok_s, 3),
+                                  "token_match_sd_vs_ar": match}
         print(json.dumps(out), flush=True)
     eng.close()
     if pg is not None:
@@ -391,6 +608,9 @@ def main():
     ap.add_argument("--ar-baseline", type=int, default=1)
     ap.add_argument("--cpu-gen", type=int, default=8)
     ap.add_argument("--cpu-prompt", type=int, default=8)
+    ap.add_argument("--cpu-rows", type=int, default=1)
+    ap.add_argument("--bucket-steps", type=int, default=12)
+    ap.add_argument("--bucket-ctx", type=int, default=400, help="untimed plain steps before the bucket rows")
     a = ap.parse_args()
     if a.impl == "reference":
         run_reference(a)

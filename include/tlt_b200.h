@@ -143,6 +143,37 @@ typedef struct {
  * (batch bucket, strategy) when a pool is built. `tree` may be NULL. */
 TLT_API int tlt_sd_step(tlt_engine* e, const tlt_strategy* s, int b, const int32_t* slot_ids, tlt_tree_out* tree,
                         tlt_accept_out* out);
+/* ---- split boundary: propose and verify as separate calls ---------------- */
+/* The reference's drafter seam is DraftPlanner (spec_decode.hpp:319-341),
+ * a (ctx, strategy, rng) -> DraftTree function consumed by spec_generate,
+ * and its target side is verify_greedy(target, ctx, tree) (:245-268). These
+ * two calls back that seam; tlt_sd_step is their fused, graph-replayed form.
+ *
+ * tlt_draft: build_draft_tree (spec_decode.hpp:111-197) with the EAGLE
+ * drafter for each request; writes the tree (rank order, parent -1 = root)
+ * and commits nothing to the target (the drafter's own KV of the committed
+ * positions is written; drafting twice is idempotent). */
+TLT_API int tlt_draft(tlt_engine* e, const tlt_strategy* s, int b, const int32_t* slot_ids, tlt_tree_out* tree);
+/* A caller-supplied tree (reference DraftTree, spec_decode.hpp:50-70) per
+ * request: nodes in rank order, each parent index < its own (-1 = root).
+ * Arrays are [b][stride]; probs / path_probs may be NULL (reported as 1). */
+typedef struct {
+    const int32_t* tokens;
+    const int32_t* parents;
+    const double* probs;
+    const double* path_probs;
+    const int32_t* n_nodes; /* [b], 0 <= n <= stride */
+    int32_t stride;         /* <= 128 nodes per request, depth <= 15 */
+} tlt_tree_in;
+/* verify_greedy (spec_decode.hpp:245-268) of one tree per request in one
+ * tree-masked target forward, then the KV commit of the accepted branch.
+ * tree == NULL verifies the engine's own last tlt_draft of exactly these
+ * slots (device-resident, no upload); otherwise the host tree is uploaded.
+ * `out` arrays are [b][stride] (stride = tree->stride, or the drafted
+ * strategy's draft_depth when tree == NULL). */
+TLT_API int tlt_verify_accept_commit(tlt_engine* e, int b, const int32_t* slot_ids, const tlt_tree_in* tree,
+                                     tlt_accept_out* out);
+
 /* Stochastic linear-chain SD step: build_sampled_chain (:202-223) +
  * verify_stochastic (:275-313), temperature t > 0. Uniforms are the
  * reference RngStream draws (rng.hpp:54-56), host-generated per request in

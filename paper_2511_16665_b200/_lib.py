@@ -69,8 +69,8 @@ class TltError(RuntimeError):
 
 
 def check(rc: int, engine=None) -> int:
-    if rc < 0 or rc in (1, 2, 3, 4, 5) and False:
-        pass
+    """Raise on a negative return of the kernel-level dev entry points (which
+    return a count, or -1 with tlt_last_error set); pass the count through."""
     if rc < 0:
         raise TltError(last_error(engine))
     return rc

@@ -97,6 +97,17 @@ TLT_API int tlt_sd_step(tlt_engine* e, const tlt_strategy* s, int b, const int32
     return guard([&] { e->e->sd_step(*s, b, slot_ids, tree, out); });
 }
 
+TLT_API int tlt_draft(tlt_engine* e, const tlt_strategy* s, int b, const int32_t* slot_ids, tlt_tree_out* tree) {
+    if (!e || !s || !slot_ids) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { e->e->draft(*s, b, slot_ids, tree); });
+}
+
+TLT_API int tlt_verify_accept_commit(tlt_engine* e, int b, const int32_t* slot_ids, const tlt_tree_in* tree,
+                                     tlt_accept_out* out) {
+    if (!e || !slot_ids) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] { e->e->verify_tree(b, slot_ids, tree, out); });
+}
+
 TLT_API int tlt_sd_step_chain(tlt_engine* e, int draft_depth, int b, const int32_t* slot_ids, const int32_t* chains,
                               const int32_t* chain_lens, tlt_accept_out* out) {
     if (!e || !slot_ids || !chains || !chain_lens) return fail(TLT_ERR_STATE, "null argument");

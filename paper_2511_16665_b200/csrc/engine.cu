@@ -672,6 +672,7 @@ void Engine::upload_rows_host(const std::vector<int>& tok, const std::vector<int
 // the drafter over the same positions with inputs (f_{p-1}, e(x_p)). The last
 // prompt token is the first step's root.
 void Engine::prefill(int b, const int32_t* slots, const int32_t* lens, const int32_t* tokens) {
+    draft_slots_.clear();
     std::vector<int> off(b + 1, 0);
     for (int i = 0; i < b; ++i) {
         if (slots[i] < 0 || slots[i] >= cfg.max_slots) throw ConfigErr("slot_ids", "slot out of range");
@@ -987,7 +988,7 @@ float Engine::probe_attention(int b, int ctx, int rpr, int iters, double* bytes)
 // draft (D levels) -> tree final -> verify forward -> argmax -> accept ->
 // commit. All shapes static in (b_hi, D, k, T); per-step data lives on the
 // device (StepIn uploaded first), so the sequence is graph-capturable.
-void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real) {
+void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real, bool verify) {
     (void)b_real;
     const int d = cfg.hidden, V = cfg.vocab, D1 = D + 1;
     CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
@@ -1060,7 +1061,8 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
         d2d(dbg_arena_, arena_, sizeof(Cand) * (size_t)b_hi * arena_cap_);
         d2d(dbg_node_, row_node_, sizeof(int) * (size_t)(base[D] + b_hi * Fd[D]));
     }
-    verify_accept_commit(b_hi, T, dbg, b_real);
+    if (verify) verify_accept_commit(b_hi, T, dbg, b_real);
+    else tree_to_host(b_hi, T);
 }
 
 // Target verify over root + the final tree (rows written by k_tree_final),
@@ -1121,6 +1123,13 @@ void Engine::verify_accept_commit(int b_hi, int T, bool dbg, int b_real) {
     d2h(ho_.bonus, bonus_, sizeof(int) * b_hi);
     d2h(ho_.acc_tok, acc_tok_, sizeof(int) * b_hi * kMaxD);
     d2h(ho_.acc_nodes, acc_nodes_, sizeof(int) * b_hi * kMaxD);
+    tree_to_host(b_hi, T);
+}
+
+void Engine::tree_to_host(int b_hi, int T) {
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st_));
+    };
     d2h(ho_.tree_tok, tree_tok_, sizeof(int) * b_hi * T);
     d2h(ho_.tree_par, tree_par_, sizeof(int) * b_hi * T);
     d2h(ho_.tree_dep, tree_dep_, sizeof(int) * b_hi * T);
@@ -1129,7 +1138,7 @@ void Engine::verify_accept_commit(int b_hi, int T, bool dbg, int b_real) {
     d2h(ho_.tree_n, tree_n_, sizeof(int) * b_hi);
 }
 
-float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out) {
+int Engine::prepare_tree_step(const tlt_strategy& s, int b, const int32_t* slots, float* catchup_ms) {
     const int D = s.draft_depth, k = s.top_k, T = s.tokens_to_verify;
     if (D < 1) throw ConfigErr("draft_depth", "must be >= 1");
     if (k < 1) throw ConfigErr("top_k", "must be >= 1");
@@ -1155,12 +1164,12 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
     }
     // drafter catch-up for requests whose pending rows exceed the graph stride
     // (after plain-decode steps); its device time is part of the step's
-    float catchup_ms = 0.f;
+    *catchup_ms = 0.f;
     {
         std::vector<int32_t> need;
         for (int i = 0; i < b; ++i)
             if (lt_[slots[i]] - ld_[slots[i]] + 1 > D + 1) need.push_back(slots[i]);
-        if (!need.empty()) catchup_ms = catchup_drafter((int)need.size(), need.data());
+        if (!need.empty()) *catchup_ms = catchup_drafter((int)need.size(), need.data());
     }
     const int b_hi = bucket_hi_for(b, T);
     for (int i = 0; i < b_hi; ++i) {
@@ -1174,6 +1183,45 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
             h_step_[i] = StepIn{-1, 0, 0, 0};
         }
     }
+    return b_hi;
+}
+
+// Step results (pinned staging) -> caller arrays ([b][stride] accept arrays,
+// [b][T] tree arrays); host mirrors are updated by the caller.
+void Engine::copy_step_out(int b, const int32_t* slots, int T, int stride, tlt_tree_out* tree, tlt_accept_out* out) {
+    for (int i = 0; i < b; ++i) {
+        const int sl = slots[i];
+        if (out) {
+            const int a = ho_.acc_len[i];
+            if (out->accept_len) out->accept_len[i] = a;
+            if (out->bonus) out->bonus[i] = ho_.bonus[i];
+            for (int j = 0; j < a && j < stride; ++j) {
+                if (out->accepted) out->accepted[(size_t)i * stride + j] = ho_.acc_tok[(size_t)i * kMaxD + j];
+                if (out->nodes) out->nodes[(size_t)i * stride + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
+                if (out->kv_src) out->kv_src[(size_t)i * stride + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
+            }
+            if (out->kv_len) out->kv_len[i] = lt_[sl] + 1 + a;
+        }
+        if (tree) {
+            const int n = ho_.tree_n[i];
+            if (tree->n_nodes) tree->n_nodes[i] = n;
+            for (int t = 0; t < n; ++t) {
+                const size_t o = (size_t)i * T + t;
+                if (tree->tokens) tree->tokens[o] = ho_.tree_tok[o];
+                if (tree->parents) tree->parents[o] = ho_.tree_par[o];
+                if (tree->depths) tree->depths[o] = ho_.tree_dep[o];
+                if (tree->probs) tree->probs[o] = ho_.tree_prob[o];
+                if (tree->path_probs) tree->path_probs[o] = ho_.tree_pp[o];
+            }
+        }
+    }
+}
+
+float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out) {
+    const int D = s.draft_depth, k = s.top_k, T = s.tokens_to_verify;
+    draft_slots_.clear();
+    float catchup_ms = 0.f;
+    const int b_hi = prepare_tree_step(s, b, slots, &catchup_ms);
     const bool dbg = debug_;
     if (dbg) ensure_debug_buffers(b_hi, D, k, T);  // may drop debug graphs: before the lookup
     CUDA_CHECK(cudaEventRecord(ev0_, st_));
@@ -1222,34 +1270,144 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
         CUDA_CHECK(cudaGraphDestroy(g));
         graphs_[key] = {ex, launches_in_seq_};
     }
-    // outputs + host mirrors
+    copy_step_out(b, slots, T, D, tree, out);
+    for (int i = 0; i < b; ++i) {  // host mirrors
+        const int sl = slots[i];
+        ld_[sl] = lt_[sl] + 1;
+        lt_[sl] = lt_[sl] + 1 + ho_.acc_len[i];
+    }
+    if (out && out->elapsed_ms) out->elapsed_ms[0] = ms;
+    return ms;
+}
+
+// Split boundary, propose half: the drafter levels + tree selection of the
+// fused step (sd_device_sequence without the verify tail), eager. Nothing is
+// committed to the target; the drafter's KV of the pending committed rows is
+// (idempotently) rewritten. The device tree stays resident for
+// verify_tree(tree == nullptr).
+float Engine::draft(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree) {
+    const int D = s.draft_depth, k = s.top_k, T = s.tokens_to_verify;
+    draft_slots_.clear();
+    float catchup_ms = 0.f;
+    const int b_hi = prepare_tree_step(s, b, slots, &catchup_ms);
+    CUDA_CHECK(cudaEventRecord(ev0_, st_));
+    launches_in_seq_ = 0;
+    sd_device_sequence(b_hi, D, k, T, false, b, /*verify=*/false);
+    launches += launches_in_seq_;
+    CUDA_CHECK(cudaEventRecord(ev1_, st_));
+    CUDA_CHECK(cudaEventSynchronize(ev1_));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    copy_step_out(b, slots, T, 0, tree, nullptr);
+    draft_slots_.assign(slots, slots + b);
+    draft_lt_.resize(b);
+    for (int i = 0; i < b; ++i) draft_lt_[i] = lt_[slots[i]];
+    draft_T_ = T;
+    draft_D_ = D;
+    return ms + catchup_ms;
+}
+
+// Split boundary, verify half: verify_greedy + KV commit of the engine's
+// own last draft (tree == nullptr) or of caller trees, uploaded into the
+// tree arena as each request's kept list (arena index = rank) so k_tree_final
+// builds the verify rows / ancestor masks exactly as for a drafted tree.
+float Engine::verify_tree(int b, const int32_t* slots, const tlt_tree_in* tree, tlt_accept_out* out) {
+    if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");
+    // did the drafter (tlt_draft) process these slots at their current length?
+    bool drafted = (int)draft_slots_.size() == b;
+    for (int i = 0; drafted && i < b; ++i) drafted = draft_slots_[i] == slots[i] && draft_lt_[i] == lt_[slots[i]];
+    if (!tree && !drafted) throw ConfigErr("tree", "no tlt_draft of these slots at their current length");
+    const int T = tree ? tree->stride : draft_T_;
+    const int stride = tree ? tree->stride : draft_D_;
+    if (T < 1 || T > kMaxT) throw ConfigErr("tree.stride", "must be in [1, 128]");
     for (int i = 0; i < b; ++i) {
         const int sl = slots[i];
-        const int a = ho_.acc_len[i];
-        if (out) {
-            if (out->accept_len) out->accept_len[i] = a;
-            if (out->bonus) out->bonus[i] = ho_.bonus[i];
-            for (int j = 0; j < a; ++j) {
-                if (out->accepted) out->accepted[(size_t)i * D + j] = ho_.acc_tok[(size_t)i * kMaxD + j];
-                if (out->nodes) out->nodes[(size_t)i * D + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
-                if (out->kv_src) out->kv_src[(size_t)i * D + j] = ho_.acc_nodes[(size_t)i * kMaxD + j];
+        if (sl < 0 || sl >= cfg.max_slots || !live_[sl]) throw ConfigErr("slot_ids", "slot not prefilled");
+        if (lt_[sl] + T + 2 > cap_ - 1) throw ConfigErr("max_ctx", "context full");
+        h_step_[i] = StepIn{sl, lt_[sl], ld_[sl], 0};
+    }
+    std::vector<Cand> cand;
+    std::vector<int> kept, kept_n;
+    if (tree) {
+        if (!tree->tokens || !tree->parents || !tree->n_nodes) throw ConfigErr("tree", "null node arrays");
+        cand.resize((size_t)b * T);
+        kept.resize((size_t)b * T);
+        kept_n.resize(b);
+        for (int i = 0; i < b; ++i) {
+            const int n = tree->n_nodes[i];
+            if (n < 0 || n > T) throw ConfigErr("tree.n_nodes", "must be in [0, stride]");
+            kept_n[i] = n;
+            for (int j = 0; j < T; ++j) {
+                const size_t o = (size_t)i * T + j;
+                Cand c{};
+                c.row = c.eslot = -1;
+                c.birth = j;
+                kept[o] = j;
+                if (j < n) {
+                    c.token = tree->tokens[o];
+                    c.parent = tree->parents[o];
+                    if (c.token < 0 || c.token >= cfg.vocab) throw ConfigErr("tree.tokens", "token out of range");
+                    if (c.parent < -1 || c.parent >= j)
+                        throw ConfigErr("tree.parents", "parent must precede its child (rank order)");
+                    c.depth = c.parent < 0 ? 1 : cand[(size_t)i * T + c.parent].depth + 1;
+                    if (c.depth > kMaxD - 1) throw ConfigErr("tree", "depth exceeds 15");
+                    c.prob = tree->probs ? tree->probs[o] : 1.0;
+                    c.pp = tree->path_probs ? tree->path_probs[o] : 1.0;
+                }
+                cand[o] = c;
             }
-            if (out->kv_len) out->kv_len[i] = lt_[sl] + 1 + a;
         }
-        if (tree) {
-            const int n = ho_.tree_n[i];
-            if (tree->n_nodes) tree->n_nodes[i] = n;
-            for (int t = 0; t < n; ++t) {
-                const size_t o = (size_t)i * T + t;
-                if (tree->tokens) tree->tokens[o] = ho_.tree_tok[o];
-                if (tree->parents) tree->parents[o] = ho_.tree_par[o];
-                if (tree->depths) tree->depths[o] = ho_.tree_dep[o];
-                if (tree->probs) tree->probs[o] = ho_.tree_prob[o];
-                if (tree->path_probs) tree->path_probs[o] = ho_.tree_pp[o];
-            }
-        }
-        ld_[sl] = lt_[sl] + 1;
-        lt_[sl] = lt_[sl] + 1 + a;
+    }
+    draft_slots_.clear();
+    CUDA_CHECK(cudaEventRecord(ev0_, st_));
+    launches_in_seq_ = 0;
+    CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b, cudaMemcpyHostToDevice, st_));
+    if (tree) {
+        CUDA_CHECK(cudaMemcpy2DAsync(arena_, sizeof(Cand) * arena_cap_, cand.data(), sizeof(Cand) * T,
+                                     sizeof(Cand) * T, b, cudaMemcpyHostToDevice, st_));
+        CUDA_CHECK(cudaMemcpyAsync(kept_, kept.data(), sizeof(int) * kept.size(), cudaMemcpyHostToDevice, st_));
+        CUDA_CHECK(cudaMemcpyAsync(kept_n_, kept_n.data(), sizeof(int) * b, cudaMemcpyHostToDevice, st_));
+        TreeParams tp{};
+        tp.step = d_step_;
+        tp.b = b;
+        tp.b_hi = b;
+        tp.D = kMaxD - 1;
+        tp.k = 1;
+        tp.T = T;
+        tp.arena = arena_;
+        tp.arena_cap = arena_cap_;
+        tp.arena_n = arena_n_;
+        tp.kept = kept_;
+        tp.kept_n = kept_n_;
+        tp.exp_n = exp_n_;
+        tp.done = done_;
+        tp.row_node = row_node_;
+        tp.root_row = root_row_;
+        tp.rows = drows_;
+        tp.tree_tok = tree_tok_;
+        tp.tree_par = tree_par_;
+        tp.tree_dep = tree_dep_;
+        tp.tree_prob = tree_prob_;
+        tp.tree_pp = tree_pp_;
+        tp.tree_n = tree_n_;
+        tp.vrows = vrows_;
+        tp.vg = vg_;
+        tp.tok_hist = tok_hist_;
+        tp.cap = cap_;
+        launch_tree_final(tp, st_);
+        count_launch();
+    }
+    verify_accept_commit(b, T, false, b);
+    launches += launches_in_seq_;
+    CUDA_CHECK(cudaEventRecord(ev1_, st_));
+    CUDA_CHECK(cudaEventSynchronize(ev1_));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    copy_step_out(b, slots, T, stride, nullptr, out);
+    for (int i = 0; i < b; ++i) {
+        const int sl = slots[i];
+        if (drafted) ld_[sl] = lt_[sl] + 1;  // the drafter's KV covers the committed root
+        lt_[sl] = lt_[sl] + 1 + ho_.acc_len[i];
     }
     if (out && out->elapsed_ms) out->elapsed_ms[0] = ms;
     return ms;
@@ -1264,6 +1422,7 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
 float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* chains, const int32_t* lens,
                             tlt_accept_out* out, float temperature, const double* uniforms) {
     if (D < 1 || D > kMaxD - 1 || D > kMaxT) throw ConfigErr("draft_depth", "out of range (1..15)");
+    draft_slots_.clear();
     const bool stoch = temperature != 0.f;
     if (stoch && !(temperature > 0.f)) throw ConfigErr("temperature", "must be > 0");
     if (stoch && !uniforms) throw ConfigErr("uniforms", "required");
@@ -1387,6 +1546,7 @@ void Engine::ar_device_sequence(int b_hi) {
 }
 
 float Engine::ar_step(int b, const int32_t* slots, int32_t* out_tokens) {
+    draft_slots_.clear();
     if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");
     for (int i = 0; i < b; ++i) {
         const int sl = slots[i];

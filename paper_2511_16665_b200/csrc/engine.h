@@ -58,6 +58,12 @@ public:
     // greedy tree SD step; returns device ms
     float sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree, tlt_accept_out* out);
     float ar_step(int b, const int32_t* slots, int32_t* out_tokens);
+    // split boundary (reference DraftPlanner seam, spec_decode.hpp:319-341):
+    // propose only (build_draft_tree with the EAGLE drafter, no commit) ...
+    float draft(const tlt_strategy& s, int b, const int32_t* slots, tlt_tree_out* tree);
+    // ... and verify_greedy + KV commit of a tree: the engine's own last draft
+    // (tree == nullptr, device-resident) or an arbitrary host tree
+    float verify_tree(int b, const int32_t* slots, const tlt_tree_in* tree, tlt_accept_out* out);
     // greedy verify of host-proposed chains (n-gram fallback drafter)
     // temperature > 0: verify_stochastic with one-hot q and uniforms [b][D+1]
     float sd_step_chain(int D, int b, const int32_t* slots, const int32_t* chains, const int32_t* lens,
@@ -118,7 +124,14 @@ private:
     float* topk_part_ = nullptr;  // EPI_TOPK partials [vocab tiles][R][2 + 2k]
     void scatter_features(const Rows& rw, int R, const bf16* feat);
     float catchup_drafter(int b, const int32_t* slots);
-    void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real);
+    void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real, bool verify = true);
+    void tree_to_host(int b_hi, int T);
+    int prepare_tree_step(const tlt_strategy& s, int b, const int32_t* slots, float* catchup_ms);
+    void copy_step_out(int b, const int32_t* slots, int T, int stride, tlt_tree_out* tree, tlt_accept_out* out);
+    // split boundary state: the last tlt_draft (slots, strategy, lt at draft time)
+    std::vector<int32_t> draft_slots_;
+    std::vector<int> draft_lt_;
+    int draft_T_ = 0, draft_D_ = 0;
     void verify_accept_commit(int b_hi, int T, bool dbg, int b_real);
     void stoch_verify_commit(int b_hi, int D, double temperature, bool dbg, int b_real, const double* q, int cur0);
     void ar_device_sequence(int b_hi);

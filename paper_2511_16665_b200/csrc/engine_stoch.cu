@@ -215,6 +215,7 @@ void Engine::ar_sample_sequence(int b_hi, double temperature) {
 // uniform per request (sample_token over target_next_dist).
 float Engine::ar_step_sampled(int b, const int32_t* slots, float temperature, const double* uniforms,
                               int32_t* out_tokens) {
+    draft_slots_.clear();
     if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");
     if (!(temperature >= 0.0f)) throw ConfigErr("temperature", "must be >= 0");
     for (int i = 0; i < b; ++i) {
@@ -267,6 +268,7 @@ float Engine::ar_step_sampled(int b, const int32_t* slots, float temperature, co
 
 float Engine::sd_step_stochastic(int D, float temperature, int b, const int32_t* slots, const double* uniforms,
                                  tlt_accept_out* out) {
+    draft_slots_.clear();
     if (D < 1 || D > kMaxD - 1) throw ConfigErr("draft_depth", "must be in [1, 15]");
     if (!(temperature > 0.0f)) throw ConfigErr("temperature", "stochastic_linear requires temperature > 0");
     if (b < 1 || b > max_b_) throw ConfigErr("batch", "out of range");

@@ -69,6 +69,11 @@ class TreeOut(C.Structure):
                 ("path_probs", C.c_void_p), ("n_nodes", C.c_void_p)]
 
 
+class TreeIn(C.Structure):
+    _fields_ = [("tokens", C.c_void_p), ("parents", C.c_void_p), ("probs", C.c_void_p), ("path_probs", C.c_void_p),
+                ("n_nodes", C.c_void_p), ("stride", C.c_int32)]
+
+
 class AcceptOut(C.Structure):
     _fields_ = [("accepted", C.c_void_p), ("nodes", C.c_void_p), ("accept_len", C.c_void_p), ("bonus", C.c_void_p),
                 ("kv_src", C.c_void_p), ("kv_len", C.c_void_p), ("elapsed_ms", C.c_void_p)]
@@ -208,6 +213,57 @@ class Engine:
                              tpr[i, :tn[i]].tolist(), tpp[i, :tn[i]].tolist())) for i in range(b)]
         return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
                           [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), tree)
+
+    def draft(self, strategy, slots):
+        """Propose only (tlt_draft): build_draft_tree on the GPU drafter, no
+        commit. Returns per request [(token, parent, depth, prob, path_prob)]."""
+        s = Strategy(*strategy)
+        slots = np.asarray(slots, np.int32)
+        b, T = len(slots), s.tokens_to_verify
+        tt, tp, td = (np.zeros((b, T), np.int32) for _ in range(3))
+        tpr, tpp = np.zeros((b, T)), np.zeros((b, T))
+        tn = np.zeros(b, np.int32)
+        to = TreeOut(tt.ctypes.data, tp.ctypes.data, td.ctypes.data, tpr.ctypes.data, tpp.ctypes.data, tn.ctypes.data)
+        _check(self.L.tlt_draft(self.h, C.byref(s), b, _p(slots), C.byref(to)))
+        return [list(zip(tt[i, :tn[i]].tolist(), tp[i, :tn[i]].tolist(), td[i, :tn[i]].tolist(),
+                         tpr[i, :tn[i]].tolist(), tpp[i, :tn[i]].tolist())) for i in range(b)]
+
+    def verify(self, slots, trees=None, draft_depth=None):
+        """verify_greedy + KV commit (tlt_verify_accept_commit). trees None:
+        the engine's own last draft of these slots (pass its draft_depth);
+        else per request a list of (token, parent[, ...]) in rank order."""
+        slots = np.asarray(slots, np.int32)
+        b = len(slots)
+        ti = None
+        if trees is not None:
+            stride = max(1, max(len(t) for t in trees))
+            tok = np.zeros((b, stride), np.int32)
+            par = np.zeros((b, stride), np.int32)
+            pr = np.ones((b, stride))
+            pp = np.ones((b, stride))
+            nn = np.zeros(b, np.int32)
+            for i, t in enumerate(trees):
+                nn[i] = len(t)
+                for j, node in enumerate(t):
+                    tok[i, j], par[i, j] = node[0], node[1]
+                    if len(node) >= 5:
+                        pr[i, j], pp[i, j] = node[3], node[4]
+            ti = TreeIn(tok.ctypes.data, par.ctypes.data, pr.ctypes.data, pp.ctypes.data, nn.ctypes.data, stride)
+            keep = (tok, par, pr, pp, nn)  # noqa: F841 (alive across the call)
+        else:
+            stride = int(draft_depth)
+        acc = np.zeros((b, stride), np.int32)
+        nodes = np.zeros((b, stride), np.int32)
+        alen = np.zeros(b, np.int32)
+        bonus = np.zeros(b, np.int32)
+        kvl = np.zeros(b, np.int32)
+        ms = np.zeros(1, np.float32)
+        ao = AcceptOut(acc.ctypes.data, nodes.ctypes.data, alen.ctypes.data, bonus.ctypes.data, None,
+                       kvl.ctypes.data, ms.ctypes.data)
+        _check(self.L.tlt_verify_accept_commit(self.h, b, _p(slots), C.byref(ti) if ti is not None else None,
+                                               C.byref(ao)))
+        return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
+                          [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
 
     def probe_kernel(self, kind: int, m_tok: int, iters: int = 56):
         """Live timing of one engine GEMM site (tlt_probe_kernel): returns
@@ -490,6 +546,12 @@ class Mab:
     def copy_from(self, other: "Mab"):
         _check(self.L.tlt_mab_copy(self.h, other.h))
 
+    def __del__(self):
+        try:
+            self.L.tlt_mab_destroy(self.h)
+        except Exception:
+            pass
+
 
 def merge_bandit_stats(dist, local: "Mab", shared: "Mab") -> int:
     """C1: all-gather every rank's new BEG-MAB records and apply
@@ -510,12 +572,6 @@ def merge_bandit_stats(dist, local: "Mab", shared: "Mab") -> int:
             n += 1
     local.copy_from(shared)
     return n
-
-    def __del__(self):
-        try:
-            self.L.tlt_mab_destroy(self.h)
-        except Exception:
-            pass
 
 
 def handback_samples(dist, samples, trainer_rank: int = 0):
