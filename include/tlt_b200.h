@@ -269,6 +269,33 @@ TLT_API int tlt_plan_captures(const tlt_strategy* strategies, int n, const int32
                               double* total_memory_units);
 
 /* ---- rollout (the step loop's caller, reference run_rollout) ------------- */
+/* Reference CostModelParams (cost_model.hpp:16-33), abstract time units. */
+typedef struct {
+    double t_launch;
+    double model_bytes;
+    double mem_bw;
+    double flops_per_token;
+    double peak_flops;
+    double drafter_step_cost;
+} tlt_cost_model;
+/* step_latency (cost_model.hpp:38-48); sd == NULL is a plain decode step. */
+TLT_API int tlt_step_latency(const tlt_cost_model* cost, int batch, int tokens_per_request, const tlt_strategy* sd,
+                             double* out);
+
+/* Reference StepMetrics (rollout.hpp:31-38), one per engine step. The step's
+ * accept_lens are trace_accept_lens[accept_off .. accept_off + n_accept). */
+typedef struct {
+    int32_t step_index;
+    int32_t batch_size;
+    int32_t sd_active;
+    int32_t has_strategy;
+    tlt_strategy strategy;
+    double elapsed;    /* what beg_record saw: device ms, or step_latency units (parity_elapsed) */
+    double device_ms;  /* measured device time of the step (CUDA events) */
+    int64_t accept_off;
+    int32_t n_accept;
+    int32_t via_ngram; /* the step drafted with the model-free n-gram tracker */
+} tlt_step_metrics;
 /* Reference RolloutConfig (rollout.hpp:66-77) subset on the GPU path. */
 typedef struct {
     int32_t enable_sd;
@@ -287,6 +314,18 @@ typedef struct {
     int32_t ngram_n;                /* reference default 2 */
     int32_t ngram_continuation_len; /* reference default 8 */
     int64_t target_step_id;         /* recency stamp of n-gram records (target.step_id()) */
+    /* Deterministic elapsed (reference step_latency, cost_model.hpp:38-48):
+     * 0 = each step's elapsed is its measured device time in ms (CUDA
+     * events; the product setting), 1 = elapsed = step_latency(cost, batch,
+     * T or 1, strategy or none) in cost-model units, exactly as the
+     * reference run_rollout computes it (rollout.hpp:242,258), so a BEG-MAB
+     * rollout replays the reference's arm sequence bit for bit. */
+    int32_t parity_elapsed;
+    /* 1: finished requests keep their KV slot live (slot i) after the call,
+     * so the caller can tlt_export_sequence (C2) them before tlt_release;
+     * 0: slots are released as requests finish. */
+    int32_t keep_finished;
+    tlt_cost_model cost;            /* all zero = reference defaults (cost_model.hpp:16-22) */
 } tlt_rollout_cfg;
 
 /* Reference RolloutResult (rollout.hpp:79-97) flattened. generated: [n][max_len]. */
@@ -301,6 +340,19 @@ typedef struct {
     double device_ms;       /* sum of per-step device time */
     double wall_ms;         /* host wall time of the whole rollout */
     int64_t gpu_launches;   /* kernel launches issued (graph nodes counted) */
+    /* --- the rest of reference RolloutResult (rollout.hpp:79-97); every
+     * pointer below is caller-owned and may be NULL --- */
+    double total_time;            /* sum of step elapsed (rollout.hpp:263) */
+    int64_t ngram_verify_events;  /* verify events drafted by the n-gram tracker (:226) */
+    int64_t* accept_at_least;     /* [accept_at_least_cap]: [i] = events with accept_len > i (:227-229) */
+    int32_t accept_at_least_cap;
+    int32_t accept_at_least_len;  /* out: max draft depth (reference vector size) */
+    double* finish_time;          /* [n]: total_time when request i finished (:264-268) */
+    tlt_step_metrics* trace;      /* [trace_cap] (:270) */
+    int64_t trace_cap;
+    int64_t trace_len;            /* out: engine steps (entries beyond trace_cap are counted, not stored) */
+    int32_t* trace_accept_lens;   /* [trace_accept_cap] concatenated per-step accept_lens */
+    int64_t trace_accept_cap;
 } tlt_rollout_result;
 
 /* Runs n requests (prompts back to back, max_len per request) to completion

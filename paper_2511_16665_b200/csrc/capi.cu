@@ -360,6 +360,15 @@ TLT_API int tlt_plan_captures(const tlt_strategy* strategies, int n, const int32
 }
 
 // ---------------------------------------------------------------- rollout
+TLT_API int tlt_step_latency(const tlt_cost_model* cost, int batch, int tokens_per_request, const tlt_strategy* sd,
+                             double* out) {
+    if (!out) return fail(TLT_ERR_CONFIG, "null argument");
+    return guard([&] {
+        const tlt_cost_model c = tlt::cost_or_default(cost ? *cost : tlt_cost_model{});
+        *out = tlt::step_latency(c, batch, tokens_per_request, sd);
+    });
+}
+
 // Reference run_rollout (rollout.hpp:130-276) on the GPU engine: elastic gate,
 // BEG-MAB select/record (measured elapsed), greedy tree SD or plain decode per
 // engine step, emission truncated at EOS / max_len (:231-240), requests
@@ -380,6 +389,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         if (cfg->temperature < 0.0f) throw tlt::ConfigErr("temperature", "must be >= 0");
         if (cfg->use_mab && !mab) throw tlt::ConfigErr("mab", "use_mab requires a bandit state");
         if (!cfg->use_mab && cfg->enable_sd) tlt::validate(cfg->fixed_strategy);
+        const tlt_cost_model cost = tlt::cost_or_default(cfg->cost);  // run_rollout: cost.validate() (:135)
         E.use_graphs = cfg->use_graphs != 0;
         std::vector<int32_t> slots(n);
         for (int i = 0; i < n; ++i) {
@@ -404,13 +414,21 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
         if (std::getenv("TLT_TRACE")) std::fprintf(stderr, "[tlt] prefill_ms %.3f n=%d\n", E.last_prefill_ms, n);
         std::vector<int> running(n, 1), glen(n, 0);
         out->sd_steps = out->plain_steps = out->verify_events = out->accepted_total = out->emitted_total = 0;
+        out->ngram_verify_events = 0;
+        out->total_time = 0.0;
+        out->trace_len = 0;
+        int64_t trace_acc_n = 0;
+        std::vector<double> finish(n, 0.0);
         out->device_ms = E.last_prefill_ms;
         const long long launches0 = E.launches;
+        // accept_at_least sized by the largest arm depth (rollout.hpp:157-163)
         int maxD = 1;
         if (cfg->use_mab)
             for (auto& a : mab->m->arms) maxD = std::max(maxD, a.strategy.draft_depth);
         else
-            maxD = std::max(1, cfg->fixed_strategy.draft_depth);
+            maxD = cfg->fixed_strategy.draft_depth > 0 ? cfg->fixed_strategy.draft_depth : 1;  // nullopt -> 1
+        std::vector<int64_t> at_least(std::max(maxD, 0), 0);
+        int step_index = 0;
         std::vector<int32_t> act, acc_len, bonus, accepted, tok;
         // per-request queue of RngStream draws: the device consumes them in
         // reference order, the host pops exactly what was consumed
@@ -431,6 +449,12 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
             const int batch = (int)act.size();
             const bool sd = cfg->enable_sd && batch < cfg->elastic_threshold;  // rollout.hpp:174
             static const bool trace = std::getenv("TLT_TRACE") != nullptr;
+            tlt_step_metrics sm{};  // StepMetrics (rollout.hpp:31-38, :175-178)
+            sm.step_index = step_index;
+            sm.batch_size = batch;
+            sm.sd_active = sd ? 1 : 0;
+            sm.accept_off = trace_acc_n;
+            sm.via_ngram = sd && via_ngram ? 1 : 0;
             auto emit = [&](int i, int32_t t) {
                 out->generated[(size_t)i * max_len_stride + glen[i]] = t;
                 glen[i] += 1;
@@ -484,7 +508,12 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 for (int j = 0; j < batch; ++j) {
                     const int i = act[j];
                     out->verify_events += 1;
+                    out->ngram_verify_events += via_ngram ? 1 : 0;
                     out->accepted_total += acc_len[j];
+                    for (int d = 0; d < acc_len[j] && d < maxD; ++d) at_least[d] += 1;  // rollout.hpp:227-229
+                    if (out->trace_accept_lens && trace_acc_n < out->trace_accept_cap)
+                        out->trace_accept_lens[trace_acc_n] = acc_len[j];
+                    ++trace_acc_n;
                     bool done = false;
                     for (int t = 0; t < acc_len[j] && !done; ++t) done = emit(i, accepted[(size_t)j * D + t]);
                     if (!done) emit(i, bonus[j]);
@@ -496,7 +525,15 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                     std::fprintf(stderr, "[tlt] sd_ms %.3f b=%d D=%d k=%d T=%d acc=%d\n", ms, batch, D, s.top_k,
                                  s.tokens_to_verify, acc);
                 }
-                if (cfg->use_mab) mab->m->record(s, (double)ms, acc_len.data(), batch);  // rollout.hpp:244
+                // rollout.hpp:242-245: elapsed -> beg_record
+                const double elapsed = cfg->parity_elapsed ? tlt::step_latency(cost, batch, s.tokens_to_verify, &s)
+                                                           : (double)ms;
+                if (cfg->use_mab) mab->m->record(s, elapsed, acc_len.data(), batch);
+                sm.has_strategy = 1;
+                sm.strategy = s;
+                sm.elapsed = elapsed;
+                sm.device_ms = ms;
+                sm.n_accept = batch;
                 out->sd_steps += 1;
             } else {
                 tok.assign(batch, 0);
@@ -512,14 +549,33 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
                 }
                 out->device_ms += ms;
                 if (trace) std::fprintf(stderr, "[tlt] ar_ms %.3f b=%d\n", ms, batch);
+                sm.elapsed = cfg->parity_elapsed ? tlt::step_latency(cost, batch, 1, nullptr) : (double)ms;  // :258
+                sm.device_ms = ms;
                 out->plain_steps += 1;
             }
+            out->total_time += sm.elapsed;  // rollout.hpp:263-268
             for (int j = 0; j < batch; ++j)
-                if (!running[act[j]]) E.release(act[j]);
+                if (!running[act[j]] && finish[act[j]] == 0.0) finish[act[j]] = out->total_time;
+            if (out->trace && out->trace_len < out->trace_cap) out->trace[out->trace_len] = sm;
+            out->trace_len += 1;
+            ++step_index;
+            for (int j = 0; j < batch; ++j) {
+                const int i = act[j];
+                if (running[i]) continue;
+                if (cfg->keep_finished)  // committed = prompt ++ generated, last emitted token = pending root
+                    E.truncate(i, prompt_lens[i] + glen[i] - 1);
+                else
+                    E.release(i);
+            }
         }
+        out->accept_at_least_len = (int32_t)at_least.size();
+        if (out->accept_at_least)
+            for (int d = 0; d < (int)at_least.size() && d < out->accept_at_least_cap; ++d)
+                out->accept_at_least[d] = at_least[d];
+        if (out->finish_time)
+            for (int i = 0; i < n; ++i) out->finish_time[i] = finish[i];
         for (int i = 0; i < n; ++i) out->gen_len[i] = glen[i];
         out->gpu_launches = E.launches - launches0;
-        (void)maxD;
         out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     });
 }

@@ -743,6 +743,16 @@ void Engine::release(int slot) {
     lt_[slot] = ld_[slot] = 0;
 }
 
+// Shorten a live slot's committed state to `len` positions (token len becomes
+// the pending root): the rollout trims requests whose last step committed KV
+// past the emission cut (EOS / max_len) before the sequence is exported.
+void Engine::truncate(int slot, int len) {
+    if (slot < 0 || slot >= cfg.max_slots || !live_[slot]) throw ConfigErr("slot_id", "slot not live");
+    if (len < 0 || len > lt_[slot]) throw ConfigErr("len", "beyond the committed length");
+    lt_[slot] = len;
+    ld_[slot] = std::min(ld_[slot], len);
+}
+
 int Engine::export_sequence(int slot, int32_t* tokens, int max_tokens, void* features, size_t features_bytes) {
     if (slot < 0 || slot >= cfg.max_slots || !live_[slot]) throw ConfigErr("slot_id", "slot not live");
     const int n = lt_[slot];  // positions with committed KV / target features; token n is the pending root

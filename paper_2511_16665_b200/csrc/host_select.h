@@ -67,6 +67,32 @@ inline void validate(const tlt_strategy& s) {  // spec_decode.hpp:36-42
         throw ConfigErr("tokens_to_verify", "exceeds tree capacity for (top_k, draft_depth)");
 }
 
+// CostModelParams (cost_model.hpp:16-33): all-zero = the reference defaults;
+// otherwise every field must be > 0 (validate, :24-32).
+inline tlt_cost_model cost_or_default(const tlt_cost_model& c) {
+    if (c.t_launch == 0 && c.model_bytes == 0 && c.mem_bw == 0 && c.flops_per_token == 0 && c.peak_flops == 0 &&
+        c.drafter_step_cost == 0)
+        return tlt_cost_model{0.05, 1.0, 1.0, 1.0, 377.0, 0.046};
+    if (!(c.t_launch > 0.0)) throw ConfigErr("cost_model.t_launch", "must be > 0");
+    if (!(c.model_bytes > 0.0)) throw ConfigErr("cost_model.model_bytes", "must be > 0");
+    if (!(c.mem_bw > 0.0)) throw ConfigErr("cost_model.mem_bw", "must be > 0");
+    if (!(c.flops_per_token > 0.0)) throw ConfigErr("cost_model.flops_per_token", "must be > 0");
+    if (!(c.peak_flops > 0.0)) throw ConfigErr("cost_model.peak_flops", "must be > 0");
+    if (!(c.drafter_step_cost > 0.0)) throw ConfigErr("cost_model.drafter_step_cost", "must be > 0");
+    return c;
+}
+// step_latency (cost_model.hpp:38-48): launch + max(weight stream, compute)
+// + one drafter pass per draft level.
+inline double step_latency(const tlt_cost_model& c, int batch, int tokens_per_request, const tlt_strategy* sd) {
+    if (batch < 1) throw ConfigErr("batch", "must be >= 1");
+    const int tokens = sd ? sd->tokens_to_verify : tokens_per_request;
+    const double memory_time = c.model_bytes / c.mem_bw;
+    const double compute_time = static_cast<double>(batch) * static_cast<double>(tokens) * c.flops_per_token / c.peak_flops;
+    double t = c.t_launch + std::max(memory_time, compute_time);
+    if (sd) t += static_cast<double>(sd->draft_depth) * c.drafter_step_cost;
+    return t;
+}
+
 // BEG-MAB state (beg_mab.hpp:28-69).
 struct Mab {
     struct Arm {

@@ -85,18 +85,45 @@ class CaptureEntry(C.Structure):
                 ("memory_units", C.c_double)]
 
 
+class CostModel(C.Structure):
+    """Reference CostModelParams (cost_model.hpp:16-33); all zero = defaults."""
+    _fields_ = [("t_launch", C.c_double), ("model_bytes", C.c_double), ("mem_bw", C.c_double),
+                ("flops_per_token", C.c_double), ("peak_flops", C.c_double), ("drafter_step_cost", C.c_double)]
+
+
 class RolloutCfg(C.Structure):
     _fields_ = [("enable_sd", C.c_int32), ("elastic_threshold", C.c_int32), ("mode", C.c_int32),
                 ("temperature", C.c_float), ("fixed_strategy", Strategy), ("use_mab", C.c_int32),
                 ("seed", C.c_uint64), ("use_graphs", C.c_int32), ("drafter_stale", C.c_int32),
-                ("ngram_n", C.c_int32), ("ngram_continuation_len", C.c_int32), ("target_step_id", C.c_int64)]
+                ("ngram_n", C.c_int32), ("ngram_continuation_len", C.c_int32), ("target_step_id", C.c_int64),
+                ("parity_elapsed", C.c_int32), ("keep_finished", C.c_int32), ("cost", CostModel)]
+
+
+class StepMetrics(C.Structure):
+    """Reference StepMetrics (rollout.hpp:31-38)."""
+    _fields_ = [("step_index", C.c_int32), ("batch_size", C.c_int32), ("sd_active", C.c_int32),
+                ("has_strategy", C.c_int32), ("strategy", Strategy), ("elapsed", C.c_double),
+                ("device_ms", C.c_double), ("accept_off", C.c_int64), ("n_accept", C.c_int32),
+                ("via_ngram", C.c_int32)]
 
 
 class RolloutResult(C.Structure):
     _fields_ = [("generated", C.c_void_p), ("gen_len", C.c_void_p), ("sd_steps", C.c_int64),
                 ("plain_steps", C.c_int64), ("verify_events", C.c_int64), ("accepted_total", C.c_int64),
                 ("emitted_total", C.c_int64), ("device_ms", C.c_double), ("wall_ms", C.c_double),
-                ("gpu_launches", C.c_int64)]
+                ("gpu_launches", C.c_int64), ("total_time", C.c_double), ("ngram_verify_events", C.c_int64),
+                ("accept_at_least", C.c_void_p), ("accept_at_least_cap", C.c_int32),
+                ("accept_at_least_len", C.c_int32), ("finish_time", C.c_void_p), ("trace", C.c_void_p),
+                ("trace_cap", C.c_int64), ("trace_len", C.c_int64), ("trace_accept_lens", C.c_void_p),
+                ("trace_accept_cap", C.c_int64)]
+
+
+def step_latency(batch, tokens_per_request, strategy=None, cost=None):
+    """Reference step_latency (cost_model.hpp:38-48) through the C-ABI."""
+    out = C.c_double()
+    _check(lib().tlt_step_latency(C.byref(cost) if cost is not None else None, batch, tokens_per_request,
+                                  C.byref(Strategy(*strategy)) if strategy is not None else None, C.byref(out)))
+    return out.value
 
 
 def _p(a: np.ndarray) -> C.c_void_p:
@@ -417,7 +444,11 @@ class Engine:
     # ---------------------------------------------------------- rollout
     def run_rollout(self, prompts, max_lens, request_ids=None, *, enable_sd=True, elastic_threshold=32,
                     strategy=(4, 4, 16), mab: "Mab | None" = None, seed=0, use_graphs=True, mode="greedy",
-                    temperature=0.0, drafter_stale=False, ngram_n=2, ngram_continuation_len=8, target_step_id=0):
+                    temperature=0.0, drafter_stale=False, ngram_n=2, ngram_continuation_len=8, target_step_id=0,
+                    parity_elapsed=False, keep_finished=False, cost=None, trace_cap=1 << 16):
+        """Reference run_rollout (rollout.hpp:130-276). Returns the RolloutResult
+        fields (requests' tokens and finish_time, trace of StepMetrics,
+        accept_at_least, counters) as a dict."""
         n = len(prompts)
         rid = np.asarray(request_ids if request_ids is not None else range(n), np.int32)
         plen = np.asarray([len(p) for p in prompts], np.int32)
@@ -429,14 +460,34 @@ class Engine:
         cfg = RolloutCfg(1 if enable_sd else 0, elastic_threshold, 1 if mode == "stochastic" else 0,
                          float(temperature), Strategy(*strategy),
                          1 if mab is not None else 0, seed, 1 if use_graphs else 0, 1 if drafter_stale else 0,
-                         ngram_n, ngram_continuation_len, target_step_id)
+                         ngram_n, ngram_continuation_len, target_step_id, 1 if parity_elapsed else 0,
+                         1 if keep_finished else 0, cost if cost is not None else CostModel())
         res = RolloutResult(gen.ctypes.data, glen.ctypes.data)
+        aal = np.zeros(64, np.int64)
+        fin = np.zeros(n, np.float64)
+        trace = (StepMetrics * trace_cap)()
+        tacc = np.zeros(trace_cap * 4, np.int32)
+        res.accept_at_least, res.accept_at_least_cap = aal.ctypes.data, len(aal)
+        res.finish_time = fin.ctypes.data
+        res.trace, res.trace_cap = C.cast(trace, C.c_void_p), trace_cap
+        res.trace_accept_lens, res.trace_accept_cap = tacc.ctypes.data, len(tacc)
         _check(self.L.tlt_run_rollout(self.h, C.byref(cfg), mab.h if mab is not None else None, n, _p(rid),
                                       _p(plen), _p(toks), _p(ml), stride, C.byref(res)))
+        steps = []
+        for t in trace[:min(res.trace_len, trace_cap)]:
+            o = t.accept_off
+            steps.append(dict(step_index=t.step_index, batch_size=t.batch_size, sd_active=bool(t.sd_active),
+                              strategy=t.strategy.tuple() if t.has_strategy else None, elapsed=t.elapsed,
+                              device_ms=t.device_ms, via_ngram=bool(t.via_ngram),
+                              accept_lens=tacc[o:o + t.n_accept].tolist() if o + t.n_accept <= len(tacc) else None))
         return dict(tokens=[gen[i, :glen[i]].tolist() for i in range(n)], sd_steps=res.sd_steps,
                     plain_steps=res.plain_steps, verify_events=res.verify_events,
+                    ngram_verify_events=res.ngram_verify_events,
                     accepted_total=res.accepted_total, emitted_total=res.emitted_total, device_ms=res.device_ms,
-                    wall_ms=res.wall_ms, gpu_launches=res.gpu_launches)
+                    wall_ms=res.wall_ms, gpu_launches=res.gpu_launches, total_time=res.total_time,
+                    accept_at_least=aal[:res.accept_at_least_len].tolist(), finish_time=fin.tolist(),
+                    trace=steps, trace_len=res.trace_len,
+                    mean_accept_len=(res.accepted_total / res.verify_events) if res.verify_events else 0.0)
 
 
 class Rng:
@@ -583,8 +634,9 @@ def handback_samples(dist, samples, trainer_rank: int = 0):
     off the decode critical path (called at rollout boundaries)."""
     import torch
     rank, world = dist.get_rank(), dist.get_world_size()
-    dev = samples[0][1].device if samples else (torch.device("cuda", torch.cuda.current_device())
-                                                 if dist.get_backend() == "nccl" else torch.device("cpu"))
+    # the transport device follows the backend, not the samples: NCCL moves
+    # CUDA tensors only, gloo point-to-point CPU tensors only
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
     cnt = torch.tensor([len(samples)], dtype=torch.int64, device=dev)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(counts, cnt)
@@ -596,11 +648,11 @@ def handback_samples(dist, samples, trainer_rank: int = 0):
                                dtype=torch.int64, device=dev)
             dist.send(hdr, trainer_rank)
             dist.send(t, trainer_rank)
-            dist.send(feats.contiguous().view(torch.int16), trainer_rank)  # bf16 bits
+            dist.send(feats.contiguous().view(torch.int16).to(dev), trainer_rank)  # bf16 bits
         return out
     for r in range(world):
         if r == trainer_rank:
-            out += [(r, torch.as_tensor(np.asarray(t, np.int32)).to(dev), f) for t, f in samples]
+            out += [(r, torch.as_tensor(np.asarray(t, np.int32)).to(dev), f.to(dev)) for t, f in samples]
             continue
         for _ in range(int(counts[r].item())):
             hdr = torch.zeros(3, dtype=torch.int64, device=dev)

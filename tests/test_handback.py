@@ -90,3 +90,29 @@ def test_gpu_export_sequence():
         tc, fc = eng.export_sequence(i, device=False)
         assert np.array_equal(tc, t) and torch.equal(fc.view(torch.int16), f.cpu().view(torch.int16))
     eng.close()
+
+
+@pytest.mark.gpu
+def test_gpu_handback_of_exported_cuda_tensors_over_gloo():
+    """samples exported as CUDA tensors travel over a gloo group
+    (CPU transport) — world size 1, the trainer rank gets them back on CPU."""
+    from torch.distributed import FileStore
+
+    from paper_2511_16665_b200.engine import Engine, handback_samples
+    import tempfile
+    rng = np.random.default_rng(3)
+    prompts = [rng.integers(2, 4096, 12).tolist() for _ in range(2)]
+    eng = Engine("tiny", max_slots=2, max_ctx=256, device=0)
+    eng.run_rollout(prompts, [10, 15], enable_sd=True, elastic_threshold=8, strategy=(4, 4, 16), keep_finished=True)
+    samples = [eng.export_sequence(i) for i in range(2)]
+    with tempfile.NamedTemporaryFile() as f:
+        dist.init_process_group("gloo", store=FileStore(f.name, 1), rank=0, world_size=1)
+        try:
+            got = handback_samples(dist, samples, trainer_rank=0)
+        finally:
+            dist.destroy_process_group()
+    assert len(got) == 2
+    for (r, t, feats), (wt, wf) in zip(got, samples):
+        assert r == 0 and not feats.is_cuda and t.tolist() == wt.tolist()
+        assert torch.equal(feats.view(torch.int16), wf.cpu().view(torch.int16))
+    eng.close()

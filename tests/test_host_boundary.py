@@ -129,3 +129,27 @@ def test_mab_merge_of_foreign_records_is_order_deterministic():
     for i in range(len(DEFAULT_ARMS)):
         assert a.arm_stats(i) == b.arm_stats(i)
     assert a.arm_stats(3)[2] == 2 and a.arm_stats(3)[0] == pytest.approx((120.5 + 99.0) / 2)
+
+
+@needs_ref
+def test_product_step_latency_matches_reference():
+    """tlt_step_latency (the parity_elapsed clock) == reference step_latency
+    (cost_model.hpp:38-48) with the default CostModelParams."""
+    from paper_2511_16665_b200.engine import step_latency
+    R = O.ref()
+    R.ref_step_latency.argtypes = [C.c_int] * 6
+    for batch in [1, 2, 7, 16, 31, 64, 377, 1000]:
+        assert step_latency(batch, 1) == R.ref_step_latency(batch, 1, 0, 0, 0, 0)
+        for s in DEFAULT_ARMS + [(4, 4, 16), (2, 1, 2)]:
+            assert step_latency(batch, s[2], s) == R.ref_step_latency(batch, s[2], *s, 1)
+
+
+def test_step_latency_cost_validation():
+    from paper_2511_16665_b200.engine import ConfigError, CostModel, step_latency
+    c = CostModel(0.5, 2.0, 1.0, 1.0, 100.0, 0.25)
+    assert step_latency(8, 1, None, c) == 0.5 + 2.0
+    assert step_latency(100, 16, (4, 4, 16), c) == 0.5 + 16.0 + 4 * 0.25
+    with pytest.raises(ConfigError, match="cost_model.mem_bw"):
+        step_latency(1, 1, None, CostModel(0.5, 2.0, -1.0, 1.0, 100.0, 0.25))
+    with pytest.raises(ConfigError, match="batch"):
+        step_latency(0, 1)

@@ -186,10 +186,12 @@ def test_gpu_rollout_ngram_branch_is_lossless(D):
 
 
 def test_rollout_cfg_ngram_fields():
-    """The ctypes mirror appends the n-gram fields in the C struct's order."""
+    """The ctypes mirror carries the n-gram fields in the C struct's order
+    (offsets are checked against the compiled header in test_abi_layout.py)."""
     import paper_2511_16665_b200.engine as E
-    assert [f[0] for f in E.RolloutCfg._fields_][-4:] == ["drafter_stale", "ngram_n", "ngram_continuation_len",
-                                                          "target_step_id"]
+    names = [f[0] for f in E.RolloutCfg._fields_]
+    i = names.index("drafter_stale")
+    assert names[i:i + 4] == ["drafter_stale", "ngram_n", "ngram_continuation_len", "target_step_id"]
 
 
 @pytest.mark.gpu
