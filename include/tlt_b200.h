@@ -213,7 +213,23 @@ typedef struct {
     int32_t draft_depth;
     double memory_units;
 } tlt_capture_entry;
+/* Pre-captures the pool (replaces any existing graphs): for every bucket
+ * [lo, hi] of the entries, one fused step graph per TARGET(T) x DRAFT(k, D)
+ * pair whose strategy is valid, captured at batch hi and replayed for any
+ * batch in the bucket (padding requests inert, their GEMM token tiles
+ * skipped on the device); plus plain-decode graphs at padded batch sizes
+ * 1, 2, 4, 8, 16, 24, ... max_slots. An SD step whose (batch, strategy) is
+ * outside the pool falls back to an exact-batch graph captured on first use.
+ * graph_bytes = device memory the pool took (cudaMemGetInfo delta; all
+ * graphs share the engine's activation buffers). */
 TLT_API int tlt_graph_pool_build(tlt_engine* e, const tlt_capture_entry* entries, int n, size_t* graph_bytes);
+/* Last pool build: graphs captured, plan pairs skipped (draft rows beyond
+ * the engine buffers at that bucket size), bytes, host build time, and the
+ * number of executable graphs the engine holds now (pool + on-demand). */
+TLT_API int tlt_graph_pool_stats(tlt_engine* e, int32_t* n_graphs, int32_t* n_skipped, size_t* graph_bytes,
+                                 double* build_ms, int32_t* n_live);
+/* Destroys every graph and forgets the pool's buckets (exact-batch graphs
+ * are captured on demand again). */
 TLT_API int tlt_graph_pool_clear(tlt_engine* e);
 
 /* ---- strategy selection (host, reference semantics) ---------------------- */

@@ -197,6 +197,18 @@ TLT_API int tlt_graph_pool_build(tlt_engine* e, const tlt_capture_entry* entries
     });
 }
 
+TLT_API int tlt_graph_pool_stats(tlt_engine* e, int32_t* n_graphs, int32_t* n_skipped, size_t* graph_bytes,
+                                 double* build_ms, int32_t* n_live) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] {
+        if (n_graphs) *n_graphs = e->e->pool_graphs_;
+        if (n_skipped) *n_skipped = e->e->pool_skipped_;
+        if (graph_bytes) *graph_bytes = e->e->pool_bytes_;
+        if (build_ms) *build_ms = e->e->pool_capture_ms_;
+        if (n_live) *n_live = e->e->graph_count();
+    });
+}
+
 TLT_API int tlt_graph_pool_clear(tlt_engine* e) {
     if (!e) return fail(TLT_ERR_STATE, "null engine");
     return guard([&] { e->e->graph_pool_clear(); });

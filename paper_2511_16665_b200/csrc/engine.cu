@@ -5,12 +5,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
 #include "engine.h"
+#include "host_select.h"
 #include "pdl.cuh"
 
 namespace tlt {
@@ -289,6 +291,9 @@ void Engine::alloc_state() {
     ar_tok_ = dmalloc<int>(S);
     d_step_ = dmalloc<StepIn>(S);
     h_step_ = hmalloc<StepIn>(S);
+    d_nreal_ = dmalloc<int>(1);
+    h_nreal_ = hmalloc<int>(1);
+    *h_nreal_ = 0;
     ho_.acc_len = hmalloc<int32_t>(S);
     ho_.bonus = hmalloc<int32_t>(S);
     ho_.acc_tok = hmalloc<int32_t>((size_t)S * kMaxD);
@@ -334,8 +339,19 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
     EpiParams ep = ep_in;
     ep.n_out = N;
     ep.m_tok = M;
+    set_dyn(ep, M);
     launch_gemm(g, tmW, tx, ep, ws_, ws_elems_, st_);
     count_launch(1);  // split-K reduction happens inside the same launch (cluster DSMEM)
+}
+
+// Bucketed graphs: inside a step sequence padded to b_hi requests, every
+// GEMM over b_hi x rpr request-major rows skips the token tiles of the
+// padding requests (the live count is uploaded with the step inputs).
+void Engine::set_dyn(EpiParams& e, int M) const {
+    if (dyn_b_hi_ > 0 && M % dyn_b_hi_ == 0) {
+        e.dyn_n = d_nreal_;
+        e.dyn_rpr = M / dyn_b_hi_;
+    }
 }
 
 // x_ += X W^T, then h_ = bf16(rmsnorm(x_) * norm_w) when norm_w != null. The
@@ -351,6 +367,7 @@ void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const C
     e.kind = EPI_RESID_ADD;
     e.out_f32 = x_;
     e.ld_f32 = d;
+    set_dyn(e, M);
     static const int fuse_max_m = [] {
         // off by default: the serial tail of the electing CTA measured slower
         // than the 8-CTA cluster norm kernel under PDL (profiles/r1_*)
@@ -529,6 +546,7 @@ void Engine::drafter_logits(int n) {
     f.m_tok = n;
     f.row_scale = lm8_s_;
     f.tok_scale = h8_s_;
+    set_dyn(f, n);
     launch_gemm(g, tm_lm8_, it->second, f, ws_, ws_elems_, st_);
     count_launch();
 }
@@ -839,8 +857,21 @@ float Engine::catchup_drafter(int b, const int32_t* slots) {
     return ms;
 }
 
+// Batch bucket of an SD step (capture_plan.hpp:64-70,103-122): the step is
+// padded to the hi end of the pool bucket holding b whose captured graphs
+// verify T tokens; outside the pool (or without one) the exact batch.
 int Engine::bucket_hi_for(int b, int T) const {
-    (void)T;
+    for (const auto& pb : pool_)
+        if (b >= pb.lo && b <= pb.hi && std::find(pb.Ts.begin(), pb.Ts.end(), T) != pb.Ts.end())
+            return std::min(pb.hi, max_b_);
+    return b;
+}
+
+// Plain-decode batch bucket: the smallest pooled size >= b (sizes 1, 2, 4, 8,
+// then multiples of 8, as serving engines pad decode graphs), else exact b.
+int Engine::ar_bucket_for(int b) const {
+    for (int s : ar_sizes_)
+        if (s >= b) return s;
     return b;
 }
 
@@ -1002,6 +1033,8 @@ void Engine::sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_r
     (void)b_real;
     const int d = cfg.hidden, V = cfg.vocab, D1 = D + 1;
     CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(d_nreal_, h_nreal_, sizeof(int), cudaMemcpyHostToDevice, st_));
+    DynScope dyn(this, b_hi);
     std::vector<int> base, Fd, lmoff;
     level_plan(b_hi, D, k, T, base, Fd, lmoff);
     if (D >= 2 && base[D] + b_hi * Fd[D] > Rmeta_) throw ConfigErr("strategy", "draft rows exceed TLT_MAX_DRAFT_ROWS");
@@ -1182,6 +1215,7 @@ int Engine::prepare_tree_step(const tlt_strategy& s, int b, const int32_t* slots
         if (!need.empty()) *catchup_ms = catchup_drafter((int)need.size(), need.data());
     }
     const int b_hi = bucket_hi_for(b, T);
+    *h_nreal_ = b;
     for (int i = 0; i < b_hi; ++i) {
         if (i < b) {
             const int sl = slots[i];
@@ -1263,23 +1297,7 @@ float Engine::sd_step(const tlt_strategy& s, int b, const int32_t* slots, tlt_tr
         dbg_cache_.clear();
     }
     // capture for the next replay (after a successful eager run)
-    if (use_graphs && it == graphs_.end()) {
-        cudaGraph_t g;
-        launches_in_seq_ = 0;
-        CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-        // the captured sequence must not change device state: capture only
-        try {
-            sd_device_sequence(b_hi, D, k, T, dbg, b);
-        } catch (...) {
-            cudaStreamEndCapture(st_, &g);
-            throw;
-        }
-        CUDA_CHECK(cudaStreamEndCapture(st_, &g));
-        cudaGraphExec_t ex;
-        CUDA_CHECK(cudaGraphInstantiate(&ex, g, 0));
-        CUDA_CHECK(cudaGraphDestroy(g));
-        graphs_[key] = {ex, launches_in_seq_};
-    }
+    if (use_graphs && it == graphs_.end()) capture_graph(key, false);
     copy_step_out(b, slots, T, D, tree, out);
     for (int i = 0; i < b; ++i) {  // host mirrors
         const int sl = slots[i];
@@ -1546,6 +1564,8 @@ float Engine::sd_step_chain(int D, int b, const int32_t* slots, const int32_t* c
 
 void Engine::ar_device_sequence(int b_hi) {
     CUDA_CHECK(cudaMemcpyAsync(d_step_, h_step_, sizeof(StepIn) * b_hi, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(d_nreal_, h_nreal_, sizeof(int), cudaMemcpyHostToDevice, st_));
+    DynScope dyn(this, b_hi);
     launch_rows_ar(d_step_, b_hi, b_hi, prows_, pg_, tok_hist_, cap_, st_);
     count_launch();
     target_forward(prows_, pg_, b_hi, 1, b_hi, cap_, nullptr, feat_);
@@ -1563,8 +1583,9 @@ float Engine::ar_step(int b, const int32_t* slots, int32_t* out_tokens) {
         if (sl < 0 || sl >= cfg.max_slots || !live_[sl]) throw ConfigErr("slot_ids", "slot not prefilled");
         if (lt_[sl] + 2 > cap_ - 1) throw ConfigErr("max_ctx", "context full");
     }
-    const int b_hi = b;
+    const int b_hi = use_graphs && !debug_ ? std::min(ar_bucket_for(b), max_b_) : b;
     for (int i = 0; i < b_hi; ++i) h_step_[i] = i < b ? StepIn{slots[i], lt_[slots[i]], ld_[slots[i]], 0} : StepIn{-1, 0, 0, 0};
+    *h_nreal_ = b;
     CUDA_CHECK(cudaEventRecord(ev0_, st_));
     auto key = std::make_tuple(b_hi, 0, 0, 0, 1);
     auto it = graphs_.find(key);
@@ -1585,22 +1606,7 @@ float Engine::ar_step(int b, const int32_t* slots, int32_t* out_tokens) {
         CUDA_CHECK(cudaMemcpy(dbg_ar_logits.data(), logits_, sizeof(float) * dbg_ar_logits.size(),
                               cudaMemcpyDeviceToHost));
     }
-    if (use_graphs && !debug_ && it == graphs_.end()) {
-        cudaGraph_t g;
-        launches_in_seq_ = 0;
-        CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-        try {
-            ar_device_sequence(b_hi);
-        } catch (...) {
-            cudaStreamEndCapture(st_, &g);
-            throw;
-        }
-        CUDA_CHECK(cudaStreamEndCapture(st_, &g));
-        cudaGraphExec_t ex;
-        CUDA_CHECK(cudaGraphInstantiate(&ex, g, 0));
-        CUDA_CHECK(cudaGraphDestroy(g));
-        graphs_[key] = {ex, launches_in_seq_};
-    }
+    if (use_graphs && !debug_ && it == graphs_.end()) capture_graph(key, true);
     for (int i = 0; i < b; ++i) {
         if (out_tokens) out_tokens[i] = ho_.ar_tok[i];
         lt_[slots[i]] += 1;
@@ -1709,14 +1715,119 @@ std::vector<float> Engine::debug_verify_logits(int i) {
     return v;
 }
 
-size_t Engine::graph_pool_build(const std::vector<tlt_capture_entry>& entries) {
-    (void)entries;  // graphs are captured lazily on first use of each key
-    return graphs_.size();
+// Capture one step sequence into an executable graph (the sequence is only
+// recorded, not run: device state is unchanged). key = (b_hi, D, k, T, kind):
+// kind 0 greedy tree SD step, 4 its debug-export variant, 1 plain decode.
+void Engine::capture_graph(const std::tuple<int, int, int, int, int>& key, bool ar) {
+    const int b_hi = std::get<0>(key), D = std::get<1>(key), k = std::get<2>(key), T = std::get<3>(key);
+    const bool dbg = std::get<4>(key) == 4;
+    cudaGraph_t g;
+    launches_in_seq_ = 0;
+    CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    try {
+        if (ar)
+            ar_device_sequence(b_hi);
+        else
+            sd_device_sequence(b_hi, D, k, T, dbg, b_hi);
+    } catch (...) {
+        cudaStreamEndCapture(st_, &g);
+        throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+    cudaGraphExec_t ex;
+    CUDA_CHECK(cudaGraphInstantiate(&ex, g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+    auto old = graphs_.find(key);
+    if (old != graphs_.end()) cudaGraphExecDestroy(old->second.first);
+    graphs_[key] = {ex, launches_in_seq_};
+}
+
+// Pre-capture the pool of plan_captures (capture_plan.hpp:87-126): every
+// TARGET(bucket, T) x DRAFT(bucket, k, D) pair of a bucket becomes one fused
+// step graph keyed (bucket_hi, D, k, T) (within a bucket BEG-MAB routes only
+// that bucket's arms, beg_mab.hpp:95-105), captured for the bucket's largest
+// batch and replayed for every batch in it (padding requests inert, their
+// GEMM tiles skipped). Plain decode gets graphs for padded batch sizes 1, 2,
+// 4, 8, 16, 24, ... up to max_slots. Each sequence runs once eagerly with
+// every request padding (touches lazily created host state, changes no
+// device state) before it is captured. Returns the device memory the pool
+// took (cudaMemGetInfo delta; every graph shares the engine's activation
+// buffers, so this is the executable graphs' own footprint).
+size_t Engine::graph_pool_build(const std::vector<tlt_capture_entry>& entries, bool with_ar) {
+    graph_pool_clear();
+    for (const auto& e : entries) {
+        if (e.bucket_lo < 1 || e.bucket_hi < e.bucket_lo) throw ConfigErr("entries", "bad bucket range");
+        PoolBucket* pb = nullptr;
+        for (auto& q : pool_)
+            if (q.lo == e.bucket_lo && q.hi == e.bucket_hi) pb = &q;
+        if (!pb) {
+            pool_.push_back(PoolBucket{e.bucket_lo, e.bucket_hi, {}, {}});
+            pb = &pool_.back();
+        }
+        if (e.side == 0) {
+            if (std::find(pb->Ts.begin(), pb->Ts.end(), e.tokens_to_verify) == pb->Ts.end())
+                pb->Ts.push_back(e.tokens_to_verify);
+        } else if (e.side == 1) {
+            auto kd = std::make_pair((int)e.top_k, (int)e.draft_depth);
+            if (std::find(pb->kd.begin(), pb->kd.end(), kd) == pb->kd.end()) pb->kd.push_back(kd);
+        } else {
+            throw ConfigErr("entries", "side must be 0 (TARGET) or 1 (DRAFT)");
+        }
+    }
+    if (with_ar) {
+        for (int s = 1; s <= max_b_; s = s < 8 ? 2 * s : s + 8) ar_sizes_.push_back(s);
+        if (ar_sizes_.empty() || ar_sizes_.back() != max_b_) ar_sizes_.push_back(max_b_);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    size_t free0 = 0, total = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free0, &total));
+    const auto t0 = std::chrono::steady_clock::now();
+    pool_graphs_ = pool_skipped_ = 0;
+    auto warm_and_capture = [&](int b_hi, int D, int k, int T, bool ar) {
+        for (int i = 0; i < b_hi; ++i) h_step_[i] = StepIn{-1, 0, 0, 0};
+        *h_nreal_ = 0;
+        launches_in_seq_ = 0;
+        if (ar)
+            ar_device_sequence(b_hi);
+        else
+            sd_device_sequence(b_hi, D, k, T, false, 0);
+        CUDA_CHECK(cudaStreamSynchronize(st_));
+        capture_graph(std::make_tuple(b_hi, ar ? 0 : D, ar ? 0 : k, ar ? 0 : T, ar ? 1 : 0), ar);
+        ++pool_graphs_;
+    };
+    for (const auto& pb : pool_) {
+        const int b_hi = std::min(pb.hi, max_b_);
+        if (pb.lo > max_b_) continue;
+        for (int T : pb.Ts)
+            for (const auto& kd : pb.kd) {
+                tlt_strategy s{kd.second, kd.first, T};
+                try {
+                    validate(s);
+                } catch (const ConfigErr&) {
+                    continue;  // T beyond this (k, D)'s tree capacity: never selected together
+                }
+                try {
+                    warm_and_capture(b_hi, s.draft_depth, s.top_k, T, false);
+                } catch (const ConfigErr&) {
+                    ++pool_skipped_;  // exceeds the engine's draft-row buffers at this bucket size
+                }
+            }
+    }
+    for (int s : ar_sizes_) warm_and_capture(s, 0, 0, 0, true);
+    CUDA_CHECK(cudaDeviceSynchronize());
+    size_t free1 = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free1, &total));
+    pool_capture_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    pool_bytes_ = free0 > free1 ? free0 - free1 : 0;
+    return pool_bytes_;
 }
 
 void Engine::graph_pool_clear() {
+    cudaStreamSynchronize(st_);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.first);
     graphs_.clear();
+    pool_.clear();
+    ar_sizes_.clear();
 }
 
 }  // namespace tlt

@@ -80,7 +80,12 @@ public:
     int slot_len(int slot) const { return lt_.at(slot); }
     void set_debug(bool on) { debug_ = on; }
     bool use_graphs = true;
-    size_t graph_pool_build(const std::vector<tlt_capture_entry>& entries);
+    size_t graph_pool_build(const std::vector<tlt_capture_entry>& entries, bool with_ar = true);
+    size_t pool_bytes_ = 0;       // device memory taken by the last pool build
+    double pool_capture_ms_ = 0;  // host time of the last pool build
+    int pool_graphs_ = 0;         // graphs captured by the last pool build
+    int pool_skipped_ = 0;        // plan pairs not capturable (draft rows beyond the engine buffers)
+    int graph_count() const { return (int)graphs_.size(); }
     void graph_pool_clear();
     int bucket_hi_for(int b, int T) const;
     float probe_kernel(int kind, int M, int iters, double* bytes, double* flops);
@@ -223,6 +228,27 @@ private:
     int* ar_tok_ = nullptr;
     static constexpr int kMaxD = kMaxDepth;
     StepIn *d_step_ = nullptr, *h_step_ = nullptr;
+    // live request count of the current step (bucketed graphs: the step is
+    // padded to the bucket's b_hi; GEMMs skip the padding rows' tiles)
+    int *d_nreal_ = nullptr, *h_nreal_ = nullptr;
+    int dyn_b_hi_ = 0;
+    void set_dyn(EpiParams& e, int M) const;
+    struct DynScope {
+        Engine* e;
+        int prev;
+        DynScope(Engine* en, int b_hi) : e(en), prev(en->dyn_b_hi_) { en->dyn_b_hi_ = b_hi; }
+        ~DynScope() { e->dyn_b_hi_ = prev; }
+    };
+    // CUDA-graph pool built from plan_captures (tlt_graph_pool_build)
+    struct PoolBucket {
+        int lo, hi;
+        std::vector<int> Ts;                     // TARGET entries: tokens_to_verify
+        std::vector<std::pair<int, int>> kd;     // DRAFT entries: (top_k, draft_depth)
+    };
+    std::vector<PoolBucket> pool_;
+    std::vector<int> ar_sizes_;                  // padded plain-decode batch sizes
+    int ar_bucket_for(int b) const;
+    void capture_graph(const std::tuple<int, int, int, int, int>& key, bool ar);
     StepOutHost ho_{};
     int max_b_ = 0;
     // host mirrors

@@ -196,7 +196,11 @@ __global__ void __launch_bounds__(192, 1)
     const int t0 = (blockIdx.x / PAIR) * bn;
     const int z = blockIdx.z;
     const int kb0 = z * kb_per_split;
-    const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+    // padding token tile of a bucketed graph: no loads, no MMA, no epilogue
+    // (every CTA of a pair / split-K cluster shares t0, so they skip together)
+    const int m_live = epi_live_rows(ep);
+    const bool skip = t0 >= m_live;
+    const int nkb = skip ? 0 : min(kb_total, kb0 + kb_per_split) - kb0;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmW);
@@ -330,10 +334,12 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {
         // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
-        mbar_wait(tfull, 0);
-        tc_fence_after();
+        if (!skip) {
+            mbar_wait(tfull, 0);
+            tc_fence_after();
+        }
         const int q = warp & 3;
-        if (ep.dbg & 2) {
+        if (skip || (ep.dbg & 2)) {
             // diagnostics: no epilogue
         } else if (gridDim.z > 1) {
             // split-K: stage this CTA's fp32 partial in the (now idle) pipeline
@@ -377,7 +383,7 @@ __global__ void __launch_bounds__(192, 1)
         cg::cluster_group cluster = cg::this_cluster();
         cluster.sync();
         const int S = (int)gridDim.z;
-        const int tv = min(bn, ep.m_tok - t0);
+        const int tv = min(bn, m_live - t0);
         // units of 8 consecutive rows of one token: all S remote float4 pairs
         // are loaded before the fixed-order sum (DSMEM latency overlapped),
         // then the vectorised epilogue
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(192, 1)
             __threadfence();
             const int d = ep.n_out;
             const int nw = blockDim.x >> 5;
-            for (int t = warp; t < ep.m_tok; t += nw) {  // one warp per token row
+            for (int t = warp; t < m_live; t += nw) {  // one warp per live token row
                 const float* xr = ep.out_f32 + (long long)t * ep.ld_f32;
                 float ss = 0.f;
                 for (int i = lane * 4; i < d; i += 128) {
@@ -538,6 +544,13 @@ __global__ void __launch_bounds__(192, 1)
     const uint64_t pol_w = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
     const uint32_t full_bar0 = PAIR == 2 ? mapa_shared(smem_u32(&full[0]), 0) : 0u;
+    // bucketed graphs: only the token tiles holding live rows are scheduled
+    // (same tile order, the padding tiles dropped from the static schedule)
+    {
+        const int n_wt = n_tiles / n_ttiles;
+        n_ttiles = min(n_ttiles, (epi_live_rows(ep) + bn - 1) / bn);
+        n_tiles = n_ttiles * n_wt;
+    }
     // first tile's weight stages before griddepcontrol.wait (weights are not
     // produced by the previous kernel)
     const int npre = (cid < n_tiles) ? min(stages, kb_total) : 0;

@@ -62,7 +62,17 @@ struct EpiParams {
     // e4m3 GEMM dequantisation: acc * row_scale[n] * tok_scale[t] (null: none)
     const float* row_scale;
     const float* tok_scale;
+    // Bucketed CUDA graphs (capture_plan.hpp:87-126): a graph captured for
+    // the bucket's largest batch is replayed for any batch in the bucket.
+    // Rows are request-major and the padding requests come last, so only the
+    // first (*dyn_n) * dyn_rpr token rows are live; token tiles entirely past
+    // them are skipped (no weight stream, no MMA). dyn_n = null: all m_tok.
+    const int* dyn_n;
+    int dyn_rpr;
 };
+__device__ __forceinline__ int epi_live_rows(const EpiParams& p) {
+    return p.dyn_n ? min(p.m_tok, *p.dyn_n * p.dyn_rpr) : p.m_tok;
+}
 constexpr int kEpiTopkMax = 8;
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }

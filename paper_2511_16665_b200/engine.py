@@ -292,6 +292,26 @@ class Engine:
         return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
                           [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
 
+    def graph_pool_build(self, strategies, thresholds, max_batch=32, vanilla=False):
+        """Pre-capture the CUDA-graph pool of plan_captures (capture_plan.hpp:
+        87-155; vanilla = plan_captures_vanilla) and return its stats."""
+        entries, units = plan_captures(strategies, thresholds, max_batch, vanilla)
+        arr = (CaptureEntry * len(entries))(*[CaptureEntry(*e) for e in entries])
+        nbytes = C.c_size_t()
+        _check(self.L.tlt_graph_pool_build(self.h, arr, len(entries), C.byref(nbytes)))
+        st = self.graph_pool_stats()
+        st.update(plan_entries=len(entries), plan_memory_units=units)
+        return st
+
+    def graph_pool_stats(self):
+        n, sk, nl = C.c_int32(), C.c_int32(), C.c_int32()
+        nb, ms = C.c_size_t(), C.c_double()
+        _check(self.L.tlt_graph_pool_stats(self.h, C.byref(n), C.byref(sk), C.byref(nb), C.byref(ms), C.byref(nl)))
+        return dict(graphs=n.value, skipped=sk.value, bytes=nb.value, build_ms=ms.value, live_graphs=nl.value)
+
+    def graph_pool_clear(self):
+        _check(self.L.tlt_graph_pool_clear(self.h))
+
     def probe_kernel(self, kind: int, m_tok: int, iters: int = 56):
         """Live timing of one engine GEMM site (tlt_probe_kernel): returns
         (avg_ms, algorithmic_bytes, flops) of one launch."""

@@ -26,6 +26,10 @@ ARMS = {1: [(10, 8, 64), (6, 8, 64)], 5: [(10, 8, 48), (6, 8, 48)], 16: [(10, 8,
         31: [(6, 8, 16), (10, 8, 16)]}
 
 
+ARMS_ALL = [[(10, 8, 64), (6, 8, 64)], [(10, 8, 48), (6, 8, 48)], [(10, 8, 32), (6, 8, 32)],
+            [(10, 8, 16), (6, 8, 16)]]
+
+
 def _sequence(b):
     a1, a2 = ARMS[b]
     # ("ar", n) plain steps, ("sd", arm): the first SD step after AR steps runs
@@ -37,9 +41,16 @@ def _checked(b):
     return list(range(b)) if b <= 5 else [0, 1, b // 2, b - 1]
 
 
-@pytest.mark.parametrize("b", [1, 5, 16, 31])
-def test_7b_graph_replay_default_arms_oracle_in_the_loop(b):
-    eng = Engine("qwen2.5-7b", max_slots=b, max_ctx=P + 160)
+@pytest.mark.parametrize("b,pooled", [(1, False), (5, False), (16, False), (31, False), (5, True), (16, True),
+                                      (31, True)])
+def test_7b_graph_replay_default_arms_oracle_in_the_loop(b, pooled):
+    """pooled: the bucketed graph pool of plan_captures is pre-built, so every
+    step replays the graph of its bucket's largest batch (5 -> 7, 16/31 -> 32;
+    plain decode 5 -> 8, 16 -> 16, 31 -> 32) with the padding requests inert."""
+    eng = Engine("qwen2.5-7b", max_slots=32 if pooled else b, max_ctx=P + 160)
+    if pooled:
+        st = eng.graph_pool_build([a for arms in ARMS_ALL for a in arms], [1, 2, 8, 16], 32)
+        assert st["graphs"] > 0 and st["skipped"] == 0
     rng = np.random.default_rng(100 + b)
     prompts = [rng.integers(2, V, P).tolist() for _ in range(b)]
     slots = list(range(b))
@@ -71,4 +82,7 @@ def test_7b_graph_replay_default_arms_oracle_in_the_loop(b):
             assert ra == rb
         else:
             same_step(ra, rb)
+    if pooled:  # every step replayed a pre-built graph: nothing was captured on demand
+        st = eng.graph_pool_stats()
+        assert st["live_graphs"] == st["graphs"] + len({a for k, a in _sequence(b) if k == "sd"})  # + debug graphs
     eng.close()
