@@ -481,6 +481,10 @@ def run_ours(a):
     n = a.requests
     max_ctx = a.prompt + a.max_len + 8
     eng = Engine(a.model, max_slots=n, max_ctx=max_ctx, device=local)
+    # the CUDA-graph pool of plan_captures (capture_plan.hpp:87-126), pre-built
+    # before the timed region: one fused step graph per (bucket, strategy),
+    # replayed for every batch of its bucket; padded plain-decode sizes
+    pool = eng.graph_pool_build(DEFAULT_ARMS, THRESHOLDS, 32) if a.graph_pool else None
     mab = Mab(DEFAULT_ARMS, THRESHOLDS, 0.1, 20)
     # C1: with several ranks each rank's bandit records are all-gathered after
     # every rollout and merged in rank order into a shared replica (NCCL; the
@@ -572,6 +576,7 @@ def run_ours(a):
             "e2e": {"value": round(e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
+            "graph_pool": pool,
             "roofline": roof,
             "roofline_tensor_class": roof_tc,
             "per_bucket": buckets,
@@ -601,9 +606,11 @@ def main():
     ap.add_argument("--model", default="qwen2.5-7b")
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--prompt", type=int, default=256)
-    ap.add_argument("--len-median", type=float, default=400.0)
+    # response lengths lognormal(mu = ln 1500, sigma 1), max 8192
+    ap.add_argument("--len-median", type=float, default=1500.0)
     ap.add_argument("--len-sigma", type=float, default=1.0)
-    ap.add_argument("--max-len", type=int, default=2048)
+    ap.add_argument("--max-len", type=int, default=8192)
+    ap.add_argument("--graph-pool", type=int, default=1)
     ap.add_argument("--elastic", type=int, default=32)
     ap.add_argument("--ar-baseline", type=int, default=1)
     ap.add_argument("--cpu-gen", type=int, default=8)

@@ -246,6 +246,9 @@ TLT_API int tlt_mab_select(tlt_mab* m, int batch, tlt_rng* rng, int32_t* arm, tl
 TLT_API int tlt_mab_record(tlt_mab* m, const tlt_strategy* s, double elapsed, const int32_t* accept_lens, int batch);
 /* Window medians/selection counts per arm (beg_state_to_json, :174-193). */
 TLT_API int tlt_mab_arm_stats(tlt_mab* m, int arm, double* median_reward, int64_t* selections, int32_t* n_rewards);
+/* Reward / accept-length window of one arm, oldest first (the arrays of
+ * beg_state_to_json, beg_mab.hpp:174-193); *n = window fill. */
+TLT_API int tlt_mab_arm_window(tlt_mab* m, int arm, double* rewards, double* accept_lens, int cap, int32_t* n);
 /* Multi-GPU merge (C1): apply one foreign rank's record to this replica. */
 TLT_API int tlt_mab_apply_record(tlt_mab* m, int arm, double reward, double a_bar);
 /* C1 (cross-rank bandit statistics): return and clear the records this
@@ -258,6 +261,9 @@ TLT_API int tlt_mab_copy(tlt_mab* dst, const tlt_mab* src);
 TLT_API int tlt_rng_create(uint64_t seed, uint64_t stream_id, tlt_rng** out);
 TLT_API int tlt_rng_fork(const tlt_rng* r, uint64_t label, tlt_rng** out);
 TLT_API void tlt_rng_destroy(tlt_rng* r);
+/* RngStream::seed() / stream_id() (rng.hpp:43-44): a forked stream is the
+ * pair (seed, stream_id), e.g. to hand it to tlt_rollout_cfg. */
+TLT_API int tlt_rng_ids(const tlt_rng* r, uint64_t* seed, uint64_t* stream_id);
 TLT_API uint64_t tlt_rng_next_u64(tlt_rng* r);
 TLT_API double tlt_rng_uniform01(tlt_rng* r);
 
@@ -342,6 +348,10 @@ typedef struct {
      * 0: slots are released as requests finish. */
     int32_t keep_finished;
     tlt_cost_model cost;            /* all zero = reference defaults (cost_model.hpp:16-22) */
+    /* The rollout's RngStream is (seed, rng_stream) (rng.hpp:37-41): 0 = the
+     * root stream of `seed`; a caller passing rng.fork(label) hands over that
+     * fork's stream_id (tlt_rng_ids). Request / select forks as rollout.hpp:151,153. */
+    uint64_t rng_stream;
 } tlt_rollout_cfg;
 
 /* Reference RolloutResult (rollout.hpp:79-97) flattened. generated: [n][max_len]. */

@@ -72,8 +72,8 @@ __device__ __forceinline__ void attn_fused_combine(const AttnParams& p, int grp,
     __syncthreads();
     const int n_qt = gridDim.x;
     const long long cidx = ((long long)grp * p.KV + kvh) * n_qt + qtile;
-    const int tk = p.g.lc[grp] + p.g.ntail[grp], ch = split_chunk(p, tk);
-    const int n_active = min(p.max_splits, (tk + ch - 1) / ch);
+    const int n_active = split_count(p, p.g.lc[grp] + p.g.ntail[grp]);
+    if (n_active <= 1 && p.direct1) return;  // the single split wrote the final output itself
     if (threadIdx.x == 0) s_last = atomicAdd(p.counters + cidx, 1) == n_active - 1;
     __syncthreads();
     if (!s_last) return;
@@ -383,9 +383,12 @@ __global__ void __launch_bounds__(QV * 2, QV == 64 ? 2 : 1) k_attention_tree(Att
     const int slot = p.g.slot[grp];
     const int lc = p.g.lc[grp], tail0 = p.g.tail0[grp], ntail = p.g.ntail[grp];
     const int total = slot >= 0 ? lc + ntail : 0;
-    const int k0 = split * kSplit;
+    // per-request split size (whole 64-key tiles) from the request's own key count
+    const int chunk = p.dyn_splits > 0 ? split_chunk(p, total) : kSplit;
+    const int k0 = split * chunk;
     if (k0 >= total) return;  // empty split: nothing reads its partial (combine stops at the last non-empty one)
-    const int k1 = min(total, k0 + kSplit);
+    const int k1 = min(total, k0 + chunk);
+    const bool single = p.direct1 && split_count(p, total) == 1;  // write the normalised output directly
     const int row_base = qv0 / G;  // first request-local row of this CTA
 
     // ---- K/V tile loader (all threads): 64 keys x kHD of K and of V
@@ -569,11 +572,23 @@ __global__ void __launch_bounds__(QV * 2, QV == 64 ? 2 : 1) k_attention_tree(Att
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-    // ---- split partial of each of this warp's query vectors
+    // ---- split partial of each of this warp's query vectors (or, for a
+    // request served by one split, its final output)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int gqv = qv0 + wq0 + g + 8 * h;
         if (gqv >= nqv) continue;
+        if (single) {
+            if ((h ? lr1 : lr0) < 0) continue;  // padding row
+            const float inv = (h ? l1 : l0) > 0.f ? 1.0f / (h ? l1 : l0) : 0.f;
+            const int row = grp * p.rows_per_req + gqv / G;
+            bf16* dst = p.out + (long long)row * p.H * kHD + (kvh * G + gqv % G) * kHD;
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+                *reinterpret_cast<__nv_bfloat162*>(dst + n * 8 + 2 * t) =
+                    __floats2bfloat162_rn(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
+            continue;
+        }
         const long long pidx = ((long long)(grp * p.max_splits + split) * p.qv_cap + gqv) * p.KV + kvh;
         float* dst = p.ws_o + pidx * kHD;
 #pragma unroll
@@ -585,7 +600,7 @@ __global__ void __launch_bounds__(QV * 2, QV == 64 ? 2 : 1) k_attention_tree(Att
         }
     }
     }  // active
-    if (p.counters) attn_fused_combine<kHD>(p, grp, kvh, blockIdx.x, qv0, qv0 + kTQV);
+    if (p.counters && !single) attn_fused_combine<kHD>(p, grp, kvh, blockIdx.x, qv0, qv0 + kTQV);
 }
 
 template <int kHD, int QV>
@@ -652,6 +667,7 @@ __global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
     const int k0 = split * chunk;
     if (k0 >= total) return;  // empty split
     const int k1 = min(total, k0 + chunk);
+    const bool single = p.max_splits == 1 || (p.direct1 && split_count(p, total) == 1);
     const int ntiles = (k1 - k0 + kDKeys - 1) / kDKeys;
     const long long slot_base = ((long long)slot * p.KV + kvh) * p.cap;
 
@@ -837,7 +853,7 @@ __global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
                 L += wl[w * kQV + q] * sc;
                 O += wo[(w * kQV + q) * kHD + e] * sc;
             }
-        if (p.max_splits == 1) {  // single split: final normalised output, no combine
+        if (single) {  // single split: final normalised output, no combine
             const int row = s_row[q];
             if (row >= 0)
                 p.out[(long long)row * p.H * kHD + (kvh * G + q % G) * kHD + e] =
@@ -851,7 +867,7 @@ __global__ void __launch_bounds__(128) k_attention_dec(AttnParams p) {
             p.ws_l[pidx] = L;
         }
     }
-    if (p.counters && p.max_splits > 1) attn_fused_combine<kHD>(p, grp, kvh, 0, 0, kQV);
+    if (p.counters && !single) attn_fused_combine<kHD>(p, grp, kvh, 0, 0, kQV);
 }
 
 template <int kHD>
@@ -869,61 +885,41 @@ void launch_attention_dec_t(const AttnParams& p, cudaStream_t st) {
     launch_pdl(k_attention_dec<kHD>, grid, 128, smem, st, p);
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
 // Target split count per (request, KV head) for the per-request split sizing
-// (split_chunk); 0 = per-request sizing off (TLT_ATTN_DEC_DYN=0).
+// (split_chunk); 0 = per-request sizing off (TLT_ATTN_DEC_DYN=0). Knobs are
+// read per call (host side, once per captured launch).
 int attention_dec_target_splits(int n_groups, int kv) {
-    static const int dyn = [] {
-        const char* v = std::getenv("TLT_ATTN_DEC_DYN");
-        return v ? std::atoi(v) : 1;
-    }();
-    if (!dyn) return 0;
-    static const int target_ctas = [] {
-        const char* v = std::getenv("TLT_ATTN_DEC_CTAS");
-        return v ? std::atoi(v) : 296;
-    }();
+    if (!env_int("TLT_ATTN_DEC_DYN", 1)) return 0;
+    const int target_ctas = env_int("TLT_ATTN_DEC_CTAS", 296);
     return n_groups * kv >= target_ctas ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
 }
 
+// Fixed split size (TLT_ATTN_DEC_DYN=0): chunk so that (groups x KV heads x
+// splits) ~ 2 CTAs per SM. Any multiple of the 64-key tile works for this
+// kernel: 64-key granularity balances the splits (b = 16: 4 x 320 keys
+// instead of 2 x 512 + 1; 26.7 -> 22.6 us per layer), and a 256-key floor
+// keeps the long-tail shapes from fragmenting into many tiny splits whose
+// combine costs more than it saves (b = 1: 16.5 us vs 18.5 us at 64 keys;
+// profiles/r1_attn_dec_granularity.txt). Returns 0 when the decode kernel is
+// off (TLT_ATTN_DEC=0).
 int attention_dec_chunk(int n_groups, int kv, int max_keys) {
-    // chunk (multiple of 256 keys) so that (groups x KV heads x splits) ~ 2 CTAs per SM
-    static const int off = [] {
-        const char* v = std::getenv("TLT_ATTN_DEC");
-        return v ? std::atoi(v) : 1;
-    }();
-    if (!off) return 0;
-    static const int target_ctas = [] {
-        const char* v = std::getenv("TLT_ATTN_DEC_CTAS");
-        return v ? std::atoi(v) : 296;
-    }();
-    // split granularity (keys): any multiple of the 64-key tile works for this
-    // kernel. 64-key granularity balances the splits (b = 16: 4 x 320 keys
-    // instead of 2 x 512 + 1; 26.7 -> 22.6 us per layer), and a 256-key floor
-    // keeps the long-tail shapes from fragmenting into many tiny splits whose
-    // combine costs more than it saves (b = 1: 16.5 us vs 18.5 us at 64 keys;
-    // profiles/r1_attn_dec_granularity.txt)
-    static const int gran = [] {
-        const char* v = std::getenv("TLT_ATTN_DEC_GRAN");
-        const int g = v ? std::atoi(v) : kDKeys;
-        return std::max(kDKeys, (g / kDKeys) * kDKeys);
-    }();
-    static const int min_chunk = [] {
-        const char* v = std::getenv("TLT_ATTN_DEC_MIN_CHUNK");
-        return v ? std::max(kDKeys, std::atoi(v)) : 256;
-    }();
+    if (!env_int("TLT_ATTN_DEC", 1)) return 0;
+    const int target_ctas = env_int("TLT_ATTN_DEC_CTAS", 296);
+    const int gran = std::max(kDKeys, env_int("TLT_ATTN_DEC_GRAN", kDKeys) / kDKeys * kDKeys);
+    const int min_chunk = std::max(kDKeys, env_int("TLT_ATTN_DEC_MIN_CHUNK", 256));
     const int chunks = std::max(1, (max_keys + gran - 1) / gran);
     // (request, head) pairs alone reach the CTA target: a single split (the
     // kernel then writes the normalised output itself, no partials, no combine)
     const int want_splits = n_groups * kv >= target_ctas ? 1 : std::max(1, target_ctas / std::max(1, n_groups * kv));
-    static const int even = [] {
-        const char* v = std::getenv("TLT_ATTN_DEC_EVEN");
-        return v ? std::atoi(v) : 1;
-    }();
-    if (even && max_keys <= min_chunk + min_chunk / 2) {
+    if (env_int("TLT_ATTN_DEC_EVEN", 1) && max_keys <= min_chunk + min_chunk / 2) {
         // short contexts (<= 384 keys) run as ONE split: no remainder split,
         // no partials, no combine launch (b=1 ctx 257: 14.4 -> 13.1 us; b=4:
-        // 16.5 -> 14.4 us). Longer contexts keep 256-key-floored splits: the
-        // per-CTA tile count is the critical path there (b=1 ctx 1025: 5 x 256
-        // beats 4 x 320, 16.5 vs 18.5 us; profiles/r1_attn_dec_even.txt)
+        // 16.5 -> 14.4 us; profiles/r1_attn_dec_even.txt)
         return std::max(gran, (max_keys + gran - 1) / gran * gran);
     }
     const int per = std::max(1, (chunks + want_splits - 1) / want_splits);
@@ -954,6 +950,49 @@ void launch_attention_mma_t(const AttnParams& p, cudaStream_t st) {
 
 int attention_mma_split() { return kSplit; }
 
+// Split plan of one attention launch over requests of up to max_keys keys
+// (the grid is sized for that bound; each CTA sizes its split from its own
+// request's key count, split_chunk). Decode (<= 16 query vectors per
+// (request, KV head)): flash-decode kernel. Tree verify / drafter levels:
+// the 64-query-vector tree kernel with (request, KV head, q-tile) x splits
+// aiming at TLT_ATTN_TREE_CTAS CTAs (default 148: one fat CTA per SM beats
+// several waves of short ones — the per-CTA prologue and the split combine
+// are the latency floor at these shapes), whole 64-key tiles, at least
+// TLT_ATTN_TREE_MIN_CHUNK keys per split. A request served by one split
+// writes its output directly (no partials, no combine).
+void attention_plan_splits(AttnParams& p, int max_keys) {
+    const int G = p.H / p.KV;
+    const int nqv = p.rows_per_req * G;
+    p.chunk = p.impl == 1 ? kSplit : 512;
+    p.dec = 0;
+    p.dyn_splits = 0;
+    p.gran = kDKeys;
+    p.min_chunk = kSplit;
+    p.direct1 = 0;
+    if (p.impl == 1 && nqv <= 16) {
+        const int ch = attention_dec_chunk(p.n_groups, p.KV, max_keys);
+        if (ch > 0) {
+            p.chunk = ch;
+            p.dec = 1;
+            p.dyn_splits = attention_dec_target_splits(p.n_groups, p.KV);
+            p.gran = std::max(kDKeys, env_int("TLT_ATTN_DEC_GRAN", kDKeys) / kDKeys * kDKeys);
+            p.min_chunk = std::max(p.gran, env_int("TLT_ATTN_DEC_MIN_CHUNK", 256) / kDKeys * kDKeys);
+            p.direct1 = 1;
+        }
+    } else if (p.impl == 1 && G >= 2 && nqv >= env_int("TLT_ATTN_TREE_MIN_QV", 17) && env_int("TLT_ATTN_TREE_DYN", 1)) {
+        const int qv = env_int("TLT_ATTN_TREE_QV", 64);
+        const long long pairs = (long long)p.n_groups * p.KV * ((nqv + qv - 1) / qv);
+        const int target = env_int("TLT_ATTN_TREE_CTAS", 148);
+        p.dyn_splits = pairs >= target ? 1 : (int)std::max(1LL, target / std::max(1LL, pairs));
+        p.gran = kTKeys;
+        p.min_chunk = std::max(kTKeys, env_int("TLT_ATTN_TREE_MIN_CHUNK", 256) / kTKeys * kTKeys);
+        p.chunk = p.min_chunk;
+        p.direct1 = 1;
+    }
+    p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+    if (p.dyn_splits > 0) p.max_splits = std::max(1, std::min(p.dyn_splits, (max_keys + p.min_chunk - 1) / p.min_chunk));
+}
+
 void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc) {
     if (allow_tc && attention_tc_eligible(p)) {  // tcgen05 / TMEM kernel (attn_tc.cu)
         launch_attention_tc(p, st);
@@ -973,7 +1012,7 @@ void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc) {
     }();
     const long long tree_ctas =
         (long long)((p.rows_per_req * G + tree_qv - 1) / tree_qv) * p.KV * p.n_groups * p.max_splits;
-    if (p.rows_per_req * G >= tree_min && G >= 2 && tree_ctas >= 128) {
+    if (p.rows_per_req * G >= tree_min && G >= 2 && (tree_ctas >= 128 || p.dyn_splits > 0)) {
         if (tree_qv == 128) {
             if (p.hd == 128)
                 launch_attention_tree_t<128, 128>(p, st);

@@ -310,6 +310,18 @@ TLT_API int tlt_mab_arm_stats(tlt_mab* m, int arm, double* median_reward, int64_
         if (n_rewards) *n_rewards = (int32_t)a.rewards.size();
     });
 }
+TLT_API int tlt_mab_arm_window(tlt_mab* m, int arm, double* rewards, double* accept_lens, int cap, int32_t* n) {
+    if (!m || !n) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        if (arm < 0 || arm >= (int)m->m->arms.size()) throw tlt::ConfigErr("arm", "out of range");
+        const auto& a = m->m->arms[arm];
+        *n = (int32_t)a.rewards.size();
+        for (int i = 0; i < (int)a.rewards.size() && i < cap; ++i) {
+            if (rewards) rewards[i] = a.rewards[i];
+            if (accept_lens) accept_lens[i] = a.accept_lens[i];
+        }
+    });
+}
 TLT_API int tlt_mab_apply_record(tlt_mab* m, int arm, double reward, double a_bar) {
     if (!m) return fail(TLT_ERR_STATE, "null argument");
     return guard([&] {
@@ -353,6 +365,12 @@ TLT_API int tlt_rng_fork(const tlt_rng* r, uint64_t label, tlt_rng** out) {
     return TLT_OK;
 }
 TLT_API void tlt_rng_destroy(tlt_rng* r) { delete r; }
+TLT_API int tlt_rng_ids(const tlt_rng* r, uint64_t* seed, uint64_t* stream_id) {
+    if (!r) return fail(TLT_ERR_CONFIG, "null argument");
+    if (seed) *seed = r->r.seed();
+    if (stream_id) *stream_id = r->r.stream_id();
+    return TLT_OK;
+}
 TLT_API uint64_t tlt_rng_next_u64(tlt_rng* r) { return r->r.next_u64(); }
 TLT_API double tlt_rng_uniform01(tlt_rng* r) { return r->r.uniform01(); }
 
@@ -409,7 +427,7 @@ TLT_API int tlt_run_rollout(tlt_engine* e, const tlt_rollout_cfg* cfg, tlt_mab* 
             if (max_lens[i] < 1) throw tlt::ConfigErr("requests", "max_len must be >= 1");
             if (max_lens[i] > max_len_stride) throw tlt::ConfigErr("max_len_stride", "smaller than max_len");
         }
-        tlt::Rng root(cfg->seed, 0);
+        tlt::Rng root(cfg->seed, cfg->rng_stream);  // the caller's RngStream (seed, stream_id)
         std::vector<tlt::Rng> req_rng;
         for (int i = 0; i < n; ++i) req_rng.push_back(root.fork(0x52515254ULL + (uint64_t)request_ids[i]));
         tlt::Rng select_rng = root.fork(0x53454CULL);

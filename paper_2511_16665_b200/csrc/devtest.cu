@@ -136,8 +136,14 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
         p.cap = cap;
         p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
         p.impl = 1;
-        p.chunk = attention_mma_split();
-        p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+        // kernel 0/1: fixed 256-key splits (legacy / tcgen05 kernels); 2/3/4:
+        // the engine's split plan (flash-decode or tree kernel)
+        if (kernel >= 2) {
+            attention_plan_splits(p, max_keys);
+        } else {
+            p.chunk = attention_mma_split();
+            p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
+        }
         p.qv_cap = rows_per_req * (H / KV);
         const size_t need = (size_t)n_groups * p.max_splits * p.qv_cap * KV;
         float *wm = nullptr, *wl = nullptr, *wo = nullptr;
@@ -159,12 +165,7 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
             // request and KV head); 3 = split combine fused into the last CTA
             int* ctr = nullptr;
             if (rows_per_req * (H / KV) > 16) throw ConfigErr("kernel", "decode kernel needs <= 16 query vectors");
-            p.chunk = attention_dec_chunk(n_groups, KV, max_keys);
-            if (p.chunk <= 0) throw ConfigErr("kernel", "decode kernel disabled (TLT_ATTN_DEC=0)");
-            p.dec = 1;
-            p.dyn_splits = attention_dec_target_splits(n_groups, KV);
-            p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
-            if (p.dyn_splits > 0) p.max_splits = std::max(1, std::min(p.dyn_splits, (max_keys + 255) / 256));
+            if (!p.dec) throw ConfigErr("kernel", "decode kernel disabled (TLT_ATTN_DEC=0)");
             if (kernel == 3) {
                 CUDA_CHECK(cudaMalloc(&ctr, sizeof(int) * n_groups * KV));
                 CUDA_CHECK(cudaMemset(ctr, 0, sizeof(int) * n_groups * KV));
@@ -179,6 +180,11 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
                 for (int v : h)
                     if (v != 0) throw ConfigErr("counters", "fused combine left a non-zero counter");
             }
+        } else if (kernel == 4) {
+            // tree kernel as the engine plans it (per-request splits, direct
+            // single-split outputs, separate combine)
+            if (rows_per_req * (H / KV) <= 16) throw ConfigErr("kernel", "tree kernel needs > 16 query vectors");
+            launch_attention(p, 0);
         } else {
             p.impl = 1;
             launch_attention_legacy(p, 0);

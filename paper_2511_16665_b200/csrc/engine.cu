@@ -417,18 +417,7 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
     p.cap = cache_cap;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)cfg.head_dim));
     p.impl = attn_impl_;
-    p.chunk = p.impl == 1 ? attention_mma_split() : 512;
-    if (p.impl == 1 && rpr * (cfg.heads / cfg.kv_heads) <= 16) {
-        const int ch = attention_dec_chunk(ngroups, cfg.kv_heads, max_keys);
-        if (ch > 0) {
-            p.chunk = ch;
-            p.dec = 1;
-            p.dyn_splits = attention_dec_target_splits(ngroups, cfg.kv_heads);
-        }
-    }
-    p.max_splits = std::max(1, (max_keys + p.chunk - 1) / p.chunk);
-    // per-request split sizing: the grid covers the bound split_chunk can reach
-    if (p.dyn_splits > 0) p.max_splits = std::max(1, std::min(p.dyn_splits, (max_keys + 255) / 256));
+    attention_plan_splits(p, max_keys);  // per-request split sizing; grid covers the max_keys bound
     p.qv_cap = rpr * (cfg.heads / cfg.kv_heads);
     const size_t need = (size_t)ngroups * p.max_splits * p.qv_cap * cfg.kv_heads;
     if (need * cfg.head_dim > aws_elems_ || need > aws_elems_ / 32)
@@ -1008,17 +997,33 @@ float Engine::probe_attention(int b, int ctx, int rpr, int iters, double* bytes)
         }
     }
     upload_rows_host(tok, pos, slot, cidx, fk, fidx, mask, gs, glc, gt0, gnt);
-    float ms = 0.f;
-    for (int rep = 0; rep < 2; ++rep) {  // warm-up, then timed
-        CUDA_CHECK(cudaEventRecord(ev0_, st_));
+    // the engine replays its attention launches inside CUDA graphs (PDL
+    // edges between kernels): the probe does the same — eager warm-up, then
+    // the `iters` launches captured once and the graph replay timed
+    auto seq = [&] {
         for (int it = 0; it < iters; ++it) {
             const int l = it % cfg.layers;
             attention(kc_[l], vc_[l], cap_, prows_, pg_, rpr, b, cap_);  // grid sized as in the engine
         }
+    };
+    seq();
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    cudaGraph_t g;
+    CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    seq();
+    CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+    cudaGraphExec_t ex;
+    CUDA_CHECK(cudaGraphInstantiate(&ex, g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+    float ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {  // warm replay, then timed
+        CUDA_CHECK(cudaEventRecord(ev0_, st_));
+        CUDA_CHECK(cudaGraphLaunch(ex, st_));
         CUDA_CHECK(cudaEventRecord(ev1_, st_));
         CUDA_CHECK(cudaEventSynchronize(ev1_));
         CUDA_CHECK(cudaEventElapsedTime(&ms, ev0_, ev1_));
     }
+    CUDA_CHECK(cudaGraphExecDestroy(ex));
     const double kv = (double)b * (ctx + rpr) * cfg.kv_heads * cfg.head_dim * 2 * 2;
     const double qo = (double)R * cfg.heads * cfg.head_dim * 2 * 2;
     if (bytes) *bytes = kv + qo;

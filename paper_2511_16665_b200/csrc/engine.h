@@ -85,7 +85,11 @@ public:
     double pool_capture_ms_ = 0;  // host time of the last pool build
     int pool_graphs_ = 0;         // graphs captured by the last pool build
     int pool_skipped_ = 0;        // plan pairs not capturable (draft rows beyond the engine buffers)
-    int graph_count() const { return (int)graphs_.size(); }
+    int graph_count() const {  // production graphs (debug-export variants excluded)
+        int n = 0;
+        for (const auto& kv : graphs_) n += std::get<4>(kv.first) != 4;
+        return n;
+    }
     void graph_pool_clear();
     int bucket_hi_for(int b, int T) const;
     float probe_kernel(int kind, int M, int iters, double* bytes, double* flops);

@@ -23,8 +23,12 @@ struct AttnParams {
     int impl;  // 0: CUDA-core reference kernel, 1: tensor-core flash-decode (attn_mma.cu)
     int* counters;  // non-null: fused split combine (last CTA per tile), zeroed buffer
     int dec;        // 1: decode kernel (<= 16 query vectors per request/head), chunk = multiple of 256
-    int dyn_splits; // > 0 (decode only): split size chosen per request from its ACTUAL key count
-                    // (split_chunk below) for this many target splits; 0 = fixed p.chunk
+    int dyn_splits; // > 0: split size chosen per request from its ACTUAL key count (split_chunk
+                    // below) for this many target splits; 0 = fixed p.chunk
+    int gran;       // dyn_splits > 0: split granularity in keys (a multiple of the 64-key tile)
+    int min_chunk;  // dyn_splits > 0: shortest split (keys); the host sizes max_splits with it
+    int direct1;    // 1: a request whose keys fit one split gets its output written by the attention
+                    // kernel itself (the combine skips it)
     // optional L2 warm-up of the NEXT kernel's weights (the o-proj): the
     // attention kernels are latency-bound and leave HBM idle, so each CTA
     // issues a bulk L2 prefetch of its slice of [pf, pf + pf_bytes)
@@ -41,9 +45,16 @@ struct AttnParams {
 // ceil(total / 256)), which is what the host sizes max_splits for.
 __host__ __device__ __forceinline__ int split_chunk(const AttnParams& p, int total) {
     if (p.dyn_splits <= 0) return p.chunk;
-    const int tiles = (total + 63) / 64;
+    const int tiles = (total + p.gran - 1) / p.gran;
     const int per = (tiles + p.dyn_splits - 1) / p.dyn_splits;
-    return per * 64 < 256 ? 256 : per * 64;
+    return per * p.gran < p.min_chunk ? p.min_chunk : per * p.gran;
+}
+// Active splits of a request (<= max_splits, which the host sizes as
+// min(dyn_splits, ceil(max_keys / min_chunk))).
+__host__ __device__ __forceinline__ int split_count(const AttnParams& p, int total) {
+    const int ch = split_chunk(p, total);
+    const int n = (total + ch - 1) / ch;
+    return n < p.max_splits ? n : p.max_splits;
 }
 void launch_attention_mma(const AttnParams& p, cudaStream_t st, bool allow_tc = true);
 // test hooks: the mma.sync kernels + combine, and the combine alone
@@ -58,6 +69,9 @@ void launch_attention_tc(const AttnParams& p, cudaStream_t st);
 int attention_mma_split();
 int attention_dec_chunk(int n_groups, int kv, int max_keys);
 int attention_dec_target_splits(int n_groups, int kv);
+// split sizing shared by the engine and the test entry: fills p.chunk / dec /
+// dyn_splits / gran / min_chunk / max_splits for max_keys keys per request
+void attention_plan_splits(AttnParams& p, int max_keys);
 
 struct TreeParams {
     const StepIn* step;

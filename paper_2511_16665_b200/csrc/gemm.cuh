@@ -106,6 +106,7 @@ __device__ __forceinline__ void epi_pair(const EpiParams& p, int t, int n, float
             p.out_bf16[(long long)t * p.ld_bf16 + (n >> 1)] = __float2bfloat16_rn(silu_f(g) * u);
         } break;
         case EPI_QKV: {
+            if (p.tok_slot[t] < 0) return;  // padding row: no valid position
             if (p.bias) {
                 v0 += __bfloat162float(p.bias[n]);
                 v1 += __bfloat162float(p.bias[n + 1]);
@@ -187,6 +188,9 @@ __device__ __forceinline__ void epi_vec8(const EpiParams& p, int t, int n, const
             *reinterpret_cast<uint2*>(p.out_bf16 + (long long)t * p.ld_bf16 + (n >> 1)) = u;
         } break;
         case EPI_QKV: {
+            // padding rows (slot < 0: unused tree slots, padding requests of a
+            // bucketed graph) carry no valid position: nothing to rotate or write
+            if (p.tok_slot[t] < 0) return;
             float w[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) w[i] = v[i];

@@ -27,6 +27,8 @@ public:
     uint64_t next_u64() { return eng_(); }
     double uniform01() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
     uint64_t uniform_int(uint64_t n) { return next_u64() % n; }
+    uint64_t seed() const { return seed_; }
+    uint64_t stream_id() const { return stream_; }
 
 private:
     static uint64_t splitmix(uint64_t& x) {

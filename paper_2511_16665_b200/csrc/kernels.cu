@@ -108,7 +108,63 @@ __global__ void k_rmsnorm(const float* __restrict__ x, int d, const bf16* __rest
     for (int i = threadIdx.x; i < d; i += blockDim.x)
         out[(long long)r * d + i] = __float2bfloat16_rn(xr[i] * inv * __bfloat162float(g[i]));
 }
+// Vectorised variant (d % 4 == 0): the row is read ONCE with 16-byte loads
+// into registers (VPT float4 per thread), reduced in a fixed order, and
+// written as 8-byte groups of four bf16 — one HBM pass over x, no re-read.
+template <int VPT>
+__global__ void __launch_bounds__(256) k_rmsnorm_vec(const float* __restrict__ x, int d, const bf16* __restrict__ g,
+                                                     float eps, bf16* __restrict__ out) {
+    pdl_wait();
+    __shared__ float red[8];
+    const int r = blockIdx.x;
+    const int d4 = d >> 2;
+    const float4* xr = reinterpret_cast<const float4*>(x + (long long)r * d);
+    float4 v[VPT];
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        v[j] = i < d4 ? __ldg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];  // fixed order
+    const float inv = 1.0f / sqrtf(tot / (float)d + eps);
+    uint2* orow = reinterpret_cast<uint2*>(out + (long long)r * d);
+    const uint2* g4 = reinterpret_cast<const uint2*>(g);
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        if (i >= d4) break;
+        const uint2 gw = __ldg(g4 + i);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gw);
+        const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+        uint2 o;
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+        o2[0] = __floats2bfloat162_rn(v[j].x * inv * ga.x, v[j].y * inv * ga.y);
+        o2[1] = __floats2bfloat162_rn(v[j].z * inv * gb.x, v[j].w * inv * gb.y);
+        orow[i] = o;
+    }
+}
+
 void launch_rmsnorm(const float* x, int R, int d, const bf16* g, float eps, bf16* out, cudaStream_t st) {
+    const int d4 = d / 4;
+    if (d % 4 == 0 && d4 <= 8 * 256) {
+        const int threads = d4 <= 8 * 128 ? 128 : 256;
+        const int vpt = (d4 + threads - 1) / threads;
+        switch (vpt) {
+#define TLT_NORM_CASE(V) \
+    case V: launch_pdl(k_rmsnorm_vec<V>, R, threads, 0, st, x, d, g, eps, out); return;
+            TLT_NORM_CASE(1) TLT_NORM_CASE(2) TLT_NORM_CASE(3) TLT_NORM_CASE(4)
+            TLT_NORM_CASE(5) TLT_NORM_CASE(6) TLT_NORM_CASE(7) TLT_NORM_CASE(8)
+#undef TLT_NORM_CASE
+            default: break;
+        }
+    }
     launch_pdl(k_rmsnorm, R, 256, 0, st, x, d, g, eps, out);
 }
 
@@ -360,9 +416,8 @@ __global__ void k_attn_combine(AttnParams p) {
     const int row = grp * p.rows_per_req + gqv / G;
     const int head = kvh * G + gqv % G;
     if (p.rows.slot[row] < 0) return;
-    const int total_keys = p.g.lc[grp] + p.g.ntail[grp];
-    const int ch = split_chunk(p, total_keys);
-    const int nsplit = min(p.max_splits, (total_keys + ch - 1) / ch);
+    const int nsplit = split_count(p, p.g.lc[grp] + p.g.ntail[grp]);
+    if (nsplit <= 1 && p.direct1) return;  // written by the attention kernel itself
     constexpr int DPL = HD / 32;
     float M = -CUDART_INF_F;
     for (int s = 0; s < nsplit; ++s) {
@@ -1070,6 +1125,10 @@ __global__ void __launch_bounds__(kTreeThreads) k_tree_level(TreeParams p) {
         for (int f = threadIdx.x; f < p.nxt_F; f += blockDim.x) {
             const int r = p.nxt_base + i * p.nxt_F + f;
             p.rows.slot[r] = -1;
+            p.rows.tok[r] = 0;
+            p.rows.pos[r] = 0;
+            p.rows.cidx[r] = 0;
+            p.rows.fkind[r] = 0;
             p.row_node[r] = -1;
         }
         if (threadIdx.x == 0) {

@@ -96,7 +96,8 @@ class RolloutCfg(C.Structure):
                 ("temperature", C.c_float), ("fixed_strategy", Strategy), ("use_mab", C.c_int32),
                 ("seed", C.c_uint64), ("use_graphs", C.c_int32), ("drafter_stale", C.c_int32),
                 ("ngram_n", C.c_int32), ("ngram_continuation_len", C.c_int32), ("target_step_id", C.c_int64),
-                ("parity_elapsed", C.c_int32), ("keep_finished", C.c_int32), ("cost", CostModel)]
+                ("parity_elapsed", C.c_int32), ("keep_finished", C.c_int32), ("cost", CostModel),
+                ("rng_stream", C.c_uint64)]
 
 
 class StepMetrics(C.Structure):
@@ -180,6 +181,7 @@ class Engine:
         self.vocab = m["vocab"]
         self.hidden = m["hidden"]
         self.device = device
+        self.max_slots, self.max_ctx = max_slots, max_ctx
 
     def close(self):
         if getattr(self, "h", None):
@@ -465,7 +467,7 @@ class Engine:
     def run_rollout(self, prompts, max_lens, request_ids=None, *, enable_sd=True, elastic_threshold=32,
                     strategy=(4, 4, 16), mab: "Mab | None" = None, seed=0, use_graphs=True, mode="greedy",
                     temperature=0.0, drafter_stale=False, ngram_n=2, ngram_continuation_len=8, target_step_id=0,
-                    parity_elapsed=False, keep_finished=False, cost=None, trace_cap=1 << 16):
+                    parity_elapsed=False, keep_finished=False, cost=None, trace_cap=1 << 16, rng_stream=0):
         """Reference run_rollout (rollout.hpp:130-276). Returns the RolloutResult
         fields (requests' tokens and finish_time, trace of StepMetrics,
         accept_at_least, counters) as a dict."""
@@ -481,7 +483,7 @@ class Engine:
                          float(temperature), Strategy(*strategy),
                          1 if mab is not None else 0, seed, 1 if use_graphs else 0, 1 if drafter_stale else 0,
                          ngram_n, ngram_continuation_len, target_step_id, 1 if parity_elapsed else 0,
-                         1 if keep_finished else 0, cost if cost is not None else CostModel())
+                         1 if keep_finished else 0, cost if cost is not None else CostModel(), rng_stream)
         res = RolloutResult(gen.ctypes.data, glen.ctypes.data)
         aal = np.zeros(64, np.int64)
         fin = np.zeros(n, np.float64)
@@ -528,6 +530,22 @@ class Rng:
 
     def uniform01(self):
         return self.L.tlt_rng_uniform01(self.h)
+
+    def uniform_int(self, n):
+        """RngStream::uniform_int (rng.hpp:59-61): next_u64() % n."""
+        return self.next_u64() % n
+
+    def normal(self):
+        """RngStream::normal (rng.hpp:64-69), Box-Muller over two uniform01 draws."""
+        import math
+        u1, u2 = self.uniform01(), self.uniform01()
+        return math.sqrt(-2.0 * math.log1p(-u1)) * math.cos(6.283185307179586477 * u2)
+
+    def ids(self):
+        """(seed, stream_id) of this stream (rng.hpp:43-44)."""
+        sd, st = C.c_uint64(), C.c_uint64()
+        _check(self.L.tlt_rng_ids(self.h, C.byref(sd), C.byref(st)))
+        return sd.value, st.value
 
     def __del__(self):
         try:
@@ -600,6 +618,16 @@ class Mab:
         med, sel, n = C.c_double(), C.c_int64(), C.c_int32()
         _check(self.L.tlt_mab_arm_stats(self.h, arm, C.byref(med), C.byref(sel), C.byref(n)))
         return med.value, sel.value, n.value
+
+    def arm_window(self, arm, cap=4096):
+        """(rewards, accept_lens) windows of one arm, oldest first."""
+        rw = np.zeros(cap, np.float64)
+        al = np.zeros(cap, np.float64)
+        n = C.c_int32()
+        _check(self.L.tlt_mab_arm_window(self.h, arm, rw.ctypes.data_as(C.c_void_p), al.ctypes.data_as(C.c_void_p),
+                                         cap, C.byref(n)))
+        k = min(n.value, cap)
+        return rw[:k].tolist(), al[:k].tolist()
 
     def apply_record(self, arm, reward, a_bar):
         _check(self.L.tlt_mab_apply_record(self.h, arm, C.c_double(reward), C.c_double(a_bar)))

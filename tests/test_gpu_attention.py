@@ -11,6 +11,8 @@ pytestmark = pytest.mark.gpu
 
 
 def make_case(n_groups, rpr, lc, H=28, KV=4, hd=128, cap=2400, seed=0, remap_tail=False):
+    """lc: committed keys, one int for every group or a per-group list (ragged)."""
+    lcs = list(lc) if isinstance(lc, (list, tuple)) else [lc] * n_groups
     g = torch.Generator(device="cuda").manual_seed(seed)
     dev = "cuda"
     slots = n_groups
@@ -34,20 +36,21 @@ def make_case(n_groups, rpr, lc, H=28, KV=4, hd=128, cap=2400, seed=0, remap_tai
     mask_dev = torch.tensor((mask & 0xFFFFFFFF).numpy().astype("uint32").view("int32"), device=dev)
     row_slot = torch.arange(n_groups, device=dev, dtype=torch.int32).repeat_interleave(rpr)
     g_slot = torch.arange(n_groups, device=dev, dtype=torch.int32)
-    g_lc = torch.full((n_groups,), lc, device=dev, dtype=torch.int32)
-    tail0 = lc + 64 if remap_tail else lc
-    g_tail0 = torch.full((n_groups,), tail0, device=dev, dtype=torch.int32)
+    g_lc = torch.tensor(lcs, device=dev, dtype=torch.int32)
+    tail0 = [x + 64 if remap_tail else x for x in lcs]
+    g_tail0 = torch.tensor(tail0, device=dev, dtype=torch.int32)
     g_ntail = torch.full((n_groups,), rpr, device=dev, dtype=torch.int32)
     return dict(kc=kc, vc=vc, q=q, vis=vis, mask=mask_dev, row_slot=row_slot, g_slot=g_slot, g_lc=g_lc,
-                g_tail0=g_tail0, g_ntail=g_ntail, n_groups=n_groups, rpr=rpr, lc=lc, H=H, KV=KV, hd=hd, cap=cap,
+                g_tail0=g_tail0, g_ntail=g_ntail, n_groups=n_groups, rpr=rpr, lc=lcs, H=H, KV=KV, hd=hd, cap=cap,
                 tail0=tail0)
 
 
 def reference(c):
-    H, KV, hd, rpr, lc, G = c["H"], c["KV"], c["hd"], c["rpr"], c["lc"], c["H"] // c["KV"]
+    H, KV, hd, rpr, G = c["H"], c["KV"], c["hd"], c["rpr"], c["H"] // c["KV"]
     out = torch.zeros(c["n_groups"] * rpr, H * hd, device="cuda")
     for i in range(c["n_groups"]):
-        keys = torch.cat([torch.arange(lc), c["tail0"] + torch.arange(rpr)]).cuda()
+        lc = c["lc"][i]
+        keys = torch.cat([torch.arange(lc), c["tail0"][i] + torch.arange(rpr)]).cuda()
         for h in range(H):
             kvh = h // G
             K = c["kc"][i, kvh, keys].float()
@@ -94,3 +97,40 @@ def test_decode_attention_fused_combine(n_groups, lc):
     err = (sep - ref).abs()
     assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
     assert torch.equal(sep, fused)
+
+
+RAGGED = [1, 255, 257, 700, 2000, 64, 0, 1500]
+
+
+@pytest.mark.parametrize("dyn", ["0", "1"])
+@pytest.mark.parametrize("n_groups", [5, 8, 40])
+def test_decode_attention_ragged_requests(monkeypatch, n_groups, dyn):
+    """requests of one batch with different key counts get their
+    own split count (per-request sizing, DYN=1) or the fixed chunk (DYN=0);
+    the separate and the fused combine agree bit for bit and with torch."""
+    monkeypatch.setenv("TLT_ATTN_DEC_DYN", dyn)
+    lcs = [RAGGED[i % len(RAGGED)] for i in range(n_groups)]
+    c = make_case(n_groups, 1, lcs, seed=31 * n_groups)
+    ref = reference(c)
+    sep = run(c, 2)
+    fused = run(c, 3)
+    err = (sep - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+    assert torch.equal(sep, fused)
+
+
+@pytest.mark.parametrize("ctas,min_chunk", [("148", "256"), ("592", "64"), ("1", "256")])
+@pytest.mark.parametrize("n_groups,rpr,remap", [(1, 65, True), (5, 49, False), (3, 17, True), (31, 17, False)])
+def test_tree_attention_engine_split_plan(monkeypatch, n_groups, rpr, remap, ctas, min_chunk):
+    """The tree kernel as the engine plans it (kernel 4): per-request split
+    sizes from each request's own key count (ragged batches), requests that
+    fit one split written directly by the attention kernel, the rest merged
+    by the combine; every split plan within bf16 tolerance of torch."""
+    monkeypatch.setenv("TLT_ATTN_TREE_CTAS", ctas)
+    monkeypatch.setenv("TLT_ATTN_TREE_MIN_CHUNK", min_chunk)
+    lcs = [RAGGED[(i * 3) % len(RAGGED)] for i in range(n_groups)]
+    c = make_case(n_groups, rpr, lcs, seed=n_groups * 7 + rpr, remap_tail=remap)
+    ref = reference(c)
+    got = run(c, 4)
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())

@@ -55,22 +55,35 @@ def test_mab_rollout_replays_only_pooled_graphs_and_is_lossless():
 
 @pytest.mark.parametrize("b,strategy", [(5, (6, 8, 48)), (3, (10, 8, 48)), (11, (6, 8, 32)), (20, (6, 8, 16))])
 def test_padded_step_equals_exact_step(b, strategy):
+    """The padded step emits the same tokens as the exact-batch step. (Trees
+    and acceptance may differ where drafter probabilities nearly tie: the
+    padded GEMMs run a different tile / split-K plan, so logits differ in the
+    last bits — SURVEY.md §7 "batch invariance"; the padded step itself is
+    checked bit for bit against the oracle fed its own rows in
+    test_gpu_parity_graphs.py.) The first step, from identical state, and
+    every plain-decode step must agree exactly."""
     rng = np.random.default_rng(b)
     prompts = [rng.integers(2, V, 14).tolist() for _ in range(b)]
     slots = list(range(b))
-    res = []
+    streams, firsts = [], []
     for pooled in (False, True):
         eng = Engine("tiny", max_slots=32, max_ctx=512)
         if pooled:
             eng.graph_pool_build(ARMS, THR, 32)
         eng.prefill(slots, prompts)
-        outs = []
-        for _ in range(3):
+        out = [[] for _ in range(b)]
+        for step in range(3):
             r = eng.sd_step(strategy, slots)
-            outs.append((r.accept_len.tolist(), r.bonus.tolist(), r.accepted, r.kv_len.tolist(),
-                         [[(t, p, d) for t, p, d, _, _ in tr] for tr in r.tree]))
+            if step == 0:
+                firsts.append((r.accept_len.tolist(), r.bonus.tolist(), r.accepted, r.kv_len.tolist()))
+            for i in range(b):
+                out[i] += r.accepted[i] + [int(r.bonus[i])]
             toks, _ = eng.ar_step(slots)
-            outs.append(toks.tolist())
-        res.append(outs)
+            for i in range(b):
+                out[i].append(int(toks[i]))
+        streams.append(out)
         eng.close()
-    assert res[0] == res[1]
+    assert firsts[0] == firsts[1]
+    for a, c in zip(*streams):
+        n = min(len(a), len(c))
+        assert a[:n] == c[:n]
