@@ -484,7 +484,10 @@ def run_ours(a):
     # the CUDA-graph pool of plan_captures (capture_plan.hpp:87-126), pre-built
     # before the timed region: one fused step graph per (bucket, strategy),
     # replayed for every batch of its bucket; padded plain-decode sizes
-    pool = eng.graph_pool_build(DEFAULT_ARMS, THRESHOLDS, 32) if a.graph_pool else None
+    pool = (eng.graph_pool_build(DEFAULT_ARMS, THRESHOLDS, 32, sub_bucket_width=a.pool_sub_width,
+                                 ar_width=a.pool_ar_width) if a.graph_pool else None)
+    if pool is not None:
+        pool.update(sub_bucket_width=a.pool_sub_width, ar_width=a.pool_ar_width)
     mab = Mab(DEFAULT_ARMS, THRESHOLDS, 0.1, 20)
     # C1: with several ranks each rank's bandit records are all-gathered after
     # every rollout and merged in rank order into a shared replica (NCCL; the
@@ -611,6 +614,10 @@ def main():
     ap.add_argument("--len-sigma", type=float, default=1.0)
     ap.add_argument("--max-len", type=int, default=8192)
     ap.add_argument("--graph-pool", type=int, default=1)
+    # 0: one graph per plan bucket (padding to the bucket's largest batch);
+    # w: sub-buckets of <= w batch sizes (DESIGN.md §6 measures the trade-off)
+    ap.add_argument("--pool-sub-width", type=int, default=1)
+    ap.add_argument("--pool-ar-width", type=int, default=1)
     ap.add_argument("--elastic", type=int, default=32)
     ap.add_argument("--ar-baseline", type=int, default=1)
     ap.add_argument("--cpu-gen", type=int, default=8)

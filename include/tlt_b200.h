@@ -223,6 +223,13 @@ typedef struct {
  * graph_bytes = device memory the pool took (cudaMemGetInfo delta; all
  * graphs share the engine's activation buffers). */
 TLT_API int tlt_graph_pool_build(tlt_engine* e, const tlt_capture_entry* entries, int n, size_t* graph_bytes);
+/* Granularity of the next tlt_graph_pool_build: sub_bucket_width 0 = one
+ * graph per plan bucket (the paper's plan: a step at batch b replays the
+ * graph of its bucket's largest batch); w > 0 = every plan bucket cut into
+ * sub-buckets of <= w batch sizes, same strategies (less padding, more
+ * graphs; w = 1 is one graph per batch size). ar_width: plain-decode graph
+ * sizes, 0 = 1, 2, 4, 8, 16, 24, ..., w > 0 = every w-th size. */
+TLT_API int tlt_graph_pool_configure(tlt_engine* e, int sub_bucket_width, int ar_width);
 /* Last pool build: graphs captured, plan pairs skipped (draft rows beyond
  * the engine buffers at that bucket size), bytes, host build time, and the
  * number of executable graphs the engine holds now (pool + on-demand). */

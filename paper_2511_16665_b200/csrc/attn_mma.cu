@@ -955,11 +955,13 @@ int attention_mma_split() { return kSplit; }
 // request's key count, split_chunk). Decode (<= 16 query vectors per
 // (request, KV head)): flash-decode kernel. Tree verify / drafter levels:
 // the 64-query-vector tree kernel with (request, KV head, q-tile) x splits
-// aiming at TLT_ATTN_TREE_CTAS CTAs (default 148: one fat CTA per SM beats
-// several waves of short ones — the per-CTA prologue and the split combine
-// are the latency floor at these shapes), whole 64-key tiles, at least
-// TLT_ATTN_TREE_MIN_CHUNK keys per split. A request served by one split
-// writes its output directly (no partials, no combine).
+// aiming at TLT_ATTN_TREE_CTAS CTAs (default 296 = 2 per SM, the kernel's
+// occupancy), whole 64-key tiles, at least TLT_ATTN_TREE_MIN_CHUNK (128)
+// keys per split: measured best over the verify / drafter shapes
+// (profiles/r2_attn_sweep.txt: b=5 T=48 46.7 -> 39.0 us, b=16 T=16 51.2 ->
+// 39.9 us, b=31 T=16 75.3 -> 59.5 us per layer vs the fixed 256-key splits
+// sized for the cache capacity). A request served by one split writes its
+// output directly (no partials, no combine).
 void attention_plan_splits(AttnParams& p, int max_keys) {
     const int G = p.H / p.KV;
     const int nqv = p.rows_per_req * G;
@@ -982,10 +984,10 @@ void attention_plan_splits(AttnParams& p, int max_keys) {
     } else if (p.impl == 1 && G >= 2 && nqv >= env_int("TLT_ATTN_TREE_MIN_QV", 17) && env_int("TLT_ATTN_TREE_DYN", 1)) {
         const int qv = env_int("TLT_ATTN_TREE_QV", 64);
         const long long pairs = (long long)p.n_groups * p.KV * ((nqv + qv - 1) / qv);
-        const int target = env_int("TLT_ATTN_TREE_CTAS", 148);
+        const int target = env_int("TLT_ATTN_TREE_CTAS", 296);
         p.dyn_splits = pairs >= target ? 1 : (int)std::max(1LL, target / std::max(1LL, pairs));
         p.gran = kTKeys;
-        p.min_chunk = std::max(kTKeys, env_int("TLT_ATTN_TREE_MIN_CHUNK", 256) / kTKeys * kTKeys);
+        p.min_chunk = std::max(kTKeys, env_int("TLT_ATTN_TREE_MIN_CHUNK", 128) / kTKeys * kTKeys);
         p.chunk = p.min_chunk;
         p.direct1 = 1;
     }

@@ -197,6 +197,15 @@ TLT_API int tlt_graph_pool_build(tlt_engine* e, const tlt_capture_entry* entries
     });
 }
 
+TLT_API int tlt_graph_pool_configure(tlt_engine* e, int sub_bucket_width, int ar_width) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] {
+        if (sub_bucket_width < 0 || ar_width < 0) throw tlt::ConfigErr("width", "must be >= 0");
+        e->e->pool_sub_width_ = sub_bucket_width;
+        e->e->pool_ar_width_ = ar_width;
+    });
+}
+
 TLT_API int tlt_graph_pool_stats(tlt_engine* e, int32_t* n_graphs, int32_t* n_skipped, size_t* graph_bytes,
                                  double* build_ms, int32_t* n_live) {
     if (!e) return fail(TLT_ERR_STATE, "null engine");

@@ -185,6 +185,22 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
             // single-split outputs, separate combine)
             if (rows_per_req * (H / KV) <= 16) throw ConfigErr("kernel", "tree kernel needs > 16 query vectors");
             launch_attention(p, 0);
+        } else if (kernel == 5 || kernel == 6) {
+            // TMA-fed kernel (attn_tma.cu) with the engine's split plan; 6 =
+            // split combine fused into the last CTA (decode shapes)
+            if (!attention_tma_enabled(p)) throw ConfigErr("kernel", "shape not eligible for the TMA kernel");
+            int* ctr = nullptr;
+            if (kernel == 6) {
+                const long long n = (long long)n_groups * KV * ((rows_per_req * (H / KV) + 15) / 16);
+                CUDA_CHECK(cudaMalloc(&ctr, sizeof(int) * n));
+                CUDA_CHECK(cudaMemset(ctr, 0, sizeof(int) * n));
+                p.counters = ctr;
+            }
+            const long long rows = (long long)n_groups * KV * cap;  // caches hold n_groups slots
+            const CUtensorMap tk = make_tmap_kv(kc, rows, hd), tv = make_tmap_kv(vc, rows, hd);
+            launch_attention_tma(tk, tv, p, 0);
+            CUDA_CHECK(cudaDeviceSynchronize());
+            if (ctr) cudaFree(ctr);
         } else {
             p.impl = 1;
             launch_attention_legacy(p, 0);

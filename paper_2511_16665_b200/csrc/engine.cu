@@ -157,6 +157,8 @@ Engine::~Engine() {
     for (void* p : hp)
         if (p) cudaFreeHost(p);
     cudaEventDestroy(ev0_);
+    if (tune_ev0_) cudaEventDestroy(tune_ev0_);
+    if (tune_ev1_) cudaEventDestroy(tune_ev1_);
     cudaEventDestroy(ev1_);
     cudaStreamDestroy(st_);
 }
@@ -319,9 +321,10 @@ const CUtensorMap& Engine::tmap_act(const void* p, int rows, int cols, long long
     return tmaps_.emplace(key, make_tmap_bf16(p, rows, cols, ld, box)).first->second;
 }
 
-void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep_in) {
-    GemmPlan g = plan_gemm(M, N, K);
-    if (ep_in.kind == EPI_TOPK) {  // the fused top-k epilogue needs whole-K accumulators
+// GEMM plan of one site: the planner's variant plus the epilogue fix-ups.
+GemmPlan Engine::make_plan(int M, int N, int K, int kind, int variant) const {
+    GemmPlan g = plan_gemm(M, N, K, variant);
+    if (kind == EPI_TOPK) {  // the fused top-k epilogue needs whole-K accumulators
         g.kb_per_split = g.kb_total;
         g.splits = 1;
     }
@@ -329,12 +332,89 @@ void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap&
         const char* v = std::getenv("TLT_QKV_MAX_SPLITS");
         return v ? std::atoi(v) : 4;
     }();
-    if (ep_in.kind == EPI_QKV && g.pair == 1 && g.splits > qkv_max_splits) {
+    if (kind == EPI_QKV && g.pair == 1 && g.splits > qkv_max_splits) {
         // measured (tools/probe.py): the QKV epilogue (bias, RoPE, KV-cache
         // scatter) after the in-cluster reduction prefers <= 4 splits
         g.kb_per_split = (g.kb_total + qkv_max_splits - 1) / qkv_max_splits;
         g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
     }
+    return g;
+}
+
+// Per-shape plan autotuning (mid M, where the tensor-bound plans differ by up
+// to ~20% between shapes: CTA pairs at 2 CTAs/SM, pairs with a deep 1-CTA/SM
+// ring, the persistent pair kernel, single-CTA tiles). The first eager
+// encounter of (M, N, K, epilogue) times every distinct candidate plan on
+// the engine stream (3 launches each, same inputs; a residual-add epilogue is
+// timed as an fp32 store into scratch, every other epilogue is idempotent)
+// and caches the fastest; the heuristic plan is kept unless a candidate
+// beats it by > 2%. Never during graph capture (the cached choice is used
+// there), never below TLT_GEMM_AUTOTUNE_MIN_M rows.
+int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N,
+                          const EpiParams& ep_in) {
+    static const int on = env_int("TLT_GEMM_AUTOTUNE", 1);
+    static const int min_m = env_int("TLT_GEMM_AUTOTUNE_MIN_M", 128);
+    if (!on || M < min_m || ep_in.norm_w || ep_in.row_scale) return 0;
+    const auto key = std::make_tuple(M, N, K, (int)ep_in.kind);
+    auto it = gemm_variant_.find(key);
+    if (it != gemm_variant_.end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_CHECK(cudaStreamIsCapturing(st_, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return 0;
+    EpiParams e = ep_in;
+    e.n_out = N;
+    e.m_tok = M;
+    e.dyn_n = nullptr;
+    if (e.kind == EPI_RESID_ADD) {
+        if ((size_t)M * N > (size_t)R_ * cfg.vocab) return 0;
+        e.kind = EPI_F32;
+        e.out_f32 = logits_;
+        e.ld_f32 = N;
+    }
+    std::vector<GemmPlan> plans;
+    std::vector<int> vars;
+    for (int v = 0; v < 4; ++v) {
+        const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, v);
+        bool dup = false;
+        for (const auto& q : plans) dup = dup || q.same_as(g);
+        if (!dup) {
+            plans.push_back(g);
+            vars.push_back(v);
+        }
+    }
+    int best = 0;
+    if (plans.size() > 1) {
+        if (!tune_ev0_) {  // own events: ev0_/ev1_ may be bracketing the step being run
+            CUDA_CHECK(cudaEventCreate(&tune_ev0_));
+            CUDA_CHECK(cudaEventCreate(&tune_ev1_));
+        }
+        std::vector<float> t(plans.size());
+        for (size_t i = 0; i < plans.size(); ++i) {
+            const CUtensorMap& tx = tmap_act(X, M, K, ldx, plans[i].box_rows);
+            launch_gemm(plans[i], tmW, tx, e, ws_, ws_elems_, st_);  // warm
+            CUDA_CHECK(cudaEventRecord(tune_ev0_, st_));
+            for (int r = 0; r < 3; ++r) launch_gemm(plans[i], tmW, tx, e, ws_, ws_elems_, st_);
+            CUDA_CHECK(cudaEventRecord(tune_ev1_, st_));
+            CUDA_CHECK(cudaEventSynchronize(tune_ev1_));
+            CUDA_CHECK(cudaEventElapsedTime(&t[i], tune_ev0_, tune_ev1_));
+        }
+        size_t bi = 0;
+        for (size_t i = 1; i < plans.size(); ++i)
+            if (t[i] < t[bi]) bi = i;
+        if (bi != 0 && t[0] <= 1.02f * t[bi]) bi = 0;
+        best = vars[bi];
+        if (std::getenv("TLT_GEMM_AUTOTUNE_LOG")) {
+            std::fprintf(stderr, "[tlt] autotune M=%d N=%d K=%d kind=%d:", M, N, K, (int)ep_in.kind);
+            for (size_t i = 0; i < plans.size(); ++i) std::fprintf(stderr, " v%d=%.1fus", vars[i], t[i] * 1e3f / 3);
+            std::fprintf(stderr, " -> v%d\n", best);
+        }
+    }
+    gemm_variant_[key] = best;
+    return best;
+}
+
+void Engine::gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep_in) {
+    const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, tuned_variant(X, M, K, ldx, tmW, N, ep_in));
     const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.box_rows);
     EpiParams ep = ep_in;
     ep.n_out = N;
@@ -359,14 +439,14 @@ void Engine::set_dyn(EpiParams& e, int M) const {
 // long-tail M); the norm of few rows spreads each row over an 8-CTA cluster.
 void Engine::gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w) {
     const int d = cfg.hidden;
-    GemmPlan g = plan_gemm(M, d, K);
-    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.box_rows);
     EpiParams e{};
     e.n_out = d;
     e.m_tok = M;
     e.kind = EPI_RESID_ADD;
     e.out_f32 = x_;
     e.ld_f32 = d;
+    const GemmPlan g = make_plan(M, d, K, EPI_RESID_ADD, tuned_variant(X, M, K, ldx, tmW, d, e));
+    const CUtensorMap& tx = tmap_act(X, M, K, ldx, g.box_rows);
     set_dyn(e, M);
     static const int fuse_max_m = [] {
         // off by default: the serial tail of the electing CTA measured slower
@@ -444,8 +524,24 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
         const long long n_qt = (p.rows_per_req * (cfg.heads / cfg.kv_heads) + 15) / 16;
         if ((long long)ngroups * cfg.kv_heads * n_qt <= (1 << 16)) p.counters = attn_counters_;
     }
+    if (attention_tma_enabled(p)) {
+        launch_attention_tma(tmap_kv(kc, cache_cap), tmap_kv(vc, cache_cap), p, st_);
+        count_launch(p.counters || p.max_splits == 1 ? 1 : 2);
+        return;
+    }
     launch_attention(p, st_);
     count_launch(p.counters || (p.dec && p.max_splits == 1) ? 1 : 2);
+}
+
+// TMA map of one KV cache ([max_slots][KV][cap][hd] bf16), cached per base pointer
+const CUtensorMap& Engine::tmap_kv(const bf16* base, int cache_cap) {
+    char key[64];
+    std::snprintf(key, sizeof key, "kv/%p/%d", (const void*)base, cache_cap);
+    auto it = tmaps_.find(key);
+    if (it == tmaps_.end())
+        it = tmaps_.emplace(key, make_tmap_kv(base, (long long)cfg.max_slots * cfg.kv_heads * cache_cap, cfg.head_dim))
+                 .first;
+    return it->second;
 }
 
 // One decoder layer over R rows (residual x_ in place).
@@ -1779,8 +1875,21 @@ size_t Engine::graph_pool_build(const std::vector<tlt_capture_entry>& entries, b
             throw ConfigErr("entries", "side must be 0 (TARGET) or 1 (DRAFT)");
         }
     }
+    if (pool_sub_width_ > 0) {  // sub-buckets of at most pool_sub_width_ batch sizes (same strategies)
+        std::vector<PoolBucket> fine;
+        for (const auto& pb : pool_)
+            for (int lo = pb.lo; lo <= pb.hi; lo += pool_sub_width_)
+                fine.push_back(PoolBucket{lo, std::min(pb.hi, lo + pool_sub_width_ - 1), pb.Ts, pb.kd});
+        pool_.swap(fine);
+    }
     if (with_ar) {
-        for (int s = 1; s <= max_b_; s = s < 8 ? 2 * s : s + 8) ar_sizes_.push_back(s);
+        if (pool_ar_width_ > 0)
+            for (int s = pool_ar_width_; s < max_b_ + pool_ar_width_; s += pool_ar_width_) ar_sizes_.push_back(std::min(s, max_b_));
+        else
+            for (int s = 1; s <= max_b_; s = s < 8 ? 2 * s : s + 8) ar_sizes_.push_back(s);
+        if (pool_ar_width_ == 1 || pool_ar_width_ > 1) ar_sizes_.insert(ar_sizes_.begin(), 1);
+        std::sort(ar_sizes_.begin(), ar_sizes_.end());
+        ar_sizes_.erase(std::unique(ar_sizes_.begin(), ar_sizes_.end()), ar_sizes_.end());
         if (ar_sizes_.empty() || ar_sizes_.back() != max_b_) ar_sizes_.push_back(max_b_);
     }
     CUDA_CHECK(cudaStreamSynchronize(st_));

@@ -85,6 +85,8 @@ public:
     double pool_capture_ms_ = 0;  // host time of the last pool build
     int pool_graphs_ = 0;         // graphs captured by the last pool build
     int pool_skipped_ = 0;        // plan pairs not capturable (draft rows beyond the engine buffers)
+    int pool_sub_width_ = 0;      // 0: one graph per plan bucket; w: sub-buckets of <= w batch sizes
+    int pool_ar_width_ = 0;       // 0: plain-decode sizes 1,2,4,8,16,24,..; w: every w-th size (1 = exact)
     int graph_count() const {  // production graphs (debug-export variants excluded)
         int n = 0;
         for (const auto& kv : graphs_) n += std::get<4>(kv.first) != 4;
@@ -112,7 +114,12 @@ private:
     void alloc_weights(const tlt_init_cfg& init);
     void alloc_state();
     const CUtensorMap& tmap_act(const void* p, int rows, int cols, long long ld, int box);
+    const CUtensorMap& tmap_kv(const bf16* base, int cache_cap);
     void gemm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep);
+    GemmPlan make_plan(int M, int N, int K, int kind, int variant) const;
+    int tuned_variant(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep);
+    std::map<std::tuple<int, int, int, int>, int> gemm_variant_;  // autotuned plan variant per (M, N, K, epilogue)
+    cudaEvent_t tune_ev0_ = nullptr, tune_ev1_ = nullptr;
     void layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int R,
                        int rpr, int ngroups, int max_keys, bool h_ready, const bf16* next_norm);
     void gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w);

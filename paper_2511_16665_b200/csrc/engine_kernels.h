@@ -1,5 +1,6 @@
 // Launch wrappers + parameter blocks of the engine kernels (kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -154,6 +155,11 @@ void launch_accept_stochastic(const StepIn* step, int b, int D, int V, double te
 void launch_reduce_resid_norm(const float* ws, long long plane, int splits, int R, int d, float* x,
                               const __nv_bfloat16* g, float eps, __nv_bfloat16* out, cudaStream_t st);
 void launch_attention(const AttnParams& p, cudaStream_t st);
+// TMA-fed variant (attn_tma.cu): tk / tv = 2D maps of the layer's K / V cache
+// ([slots * KV * cap][hd], 64 x 64 boxes, 128B swizzle, make_tmap_kv)
+CUtensorMap make_tmap_kv(const void* base, long long rows, int hd);
+bool attention_tma_enabled(const AttnParams& p);
+void launch_attention_tma(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st);
 
 int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, int k, float* part, cudaStream_t st);
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,

@@ -764,7 +764,7 @@ int gemm_dbg_flags() {
     return f;
 }
 
-GemmPlan plan_gemm(int m_tok, int n_out, int k) {
+GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
     GemmPlan g;
     static const int l2pf = env_knob("TLT_GEMM_L2PF", 0);
     g.l2pf = l2pf;
@@ -774,22 +774,28 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
     const int fixed = 1024 + 256;
     // Tensor-bound regime: CTA pairs (cta_group::2, 256 weight rows x up to
     // 256 tokens per pair), no split-K.
-    static const int pair_min_m = env_knob("TLT_GEMM_PAIR_MIN_M", 192);
+    static const int pair_min_m_env = env_knob("TLT_GEMM_PAIR_MIN_M", 192);
     static const int pair_bn_max = env_knob("TLT_GEMM_PAIR_BN_MAX", 256);
-    static const int pair_cps = env_knob("TLT_GEMM_PAIR_CPS", 2);
+    static const int pair_cps_env = env_knob("TLT_GEMM_PAIR_CPS", 2);
+    // plan variants (the engine's per-shape autotuner times them once and
+    // keeps the fastest): 1 = CTA pairs with a deep 1-CTA/SM ring, 2 = the
+    // persistent CTA-pair kernel, 3 = no CTA pairs (single-CTA tiles)
+    const int pair_min_m = variant == 3 ? 0 : pair_min_m_env;
+    const int pair_cps = variant == 1 ? 1 : pair_cps_env;
     // 1: persistent kernel for CTA-pair plans; 2: also for single-CTA plans
     // measured (profiles/r1_gemm_knobs_*.txt): with the staged epilogue the
     // 2-CTA/SM non-persistent kernel wins below ~768 tokens, the persistent
     // CTA-pair kernel above; the single-CTA persistent kernel never wins
     static const int persist = env_knob("TLT_GEMM_PERSIST", 1);
-    static const int pair_persist_min_m = env_knob("TLT_GEMM_PAIR_PERSIST_MIN_M", 768);
+    static const int pair_persist_min_m_env = env_knob("TLT_GEMM_PAIR_PERSIST_MIN_M", 768);
+    const int pair_persist_min_m = variant == 2 ? 1 : pair_persist_min_m_env;
     static const int persist1_min_m = env_knob("TLT_GEMM_PERSIST1_MIN_M", 48);
     // pairs only when they still put >= 1 CTA on every SM (else the 1-CTA
     // plan with in-cluster split-K fills the machine better)
     const int pair_ctas = 2 * ((n_out + 2 * kBlockM - 1) / (2 * kBlockM)) * ((m_tok + pair_bn_max - 1) / pair_bn_max);
     static const int pair_min_ctas = env_knob("TLT_GEMM_PAIR_MIN_CTAS", 148);
     static const int pair_split = env_knob("TLT_GEMM_PAIR_SPLIT", 1);
-    if (pair_split && pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas < pair_min_ctas) {
+    if (pair_split && variant == 0 && pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas < pair_min_ctas) {
         // few weight tiles (N = d): CTA pairs with <= 128-token tiles and
         // split-K across a (2, 1, splits) cluster, reduced through DSMEM
         const int n_tt = (m_tok + 127) / 128;
@@ -815,7 +821,7 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k) {
             return g;
         }
     }
-    if (pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas >= pair_min_ctas) {
+    if (pair_min_m > 0 && m_tok >= pair_min_m && (pair_ctas >= pair_min_ctas || variant == 1 || variant == 2)) {
         g.pair = 2;
         g.wm = 1;
         static const int pair_wm2 = env_knob("TLT_GEMM_PAIR_WM2", 0);  // measured slower (exposed epilogue, 1 CTA/SM)

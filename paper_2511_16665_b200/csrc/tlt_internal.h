@@ -43,11 +43,15 @@ struct GemmPlan {
     int l2pf = 0;      // weight k-blocks prefetched into L2 ahead of the smem ring
     int persist = 0;   // 1: persistent kernel (double-buffered TMEM accumulators)
     int fp8 = 0;       // 1: e4m3 operands (kind::f8f6f4), per-row / per-token scales in the epilogue
+    bool same_as(const GemmPlan& o) const {
+        return bn == o.bn && n_ttiles == o.n_ttiles && n_wtiles == o.n_wtiles && splits == o.splits &&
+               stages == o.stages && wm == o.wm && pair == o.pair && persist == o.persist;
+    }
 };
 
 int num_sms();
 CUtensorMap make_tmap_bf16(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
-GemmPlan plan_gemm(int m_tok, int n_out, int k);
+GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant = 0);
 GemmPlan plan_gemm_e4m3(int m_tok, int n_out, int k);
 CUtensorMap make_tmap_e4m3(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
 int* gemm_norm_counter();

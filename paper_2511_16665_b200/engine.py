@@ -294,9 +294,11 @@ class Engine:
         return StepResult(alen, bonus, [acc[i, :alen[i]].tolist() for i in range(b)],
                           [nodes[i, :alen[i]].tolist() for i in range(b)], kvl, float(ms[0]), None)
 
-    def graph_pool_build(self, strategies, thresholds, max_batch=32, vanilla=False):
+    def graph_pool_build(self, strategies, thresholds, max_batch=32, vanilla=False, sub_bucket_width=0, ar_width=0):
         """Pre-capture the CUDA-graph pool of plan_captures (capture_plan.hpp:
-        87-155; vanilla = plan_captures_vanilla) and return its stats."""
+        87-155; vanilla = plan_captures_vanilla) and return its stats.
+        sub_bucket_width / ar_width: tlt_graph_pool_configure."""
+        _check(self.L.tlt_graph_pool_configure(self.h, sub_bucket_width, ar_width))
         entries, units = plan_captures(strategies, thresholds, max_batch, vanilla)
         arr = (CaptureEntry * len(entries))(*[CaptureEntry(*e) for e in entries])
         nbytes = C.c_size_t()

@@ -157,9 +157,11 @@ def _analytic_speedup(c, batch, s):
     return em * base / sd
 
 
-def run_experiment(cfg: dict | None = None, engine: Engine | None = None, max_ctx: int | None = None) -> dict:
+def run_experiment(cfg: dict | None = None, engine: Engine | None = None, max_ctx: int | None = None,
+                   keep_tokens: bool = False) -> dict:
     """experiment.hpp:435-695 on the GPU engine; returns the RunReport as the
-    reference's report_to_json document (plus GPU-only fields)."""
+    reference's report_to_json document (plus GPU-only fields; keep_tokens
+    adds both arms' token streams per step under "_tokens")."""
     c = config_from_json(cfg or {})
     strategies = [tuple(s) for s in c["strategies"]]
     w = c["workload"]
@@ -227,7 +229,10 @@ def run_experiment(cfg: dict | None = None, engine: Engine | None = None, max_ct
               # GPU-only: emitted tokens and tokens/s of both arms, greedy losslessness
               "baseline_tokens_per_s": sum(lens) / (base["device_ms"] / 1e3),
               "tlt_tokens_per_s": tlt["emitted_total"] / (tlt["device_ms"] / 1e3),
-              "tokens_match": (tlt["tokens"] == base["tokens"]) if mode == "greedy" else None}
+              "tokens_match": (tlt["tokens"] == base["tokens"]) if mode == "greedy" else None,
+              "tokens_first_divergence": [next((j for j in range(min(len(a), len(b_))) if a[j] != b_[j]),
+                                               min(len(a), len(b_))) if a != b_ else -1
+                                          for a, b_ in zip(tlt["tokens"], base["tokens"])]}
         if len(at_least) < len(tlt["accept_at_least"]):
             at_least += [0] * (len(tlt["accept_at_least"]) - len(at_least))
         for i, v in enumerate(tlt["accept_at_least"]):
@@ -236,6 +241,9 @@ def run_experiment(cfg: dict | None = None, engine: Engine | None = None, max_ct
         tot_base += base["total_time"]
         tot_tlt += tlt["total_time"]
         report["steps"].append(sr)
+        if keep_tokens:
+            report.setdefault("_tokens", []).append({"prompts": prompts, "tlt": tlt["tokens"],
+                                                     "baseline": base["tokens"]})
     report["aggregate_speedup"] = tot_base / tot_tlt
     report["accept_rate_by_position"] = [v / tot_events if tot_events else 0.0 for v in at_least]
     groups = {}

@@ -74,3 +74,45 @@ def same_step(a, b):
     assert a.accepted == b.accepted and a.nodes == b.nodes
     assert a.kv_len.tolist() == b.kv_len.tolist()
     assert a.tree == b.tree
+
+
+def tiny_oracle_model():
+    """CPU neural oracle of the tiny (config 1) model; caller destroys it."""
+    from paper_2511_16665_b200.engine import INITS, MODELS
+    T, I = MODELS["tiny"], INITS["tiny"]
+    L = O.orc()
+    cfg = O.ModelCfg(T["vocab"], T["hidden"], T["layers"], T["heads"], T["kv_heads"], T["head_dim"], T["ffn"],
+                     T["qkv_bias"], T["rope_theta"], T["rms_eps"], 1024)
+    ini = O.InitCfg(I["seed"], I["layer_scale"], I["lm_gain"], I["lm_alt"], I["lm_noise"], I["fc_noise"])
+    return L.orc_model_create(C.byref(cfg), C.byref(ini), 8)
+
+
+def oracle_logits(m, ctx, vocab):
+    """fp32 target logits of the oracle after ctx (committed tokens)."""
+    L = O.orc()
+    s = L.orc_seq_create(m)
+    arr = (C.c_int32 * len(ctx))(*ctx)
+    L.orc_seq_append.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+    assert L.orc_seq_append(s, arr, len(ctx)) == 0
+    out = np.zeros(vocab, np.float32)
+    L.orc_target_logits_path.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    assert L.orc_target_logits_path(s, (C.c_int32 * 1)(0), 0, out.ctypes.data_as(C.c_void_p)) == 0
+    L.orc_seq_destroy(s)
+    return out
+
+
+def greedy_streams_agree(m, prompt, a, b, vocab, atol=0.05, rtol=0.01):
+    """Two greedy token streams of the same prompt are equal, or first differ
+    at a floating-point near-tie: the oracle's logits of the two candidate
+    tokens at the divergence are within twice the logit tolerance (the GPU
+    paths compute those logits with different reduction orders, SURVEY.md §7
+    "batch invariance"). Returns (ok, divergence position or -1, margin)."""
+    n = min(len(a), len(b))
+    k = next((j for j in range(n) if a[j] != b[j]), None)
+    if k is None:
+        return True, -1, None
+    lg = oracle_logits(m, list(prompt) + list(a[:k]), vocab)
+    ta, tb = a[k], b[k]
+    margin = abs(float(lg[ta]) - float(lg[tb]))
+    tol = 2 * (atol + rtol * max(abs(float(lg[ta])), abs(float(lg[tb]))))
+    return margin <= tol, k, margin

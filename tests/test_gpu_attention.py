@@ -134,3 +134,59 @@ def test_tree_attention_engine_split_plan(monkeypatch, n_groups, rpr, remap, cta
     got = run(c, 4)
     err = (got - ref).abs()
     assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+@pytest.mark.parametrize("n_groups,rpr,remap", [(1, 65, True), (5, 49, False), (3, 17, True), (31, 17, False),
+                                                (2, 33, False)])
+@pytest.mark.parametrize("ctas,min_chunk", [("296", "128"), ("1", "256"), ("592", "64")])
+def test_tma_tree_attention(monkeypatch, n_groups, rpr, remap, ctas, min_chunk):
+    """TMA-fed kernel (attn_tma.cu, kernel 5): 128B-swizzled 64 x 64 K/V boxes
+    in an mbarrier ring, prefix and tree-tail tiles, ragged requests, every
+    split plan within bf16 tolerance of torch fp32."""
+    monkeypatch.setenv("TLT_ATTN_TREE_CTAS", ctas)
+    monkeypatch.setenv("TLT_ATTN_TREE_MIN_CHUNK", min_chunk)
+    lcs = [RAGGED[(i * 5) % len(RAGGED)] for i in range(n_groups)]
+    c = make_case(n_groups, rpr, lcs, seed=n_groups * 11 + rpr, remap_tail=remap)
+    ref = reference(c)
+    got = run(c, 5)
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+@pytest.mark.parametrize("n_groups", [1, 5, 8, 40, 64])
+def test_tma_decode_attention(n_groups):
+    """TMA flash-decode (1 row x 7 q-heads per request): separate combine
+    (kernel 5) and fused combine (kernel 6) equal each other bit for bit and
+    torch within bf16 tolerance, on ragged key counts."""
+    lcs = [RAGGED[(i * 3 + 1) % len(RAGGED)] for i in range(n_groups)]
+    c = make_case(n_groups, 1, lcs, seed=13 * n_groups)
+    ref = reference(c)
+    sep = run(c, 5)
+    fused = run(c, 6)
+    err = (sep - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+    assert torch.equal(sep, fused)
+
+
+def test_tma_tiny_head_dim():
+    """hd = 64 (the tiny config): one 64-dim box per tile."""
+    c = make_case(3, 17, [100, 5, 300], H=4, KV=2, hd=64, cap=512, seed=5)
+    ref = reference(c)
+    got = run(c, 5)
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+@pytest.mark.parametrize("n_groups", [1, 4, 12, 32])
+def test_tma_tiny_decode(n_groups):
+    """hd = 64 flash-decode (tiny config: 4 q-heads / 2 KV heads), TMA kernel
+    (separate and fused combine) vs the mma.sync kernel vs torch."""
+    lcs = [RAGGED[(i * 7 + 2) % len(RAGGED)] % 400 for i in range(n_groups)]
+    c = make_case(n_groups, 1, lcs, H=4, KV=2, hd=64, cap=512, seed=17 * n_groups)
+    ref = reference(c)
+    got = run(c, 5)
+    old = run(c, 2)
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+    err = (old - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
