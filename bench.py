@@ -493,6 +493,12 @@ def run_ours(a):
     # every rollout and merged in rank order into a shared replica (NCCL; the
     # only collective besides the timing reductions)
     mab_shared = Mab(DEFAULT_ARMS, THRESHOLDS, 0.1, 20) if pg is not None else None
+    c1 = None
+    if pg is not None:  # C1 inside the library: NCCL communicator on the engine's device, side stream
+        from paper_2511_16665_b200.engine import C1
+        uid = [C1.nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(uid, src=0)
+        c1 = C1.nccl(eng, uid[0], world, rank)
     V = eng.vocab
 
     def workload(step):
@@ -508,7 +514,7 @@ def run_ours(a):
         r = eng.run_rollout(prompts, lens, ids, enable_sd=enable_sd, elastic_threshold=a.elastic,
                             mab=mab, seed=step, use_graphs=True)
         if mab_shared is not None and enable_sd:
-            r["c1_records"] = merge_bandit_stats(pg, mab, mab_shared)
+            r["c1_records"] = merge_bandit_stats(pg, mab, mab_shared, c1)
         return r
 
     for s in range(a.warmup):

@@ -262,6 +262,23 @@ TLT_API int tlt_mab_apply_record(tlt_mab* m, int arm, double reward, double a_ba
  * replica's beg_record logged since the last call (records applied through
  * tlt_mab_apply_record are not logged). */
 TLT_API int tlt_mab_take_log(tlt_mab* m, int32_t* arm, double* reward, double* a_bar, int cap, int32_t* n);
+/* C1 inside the library: after a rollout every rank's new beg_record
+ * records (tlt_mab_take_log) go into a fixed-size block (count + max_records
+ * x {arm, reward, a_bar}), the blocks are all-gathered and applied to
+ * `shared` in rank order (bit-identical on every rank; with one rank exactly
+ * the local beg_record sequence), and `local` restarts from `shared`.
+ * Transport: NCCL (an engine-device communicator on its own side stream;
+ * rank 0 makes the id with tlt_c1_nccl_unique_id, the host distributes it),
+ * or a host all-gather callback: gather `bytes` from every rank into
+ * recv[world][bytes] in rank order, return 0 on success. */
+typedef struct tlt_c1 tlt_c1;
+typedef int (*tlt_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
+TLT_API int tlt_c1_nccl_unique_id(void* id128);
+TLT_API int tlt_c1_create_nccl(tlt_engine* e, const void* id128, int world, int rank, int max_records, tlt_c1** out);
+TLT_API int tlt_c1_create_callback(int world, int rank, tlt_allgather_fn fn, void* user, int max_records,
+                                   tlt_c1** out);
+TLT_API int tlt_c1_merge(tlt_c1* c, tlt_mab* local, tlt_mab* shared, int32_t* n_merged);
+TLT_API void tlt_c1_destroy(tlt_c1* c);
 /* Copy the full bandit state (windows, selection counts) of src into dst. */
 TLT_API int tlt_mab_copy(tlt_mab* dst, const tlt_mab* src);
 /* Deterministic streams, reference RngStream (rng.hpp:34-86). */

@@ -41,6 +41,7 @@ def _declare(L: C.CDLL) -> None:
     L.tlt_rng_uniform01.argtypes = [C.c_void_p]
     L.tlt_rng_destroy.argtypes = [C.c_void_p]
     L.tlt_engine_destroy.argtypes = [C.c_void_p]
+    L.tlt_c1_destroy.argtypes = [C.c_void_p]
     L.tlt_mab_destroy.argtypes = [C.c_void_p]
     L.tlt_ngram_destroy.argtypes = [C.c_void_p]
     L.tlt_ngram_draft.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]

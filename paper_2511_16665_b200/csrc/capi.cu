@@ -11,21 +11,7 @@
 #include <vector>
 
 #include "../../include/tlt_b200.h"
-#include "engine.h"
-#include "host_select.h"
-
-struct tlt_engine {
-    std::unique_ptr<tlt::Engine> e;
-};
-struct tlt_mab {
-    std::unique_ptr<tlt::Mab> m;
-};
-struct tlt_rng {
-    tlt::Rng r;
-};
-struct tlt_ngram {
-    tlt::Ngram g;
-};
+#include "capi_types.h"
 
 namespace {
 int fail(int code, const char* msg) {

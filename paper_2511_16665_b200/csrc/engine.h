@@ -78,6 +78,7 @@ public:
     std::vector<std::vector<int>> last_chain;    // drafted chain per request of the last stochastic step
 
     int slot_len(int slot) const { return lt_.at(slot); }
+    int device() const { return dev_; }
     void set_debug(bool on) { debug_ = on; }
     bool use_graphs = true;
     size_t graph_pool_build(const std::vector<tlt_capture_entry>& entries, bool with_ar = true);

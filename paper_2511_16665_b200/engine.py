@@ -654,11 +654,76 @@ class Mab:
             pass
 
 
-def merge_bandit_stats(dist, local: "Mab", shared: "Mab") -> int:
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
+class C1:
+    """C1 inside the library (tlt_c1_*): fixed-size BEG-MAB record blocks
+    all-gathered over NCCL (engine-device communicator, side stream) or a
+    host all-gather callback, applied in rank order to the shared replica."""
+
+    def __init__(self, h, keep=None):
+        self.L = lib()
+        self.h = h
+        self._keep = keep  # the ctypes callback must outlive the handle
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        _check(lib().tlt_c1_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, engine: "Engine", uid: bytes, world: int, rank: int, max_records: int = 4096):
+        h = C.c_void_p()
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        _check(lib().tlt_c1_create_nccl(engine.h, buf, world, rank, max_records, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_dist(cls, dist, max_records: int = 4096):
+        """Callback transport over a torch.distributed group (the record block
+        travels as a CPU or CUDA byte tensor, as the backend needs)."""
+        import torch
+        world, rank = dist.get_world_size(), dist.get_rank()
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+
+        def gather(user, send, recv, nbytes):
+            try:
+                t = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8).to(dev)
+                outs = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(outs, t)
+                blob = torch.cat(outs).cpu().numpy().tobytes()
+                C.memmove(recv, blob, len(blob))
+                return 0
+            except Exception:
+                return 1
+
+        fn = ALLGATHER_FN(gather)
+        h = C.c_void_p()
+        _check(lib().tlt_c1_create_callback(world, rank, fn, None, max_records, C.byref(h)))
+        return cls(h, keep=fn)
+
+    def merge(self, local: "Mab", shared: "Mab") -> int:
+        n = C.c_int32()
+        _check(self.L.tlt_c1_merge(self.h, local.h, shared.h, C.byref(n)))
+        return n.value
+
+    def __del__(self):
+        try:
+            self.L.tlt_c1_destroy(self.h)
+        except Exception:
+            pass
+
+
+def merge_bandit_stats(dist, local: "Mab", shared: "Mab", c1: "C1 | None" = None) -> int:
     """C1: all-gather every rank's new BEG-MAB records and apply
     them to the shared replica in rank order, so every rank's shared replica is
     bit-identical; the local replica then restarts from it. With one rank this
-    is exactly the local beg_record sequence. Returns the records merged."""
+    is exactly the local beg_record sequence. Returns the records merged.
+    With `c1` the library does the pack / all-gather / apply (tlt_c1_merge)."""
+    if c1 is not None:
+        return c1.merge(local, shared)
     mine = local.take_log()
     world = dist.get_world_size() if dist is not None else 1
     logs = [None] * world

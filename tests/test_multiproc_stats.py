@@ -57,7 +57,7 @@ def test_gloo_allgather_merge_keeps_replicas_identical(world):
     assert all(ok for _, ok in res), res
 
 
-def _rollout_worker(rank, world, port, q):
+def _rollout_worker(rank, world, port, q, use_lib=False):
     """bench.py's C1 path: per 'rollout' each rank records into its local
     replica, then merge_bandit_stats all-gathers the logs and applies them in
     rank order to the shared replica; shared replicas must be bit-identical
@@ -65,8 +65,9 @@ def _rollout_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2511_16665_b200.engine import Mab, Rng, merge_bandit_stats
+    from paper_2511_16665_b200.engine import C1, Mab, Rng, merge_bandit_stats
     local, shared = Mab(ARMS, THR, 0.1, 20), Mab(ARMS, THR, 0.1, 20)
+    c1 = C1.from_dist(dist) if use_lib else None  # C1 inside the library (tlt_c1_merge)
     rng = Rng(99, 0x53454C + rank)
     g = random.Random(7 + rank)
     total = 0
@@ -78,7 +79,7 @@ def _rollout_worker(rank, world, port, q):
             arm, s = local.select(batch, rng)
             lens = [g.randrange(0, s[0] + 1) for _ in range(batch)]
             local.record(s, 1.0 + g.random(), lens)
-        total += merge_bandit_stats(dist, local, shared)
+        total += merge_bandit_stats(dist, local, shared, c1)
     stats = torch.tensor([v for i in range(len(ARMS)) for v in (shared.arm_stats(i)[0], shared.arm_stats(i)[2])],
                          dtype=torch.float64)
     gathered = [torch.zeros_like(stats) for _ in range(world)]
@@ -91,15 +92,46 @@ def _rollout_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_gloo_rollout_boundary_merge():
+@pytest.mark.parametrize("use_lib", [False, True])
+def test_gloo_rollout_boundary_merge(use_lib):
+    """use_lib: the library's C1 (fixed-size record blocks, rank-order apply in
+    C++) over a host all-gather callback on the gloo group."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29500 + random.randrange(1000, 2000)
-    procs = [ctx.Process(target=_rollout_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rollout_worker, args=(r, world, port, q, use_lib)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+@pytest.mark.gpu
+def test_gpu_c1_nccl_world1_equals_local_sequence():
+    """C1 over NCCL inside the library, one rank: the shared replica equals a
+    replica that ran the same beg_record sequence locally."""
+    from paper_2511_16665_b200.engine import C1, Engine, Mab, Rng
+    eng = Engine("tiny", max_slots=2, max_ctx=64)
+    c1 = C1.nccl(eng, C1.nccl_unique_id(), 1, 0)
+    local, shared, ref = Mab(ARMS, THR, 0.1, 20), Mab(ARMS, THR, 0.1, 20), Mab(ARMS, THR, 0.1, 20)
+    rng, rref = Rng(5, 1), Rng(5, 1)
+    g = random.Random(3)
+    for rollout in range(4):
+        for step in range(15):
+            batch = g.choice([1, 4, 12, 25])
+            _, s = local.select(batch, rng)
+            _, s2 = ref.select(batch, rref)
+            assert s == s2
+            lens = [g.randrange(0, s[0] + 1) for _ in range(batch)]
+            el = 1.0 + g.random()
+            local.record(s, el, lens)
+            ref.record(s, el, lens)
+        assert c1.merge(local, shared) == 15
+        for i in range(len(ARMS)):
+            assert shared.arm_stats(i)[0] == ref.arm_stats(i)[0] and shared.arm_stats(i)[2] == ref.arm_stats(i)[2]
+            assert shared.arm_window(i) == ref.arm_window(i) == local.arm_window(i)
+    del c1
+    eng.close()
