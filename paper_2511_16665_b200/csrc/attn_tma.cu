@@ -75,8 +75,10 @@ template <int HD>
 __device__ __forceinline__ void attn_fused_combine_tma(const AttnParams& p, int grp, int kvh, int qtile, int qv_lo,
                                                        int qv_hi);
 
-template <int HD, bool DEC, int STAGES>
-__global__ void __launch_bounds__(128, 2)
+// SUBK: keys per S / P chunk of the TREE warps (64: one chunk per tile; 32:
+// two, halving the S / P registers so 3 CTAs fit per SM with STAGES = 2)
+template <int HD, bool DEC, int STAGES, int SUBK>
+__global__ void __launch_bounds__(128, STAGES == 2 ? 3 : 2)
     k_attention_tma(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p) {
     constexpr int QV = DEC ? 16 : 64;      // query vectors per CTA
     constexpr int KS = HD / 16;            // k-steps over head_dim (QK^T)
@@ -194,9 +196,27 @@ __global__ void __launch_bounds__(128, 2)
         const int nk = tail ? min(kTK, te - kb) : min(kTK, pe - kb);
         mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
         const uint32_t kbase = smem_u32(ring + s * 2 * TILE_B), vbase = kbase + TILE_B;
-        // keys of this warp within the tile: DEC 16 (warp-sliced), TREE all 64
-        constexpr int WK = DEC ? 16 : kTK;
-        const int key0 = DEC ? warp * 16 : 0;
+        // keys of this warp within the tile: DEC 16 (warp-sliced), TREE all
+        // 64 in chunks of SUBK
+        constexpr int WK = DEC ? 16 : SUBK;
+        const int wk0 = DEC ? warp * 16 : 0, wk1 = DEC ? warp * 16 + 16 : kTK;
+        const bool zfix = active && wk0 < nk && nk < wk1;
+        if (zfix) {
+            // rows past the tile's valid keys hold whatever the cache has there
+            // (later positions, never-written memory: possibly NaN bit patterns):
+            // P is 0 for them but 0 * NaN is NaN, so zero this warp's V rows
+            // [nk, wk1) first (other warps write the same zeros)
+            uint4* vz = reinterpret_cast<uint4*>(ring + s * 2 * TILE_B + TILE_B);
+            constexpr int CPR = 8 * (HD / 64);  // 16-byte chunks per key row (both halves)
+            const int z0 = nk, z1 = wk1;
+            for (int c = lane; c < (z1 - z0) * CPR; c += 32) {
+                const int r = z0 + c / CPR, rem = c % CPR;
+                vz[((rem >> 3) * (kTK * 128) + r * 128 + (rem & 7) * 16) >> 4] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            __syncwarp();
+        }
+#pragma unroll 1
+        for (int key0 = wk0; key0 < wk1; key0 += WK)
         if (active && key0 < nk) {
             float sc[WK / 8][4];
 #pragma unroll
@@ -282,6 +302,7 @@ __global__ void __launch_bounds__(128, 2)
                 }
             }
         }
+        if (zfix) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before the next TMA write
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (warp == 0) {  // refill the stage once every warp released it
@@ -426,14 +447,14 @@ CUtensorMap make_tmap_kv(const void* base, long long rows, int hd) {
     return make_tmap_bf16(base, (int)rows, hd, hd, 64);
 }
 
-template <int HD, bool DEC, int STAGES>
+template <int HD, bool DEC, int STAGES, int SUBK>
 static void launch_tma_t(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st) {
     constexpr int TILE_B = kTK * HD * 2;
     constexpr int kRows = DEC ? 16 : 34;
     const size_t smem = 1024 + (size_t)STAGES * 2 * TILE_B + sizeof(uint32_t) * kRows * kMaskWords;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_attention_tma<HD, DEC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_CHECK(cudaFuncSetAttribute(k_attention_tma<HD, DEC, STAGES, SUBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
         attr = true;
     }
@@ -441,7 +462,7 @@ static void launch_tma_t(const CUtensorMap& tk, const CUtensorMap& tv, const Att
     const int nqv = p.rows_per_req * G;
     constexpr int QV = DEC ? 16 : 64;
     dim3 grid((nqv + QV - 1) / QV, p.KV, p.n_groups * p.max_splits);
-    launch_pdl(k_attention_tma<HD, DEC, STAGES>, grid, 128, smem, st, tk, tv, p);
+    launch_pdl(k_attention_tma<HD, DEC, STAGES, SUBK>, grid, 128, smem, st, tk, tv, p);
 }
 
 // TMA attention for a plan from attention_plan_splits (dec: <= 16 query
@@ -450,16 +471,25 @@ static void launch_tma_t(const CUtensorMap& tk, const CUtensorMap& tv, const Att
 // served by a single split.
 void launch_attention_tma(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st) {
     if (p.hd != 128 && p.hd != 64) throw CudaError("attention (TMA): head_dim must be 64 or 128");
+    static const int tree_v = [] {  // TREE variant: 0 = 3 stages x 64-key chunks (2 CTAs/SM), 1 = 2 stages x 32 (3/SM)
+        const char* v = std::getenv("TLT_ATTN_TMA_TREE");
+        return v ? std::atoi(v) : 0;
+    }();
     if (p.dec) {
         if (p.hd == 128)
-            launch_tma_t<128, true, 3>(tk, tv, p, st);
+            launch_tma_t<128, true, 3, 16>(tk, tv, p, st);
         else
-            launch_tma_t<64, true, 3>(tk, tv, p, st);
+            launch_tma_t<64, true, 3, 16>(tk, tv, p, st);
+    } else if (tree_v == 1) {
+        if (p.hd == 128)
+            launch_tma_t<128, false, 2, 32>(tk, tv, p, st);
+        else
+            launch_tma_t<64, false, 2, 32>(tk, tv, p, st);
     } else {
         if (p.hd == 128)
-            launch_tma_t<128, false, 3>(tk, tv, p, st);
+            launch_tma_t<128, false, 3, 64>(tk, tv, p, st);
         else
-            launch_tma_t<64, false, 3>(tk, tv, p, st);
+            launch_tma_t<64, false, 3, 64>(tk, tv, p, st);
     }
     if (p.counters || p.max_splits == 1) return;
     launch_attn_combine_only(p, st);

@@ -190,3 +190,32 @@ def test_tma_tiny_decode(n_groups):
     assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
     err = (old - ref).abs()
     assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+def _poison(c):
+    """Every cache row outside a group's visible keys (committed prefix and
+    tree tail) := NaN: kernels must never let an unused row reach the output
+    (a masked probability of 0 times a NaN value is NaN)."""
+    for i in range(c["n_groups"]):
+        keep = torch.zeros(c["cap"], dtype=torch.bool)
+        keep[:c["lc"][i]] = True
+        keep[c["tail0"][i]:c["tail0"][i] + c["rpr"]] = True
+        c["kc"][i][:, ~keep] = float("nan")
+        c["vc"][i][:, ~keep] = float("nan")
+    return c
+
+
+@pytest.mark.parametrize("kernel", [5, 0, 4])
+@pytest.mark.parametrize("n_groups,rpr,hd,H,KV", [(3, 17, 128, 28, 4), (2, 49, 128, 28, 4), (5, 1, 128, 28, 4),
+                                                  (3, 17, 64, 4, 2), (4, 1, 64, 4, 2)])
+def test_attention_ignores_nan_in_unused_cache_rows(kernel, n_groups, rpr, hd, H, KV):
+    if kernel == 4 and rpr * H // KV <= 16:
+        pytest.skip("tree-kernel entry needs > 16 query vectors")
+    lcs = [(37 * (i + 1)) % 300 + 1 for i in range(n_groups)]
+    c = _poison(make_case(n_groups, rpr, lcs, H=H, KV=KV, hd=hd, cap=512, seed=n_groups + rpr + hd,
+                          remap_tail=True))
+    ref = reference(c)
+    got = run(c, kernel)
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
