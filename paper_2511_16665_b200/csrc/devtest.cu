@@ -185,6 +185,14 @@ extern "C" TLT_API int tlt_dev_attention(const void* q, const void* kc, const vo
             // single-split outputs, separate combine)
             if (rows_per_req * (H / KV) <= 16) throw ConfigErr("kernel", "tree kernel needs > 16 query vectors");
             launch_attention(p, 0);
+        } else if (kernel == 7) {
+            // tcgen05 / TMEM tree attention (attn_tc5.cu) with the engine's split plan
+            if (!attention_tma_enabled(p) || !attention_tree_tc_eligible(p))
+                throw ConfigErr("kernel", "shape not eligible for the tcgen05 tree kernel");
+            const long long rows = (long long)n_groups * KV * cap;
+            const CUtensorMap tk = make_tmap_kv(kc, rows, hd), tv = make_tmap_kv(vc, rows, hd);
+            launch_attention_tree_tc(tk, tv, p, 0);
+            CUDA_CHECK(cudaDeviceSynchronize());
         } else if (kernel == 5 || kernel == 6) {
             // TMA-fed kernel (attn_tma.cu) with the engine's split plan; 6 =
             // split combine fused into the last CTA (decode shapes)

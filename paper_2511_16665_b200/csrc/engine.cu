@@ -525,7 +525,10 @@ void Engine::attention(const bf16* kc, const bf16* vc, int cache_cap, const Rows
         if ((long long)ngroups * cfg.kv_heads * n_qt <= (1 << 16)) p.counters = attn_counters_;
     }
     if (attention_tma_enabled(p)) {
-        launch_attention_tma(tmap_kv(kc, cache_cap), tmap_kv(vc, cache_cap), p, st_);
+        if (attention_tree_tc_eligible(p))
+            launch_attention_tree_tc(tmap_kv(kc, cache_cap), tmap_kv(vc, cache_cap), p, st_);
+        else
+            launch_attention_tma(tmap_kv(kc, cache_cap), tmap_kv(vc, cache_cap), p, st_);
         count_launch(p.counters || p.max_splits == 1 ? 1 : 2);
         return;
     }

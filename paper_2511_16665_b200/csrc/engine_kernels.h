@@ -160,6 +160,9 @@ void launch_attention(const AttnParams& p, cudaStream_t st);
 CUtensorMap make_tmap_kv(const void* base, long long rows, int hd);
 bool attention_tma_enabled(const AttnParams& p);
 void launch_attention_tma(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st);
+// tcgen05 / TMEM tree attention (attn_tc5.cu), same maps and split plan, hd = 128
+bool attention_tree_tc_eligible(const AttnParams& p);
+void launch_attention_tree_tc(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st);
 
 int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, int k, float* part, cudaStream_t st);
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,

@@ -219,3 +219,42 @@ def test_attention_ignores_nan_in_unused_cache_rows(kernel, n_groups, rpr, hd, H
     assert torch.isfinite(got).all()
     err = (got - ref).abs()
     assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+@pytest.mark.parametrize("n_groups,rpr,remap", [(1, 65, True), (5, 49, False), (3, 17, True), (31, 17, False),
+                                                (2, 33, False), (4, 100, True)])
+@pytest.mark.parametrize("ctas,min_chunk", [("296", "128"), ("1", "256"), ("1184", "64")])
+def test_tcgen05_tree_attention(monkeypatch, n_groups, rpr, remap, ctas, min_chunk):
+    """tcgen05 / TMEM tree attention (attn_tc5.cu, kernel 7): TMA ring, S and O
+    in TMEM, lazy-rescaled online softmax, ragged requests and every split plan,
+    within bf16 tolerance of torch fp32."""
+    monkeypatch.setenv("TLT_ATTN_TREE_CTAS", ctas)
+    monkeypatch.setenv("TLT_ATTN_TREE_MIN_CHUNK", min_chunk)
+    lcs = [RAGGED[(i * 5 + 3) % len(RAGGED)] for i in range(n_groups)]
+    c = make_case(n_groups, rpr, lcs, seed=n_groups * 13 + rpr, remap_tail=remap)
+    ref = reference(c)
+    got = run(c, 7)
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+@pytest.mark.parametrize("n_groups,rpr", [(3, 17), (2, 49)])
+def test_tcgen05_tree_attention_nan_poisoned_cache(n_groups, rpr):
+    lcs = [(37 * (i + 1)) % 300 + 1 for i in range(n_groups)]
+    c = _poison(make_case(n_groups, rpr, lcs, cap=512, seed=n_groups + rpr, remap_tail=True))
+    ref = reference(c)
+    got = run(c, 7)
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs()
+    assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
+
+
+def test_tcgen05_tree_attention_large_score_growth():
+    """Scores that grow by >> 2^8 along the keys force O rescales in TMEM."""
+    c = make_case(2, 17, [900, 400], seed=3)
+    ramp = torch.linspace(0.0, 6.0, c["cap"], device="cuda").view(1, 1, -1, 1)
+    c["kc"] = (c["kc"].float() * (1.0 + ramp)).to(torch.bfloat16)
+    ref = reference(c)
+    got = run(c, 7)
+    err = (got - ref).abs()
+    assert torch.all(err <= 3e-2 + 3e-2 * ref.abs()), float(err.max())
