@@ -112,6 +112,27 @@ TLT_API int tlt_slot_len(tlt_engine* e, int slot_id, int32_t* len);
 TLT_API int tlt_export_sequence(tlt_engine* e, int slot_id, int32_t* tokens, int max_tokens, void* features,
                                 size_t features_bytes, int32_t* len);
 
+/* ---- drafter weights (spot drafter training) ---------- */
+/* Device view of one weight tensor: bf16 [rows][cols] row-major. */
+typedef struct {
+    const char* name;  /* fc, attn_norm, qkv, qkv_bias, o, mlp_norm, gate_up (rows interleaved gate/up), down,
+                          embed, final_norm, lm_head */
+    void* ptr;         /* device pointer (engine-owned) */
+    int64_t rows;
+    int64_t cols;
+    int32_t trainable; /* 1: the drafter's own (fc + its decoder layer); 0: shared with the target, frozen */
+} tlt_tensor_view;
+/* Lists the drafter's tensors (the trainer updates trainable ones in place,
+ * on any stream, then calls tlt_drafter_published). *n = count. */
+TLT_API int tlt_drafter_tensors(tlt_engine* e, tlt_tensor_view* out, int cap, int32_t* n);
+/* New drafter weights are in place (reference DrafterSnapshot publish,
+ * rollout.hpp:61-64): the drafter KV of live slots is recomputed on their next
+ * EAGLE step; `version` is the snapshot's drafter version. */
+TLT_API int tlt_drafter_published(tlt_engine* e, int64_t version);
+TLT_API int tlt_drafter_version(tlt_engine* e, int64_t* version);
+/* FNV-1a-64 (reference checkpoint.hpp:26-33), the drafter checkpoints' trailer. */
+TLT_API uint64_t tlt_fnv1a64(const void* data, size_t len);
+
 /* ---- one engine step ---------------------------------------------------- */
 /* Tree produced by the drafter, reference DraftTree (spec_decode.hpp:50-70),
  * rank order, parent -1 = root. Caller-owned, sized [b][tokens_to_verify]. */

@@ -11,8 +11,11 @@
 
 #include "specsim/beg_mab.hpp"
 #include "specsim/capture_plan.hpp"
+#include "specsim/checkpoint.hpp"
 #include "specsim/cost_model.hpp"
+#include "specsim/data_buffer.hpp"
 #include "specsim/model_gen.hpp"
+#include "specsim/packing.hpp"
 #include "specsim/rollout.hpp"
 #include "specsim/spec_decode.hpp"
 
@@ -414,5 +417,58 @@ int ref_ngram_draft(void* t, const int32_t* ctx, int len, int depth, int32_t* ou
     }
 }
 long long ref_ngram_size(void* t) { return (long long)static_cast<detail::NgramTracker*>(t)->index.size(); }
+
+// ------------------------------------------------------- spot training (f3)
+void* ref_databuf_create(long long retention) { return new DataBuffer(retention); }
+void ref_databuf_destroy(void* b) { delete static_cast<DataBuffer*>(b); }
+// sequences back to back: toks, lens[n]
+void ref_databuf_insert(void* b, long long step, const int32_t* toks, const int32_t* lens, int n) {
+    std::vector<TokenSeq> seqs;
+    for (int i = 0, off = 0; i < n; off += lens[i], ++i) seqs.emplace_back(toks + off, toks + off + lens[i]);
+    static_cast<DataBuffer*>(b)->insert(step, seqs);
+}
+int ref_databuf_size(void* b) { return (int)static_cast<DataBuffer*>(b)->entries().size(); }
+// sample -> concatenated tokens + lens; returns the number of sequences (or -1 if cap is too small)
+int ref_databuf_sample(void* b, long long step, long long budget, int32_t* toks, int32_t* lens, int cap_seqs,
+                       long long cap_toks) {
+    auto s = static_cast<DataBuffer*>(b)->sample(step, (std::size_t)budget);
+    if ((int)s.size() > cap_seqs) return -1;
+    long long off = 0;
+    for (size_t i = 0; i < s.size(); ++i) {
+        if (off + (long long)s[i].size() > cap_toks) return -1;
+        std::copy(s[i].begin(), s[i].end(), toks + off);
+        lens[i] = (int32_t)s[i].size();
+        off += (long long)s[i].size();
+    }
+    return (int)s.size();
+}
+// pack_sequences -> per pack: member lengths (bounds, -1 separates packs) and the pack tokens back to back
+int ref_pack(const int32_t* toks, const int32_t* lens, int n, long long capacity, int32_t* bounds, int cap_bounds,
+             int32_t* out_toks, long long cap_toks) {
+    std::vector<TokenSeq> seqs;
+    for (int i = 0, off = 0; i < n; off += lens[i], ++i) seqs.emplace_back(toks + off, toks + off + lens[i]);
+    PackedBatch p;
+    try {
+        p = pack_sequences(seqs, (std::size_t)capacity);
+    } catch (const std::exception&) {
+        return -2;
+    }
+    int nb = 0;
+    long long nt = 0;
+    for (size_t k = 0; k < p.packs.size(); ++k) {
+        for (size_t m : p.boundaries[k]) {
+            if (nb >= cap_bounds) return -1;
+            bounds[nb++] = (int32_t)m;
+        }
+        if (nb >= cap_bounds) return -1;
+        bounds[nb++] = -1;
+        for (TokenId t : p.packs[k]) {
+            if (nt >= cap_toks) return -1;
+            out_toks[nt++] = t;
+        }
+    }
+    return nb;
+}
+unsigned long long ref_fnv1a64(const uint8_t* data, unsigned long long len) { return detail::fnv1a64(data, len); }
 
 }  // extern "C"

@@ -69,6 +69,36 @@ TLT_API int tlt_export_sequence(tlt_engine* e, int slot_id, int32_t* tokens, int
     return guard([&] { *len = e->e->export_sequence(slot_id, tokens, max_tokens, features, features_bytes); });
 }
 
+// FNV-1a-64 (reference checkpoint.hpp:26-33), for the drafter checkpoints
+TLT_API uint64_t tlt_fnv1a64(const void* data, size_t len) {
+    const uint8_t* b = static_cast<const uint8_t*>(data);
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (size_t i = 0; i < len; ++i) {
+        h ^= b[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+TLT_API int tlt_drafter_tensors(tlt_engine* e, tlt_tensor_view* out, int cap, int32_t* n) {
+    if (!e || !n) return fail(TLT_ERR_STATE, "null argument");
+    return guard([&] {
+        const auto v = e->e->drafter_tensors();
+        *n = (int32_t)v.size();
+        if (out)
+            for (int i = 0; i < (int)v.size() && i < cap; ++i) out[i] = v[i];
+    });
+}
+TLT_API int tlt_drafter_published(tlt_engine* e, int64_t version) {
+    if (!e) return fail(TLT_ERR_STATE, "null engine");
+    return guard([&] { e->e->drafter_published(version); });
+}
+TLT_API int tlt_drafter_version(tlt_engine* e, int64_t* version) {
+    if (!e || !version) return fail(TLT_ERR_STATE, "null argument");
+    *version = e->e->drafter_version_;
+    return TLT_OK;
+}
+
 TLT_API int tlt_slot_len(tlt_engine* e, int slot_id, int32_t* len) {
     if (!e || !len) return fail(TLT_ERR_STATE, "null argument");
     return guard([&] {

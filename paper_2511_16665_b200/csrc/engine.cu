@@ -849,6 +849,39 @@ void Engine::release(int slot) {
     lt_[slot] = ld_[slot] = 0;
 }
 
+// Drafter weights (spot training): the trainable tensors of
+// the EAGLE drafter (fc + its decoder layer) and the shared frozen ones, as
+// device views the trainer updates in place. Every captured graph and tensor
+// map keeps pointing at the same buffers, so a publish needs no re-capture.
+std::vector<tlt_tensor_view> Engine::drafter_tensors() {
+    const int64_t d = cfg.hidden, nq = (int64_t)cfg.heads * cfg.head_dim, nkv = (int64_t)cfg.kv_heads * cfg.head_dim,
+                  F = cfg.ffn, V = cfg.vocab;
+    std::vector<tlt_tensor_view> v = {
+        {"fc", fc_, d, 2 * d, 1},
+        {"attn_norm", drafter_.attn_norm, 1, d, 1},
+        {"qkv", drafter_.qkv, nq + 2 * nkv, d, 1},
+        {"o", drafter_.o, d, nq, 1},
+        {"mlp_norm", drafter_.mlp_norm, 1, d, 1},
+        {"gate_up", drafter_.gu, 2 * F, d, 1},
+        {"down", drafter_.down, d, F, 1},
+        {"embed", embed_, V, d, 0},
+        {"final_norm", final_norm_, 1, d, 0},
+        {"lm_head", lm_head_, V, d, 0},
+    };
+    if (drafter_.qkv_b) v.insert(v.begin() + 3, tlt_tensor_view{"qkv_bias", drafter_.qkv_b, 1, nq + 2 * nkv, 1});
+    return v;
+}
+
+// After new drafter weights were published: drop the drafter KV of every live
+// slot (it was computed with the old weights; the next EAGLE step's catch-up
+// recomputes it from the committed target features) and bump the version.
+void Engine::drafter_published(int64_t version) {
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    for (int s = 0; s < cfg.max_slots; ++s)
+        if (live_[s]) ld_[s] = 0;
+    drafter_version_ = version;
+}
+
 // Shorten a live slot's committed state to `len` positions (token len becomes
 // the pending root): the rollout trims requests whose last step committed KV
 // past the emission cut (EOS / max_len) before the sequence is exported.

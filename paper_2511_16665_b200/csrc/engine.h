@@ -53,6 +53,9 @@ public:
     void prefill(int b, const int32_t* slots, const int32_t* lens, const int32_t* tokens);
     void release(int slot);
     void truncate(int slot, int len);
+    std::vector<tlt_tensor_view> drafter_tensors();
+    void drafter_published(int64_t version);
+    int64_t drafter_version_ = 0;
     // C2 (drafter training samples): committed tokens [0, lt] and target
     // features [0, lt) of a live slot into caller memory (host or device)
     int export_sequence(int slot, int32_t* tokens, int max_tokens, void* features, size_t features_bytes);
