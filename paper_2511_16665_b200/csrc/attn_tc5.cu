@@ -366,7 +366,13 @@ __global__ void __launch_bounds__(192, 1)
 bool attention_tree_tc_eligible(const AttnParams& p) {
     const char* v = std::getenv("TLT_ATTN_TREE_TC");
     if (v && std::atoi(v) == 0) return false;
-    return p.hd == kHD5 && !p.dec && p.dyn_splits > 0 && p.H / p.KV >= 2;
+    if (!(p.hd == kHD5 && !p.dec && p.dyn_splits > 0 && p.H / p.KV >= 2)) return false;
+    // measured (profiles/r2_probe_tree_{tma,tc}.txt): the tcgen05 kernel wins
+    // when the (request, KV head, 128-vector q-tile) grid alone nearly fills
+    // the SMs (b = 31, T = 16: 45.2 vs 46.9 us; ctx 2000: 108.6 vs 117.8), the
+    // mma.sync TMA kernel when few q-tiles are split over keys (b <= 16)
+    const long long tiles = (long long)p.n_groups * p.KV * ((p.rows_per_req * (p.H / p.KV) + kQ5 - 1) / kQ5);
+    return v ? true : tiles >= 96;
 }
 
 void launch_attention_tree_tc(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st) {

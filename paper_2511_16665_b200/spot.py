@@ -404,7 +404,7 @@ class DrafterTrainer:
             loss = F.cross_entropy(logits, lab, ignore_index=-100, reduction="sum")
             n = int((lab >= 0).sum())
             (loss / max(1, packed.total_tokens())).backward()
-            total += float(loss)
+            total += float(loss.detach())
             count += n
         self.opt.step()
         self.version += 1
