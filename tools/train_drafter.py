@@ -24,6 +24,7 @@ ap.add_argument("--prompt", type=int, default=256)
 ap.add_argument("--lr", type=float, default=3e-4)
 ap.add_argument("--budget", type=int, default=8192)
 ap.add_argument("--capacity", type=int, default=2048)
+ap.add_argument("--wd", type=float, default=0.0)
 a = ap.parse_args()
 
 eng = Engine(a.model, max_slots=a.requests, max_ctx=a.prompt + a.gen + 200)
@@ -39,8 +40,9 @@ def accept(seed, b=8, steps=8, strategy=(6, 8, 16)):
 
 out = {"before": {str(s): accept(1000 + i, strategy=s) for i, s in enumerate([(6, 8, 16), (10, 8, 64)])}}
 buf = S.DataBuffer(retention=1)
+held = S.DataBuffer(retention=1)
 t0 = time.time()
-for step in range(2):
+for step in range(3):
     rng = np.random.default_rng(step)
     prompts = [rng.integers(2, V, a.prompt).tolist() for _ in range(a.requests)]
     eng.run_rollout(prompts, [a.gen] * a.requests, enable_sd=False, keep_finished=True)
@@ -50,15 +52,34 @@ for step in range(2):
         toks.append(t.tolist())
         feats.append(f)
         eng.release(i)
-    buf.insert(step, toks, feats)
+    (held if step == 2 else buf).insert(min(step, 1), toks, feats)
 out["collect_s"] = time.time() - t0
-tr = S.DrafterTrainer(eng, lr=a.lr)
+tr = S.DrafterTrainer(eng, lr=a.lr, weight_decay=a.wd)
+
+
+def held_loss():
+    import torch
+    import torch.nn.functional as F
+    ents = held.sample(1, 1 << 30)
+    packed = S.pack_sequences([e.length() for e in ents], a.capacity)
+    tot, n = 0.0, 0
+    with torch.no_grad():
+        for pack in packed.packs:
+            tok, fp, pos, sid, lab = tr.batch_from_pack(ents, pack)
+            lg = tr.forward(tok, fp, pos, sid)
+            tot += float(F.cross_entropy(lg, lab, ignore_index=-100, reduction="sum"))
+            n += int((lab >= 0).sum())
+    return tot / n
+
+
+out["held_loss_before"] = held_loss()
 cfg = S.SpotTrainConfig(current_step=1, token_budget=a.budget, pack_capacity=a.capacity)
 t0 = time.time()
 log = S.spot_train_loop(tr, buf, cfg, a.iters)
 out["train_s"] = time.time() - t0
 out["loss_first"] = log.losses[:5]
 out["loss_last"] = log.losses[-5:]
+out["held_loss_after"] = held_loss()
 out["after"] = {str(s): accept(1000 + i, strategy=s) for i, s in enumerate([(6, 8, 16), (10, 8, 64)])}
 print(json.dumps(out))
 eng.close()
