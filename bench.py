@@ -509,17 +509,45 @@ def run_ours(a):
         lens = response_lengths(n, math.log(a.len_median), a.len_sigma, a.max_len, seed=100 + step + 7919 * rank)
         return ids, prompts, lens
 
-    def rollout(step, enable_sd=True):
+    buf = None
+    if a.spot_train_iters > 0:  # TLT spot training: the warmup rollouts feed the drafter's trainer (untimed)
+        from paper_2511_16665_b200 import spot as S
+        buf = S.DataBuffer(retention=1)
+
+    def rollout(step, enable_sd=True, collect=False):
         ids, prompts, lens = workload(step)
         r = eng.run_rollout(prompts, lens, ids, enable_sd=enable_sd, elastic_threshold=a.elastic,
-                            mab=mab, seed=step, use_graphs=True)
+                            mab=mab, seed=step, use_graphs=True, keep_finished=collect)
+        if collect:  # C2: every finished sequence (tokens + target features) into the DataBuffer
+            toks, feats = [], []
+            for i in range(n):
+                t, f = eng.export_sequence(i)
+                toks.append(t.tolist())
+                feats.append(f)
+                eng.release(i)
+            buf.insert(step, toks, feats)
         if mab_shared is not None and enable_sd:
             r["c1_records"] = merge_bandit_stats(pg, mab, mab_shared, c1)
         return r
 
+    spot = None
     for s in range(a.warmup):
-        rollout(s)
+        r = rollout(s, collect=buf is not None)
         print(f"[bench] warmup rollout {s} done", file=sys.stderr, flush=True)
+    if buf is not None:
+        t0 = time.perf_counter()
+        tr = S.DrafterTrainer(eng, lr=a.spot_lr)
+        cfg = S.SpotTrainConfig(current_step=a.warmup - 1, token_budget=a.spot_budget, pack_capacity=2048)
+        lg = S.spot_train_loop(tr, buf, cfg, a.spot_train_iters)
+        spot = {"iterations": lg.iterations, "drafter_version": S.drafter_version(eng),
+                "loss_first": round(lg.losses[0], 4), "loss_last": round(lg.losses[-1], 4),
+                "buffer_sequences": len(buf.entries), "train_s": round(time.perf_counter() - t0, 1),
+                "note": "EAGLE drafter spot-trained on the warmup rollouts' own sequences (C2 export), untimed, "
+                        "before the timed rollouts (TLT's adaptive drafter)"}
+        del buf, tr
+        import torch
+        torch.cuda.empty_cache()
+        print(f"[bench] spot training {spot}", file=sys.stderr, flush=True)
     barrier(pg, local)
     res = []
     with ClockSampler(local) as clk:
@@ -528,6 +556,24 @@ def run_ours(a):
             res.append(rollout(a.warmup + s))
         barrier(pg, local)
         wall = time.perf_counter() - t0
+    # where the rollout time goes (trace of the timed rollouts): device ms and
+    # emitted tokens per batch range, SD vs plain steps
+    def time_split(rs):
+        bins = [("ar_b>=32", lambda m: not m["sd_active"]), ("sd_b16-31", lambda m: m["sd_active"] and m["batch_size"] >= 16),
+                ("sd_b8-15", lambda m: m["sd_active"] and 8 <= m["batch_size"] < 16),
+                ("sd_b2-7", lambda m: m["sd_active"] and 2 <= m["batch_size"] < 8),
+                ("sd_b1", lambda m: m["sd_active"] and m["batch_size"] == 1)]
+        tot = sum(m["device_ms"] for r in rs for m in r["trace"])
+        out = {}
+        for name, f in bins:
+            ms = sum(m["device_ms"] for r in rs for m in r["trace"] if f(m))
+            steps = sum(1 for r in rs for m in r["trace"] if f(m))
+            toks = sum((sum(m["accept_lens"]) + m["batch_size"]) if m["sd_active"] else m["batch_size"]
+                       for r in rs for m in r["trace"] if f(m))
+            out[name] = {"time_frac": round(ms / tot, 4) if tot else 0.0, "steps": steps,
+                         "tokens_per_s": round(toks / (ms / 1e3), 1) if ms else None}
+        return out
+    split = time_split(res)
     emitted = sum(r["emitted_total"] for r in res)
     dev_s = sum(r["device_ms"] for r in res) / 1e3
     accepted = sum(r["accepted_total"] for r in res)
@@ -586,6 +632,8 @@ def run_ours(a):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "graph_pool": pool,
+            "spot_training": spot,
+            "time_split": split,
             "roofline": roof,
             "roofline_tensor_class": roof_tc,
             "per_bucket": buckets,
@@ -620,6 +668,9 @@ def main():
     ap.add_argument("--len-sigma", type=float, default=1.0)
     ap.add_argument("--max-len", type=int, default=8192)
     ap.add_argument("--graph-pool", type=int, default=1)
+    ap.add_argument("--spot-train-iters", type=int, default=0)
+    ap.add_argument("--spot-lr", type=float, default=3e-5)
+    ap.add_argument("--spot-budget", type=int, default=65536)
     # 0: one graph per plan bucket (padding to the bucket's largest batch);
     # w: sub-buckets of <= w batch sizes (DESIGN.md §6 measures the trade-off)
     ap.add_argument("--pool-sub-width", type=int, default=1)
