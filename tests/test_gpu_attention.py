@@ -228,6 +228,7 @@ def test_tcgen05_tree_attention(monkeypatch, n_groups, rpr, remap, ctas, min_chu
     """tcgen05 / TMEM tree attention (attn_tc5.cu, kernel 7): TMA ring, S and O
     in TMEM, lazy-rescaled online softmax, ragged requests and every split plan,
     within bf16 tolerance of torch fp32."""
+    monkeypatch.setenv("TLT_ATTN_TREE_TC", "1")  # force it for shapes the engine routes elsewhere
     monkeypatch.setenv("TLT_ATTN_TREE_CTAS", ctas)
     monkeypatch.setenv("TLT_ATTN_TREE_MIN_CHUNK", min_chunk)
     lcs = [RAGGED[(i * 5 + 3) % len(RAGGED)] for i in range(n_groups)]
@@ -239,7 +240,8 @@ def test_tcgen05_tree_attention(monkeypatch, n_groups, rpr, remap, ctas, min_chu
 
 
 @pytest.mark.parametrize("n_groups,rpr", [(3, 17), (2, 49)])
-def test_tcgen05_tree_attention_nan_poisoned_cache(n_groups, rpr):
+def test_tcgen05_tree_attention_nan_poisoned_cache(monkeypatch, n_groups, rpr):
+    monkeypatch.setenv("TLT_ATTN_TREE_TC", "1")
     lcs = [(37 * (i + 1)) % 300 + 1 for i in range(n_groups)]
     c = _poison(make_case(n_groups, rpr, lcs, cap=512, seed=n_groups + rpr, remap_tail=True))
     ref = reference(c)
@@ -249,8 +251,9 @@ def test_tcgen05_tree_attention_nan_poisoned_cache(n_groups, rpr):
     assert torch.all(err <= 2e-2 + 2e-2 * ref.abs()), float(err.max())
 
 
-def test_tcgen05_tree_attention_large_score_growth():
+def test_tcgen05_tree_attention_large_score_growth(monkeypatch):
     """Scores that grow by >> 2^8 along the keys force O rescales in TMEM."""
+    monkeypatch.setenv("TLT_ATTN_TREE_TC", "1")
     c = make_case(2, 17, [900, 400], seed=3)
     ramp = torch.linspace(0.0, 6.0, c["cap"], device="cuda").view(1, 1, -1, 1)
     c["kc"] = (c["kc"].float() * (1.0 + ramp)).to(torch.bfloat16)
