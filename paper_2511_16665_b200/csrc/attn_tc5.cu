@@ -76,6 +76,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
 }
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ void cp_async16_5(uint32_t saddr, const void* gmem, bool pred) {
     const int sz = pred ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
@@ -243,7 +248,18 @@ __global__ void __launch_bounds__(192, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(&sfree[i & 1]);  // S buffer may be overwritten by S_{i+2}
-            // visibility + scale (NaN-safe: invisible scores never enter the max or P)
+            // visibility as one 64-bit mask per row (valid keys of the tile, and for
+            // tree-tail tiles the row's mask bits kb .. kb+63), then scale; NaN-safe:
+            // invisible scores never enter the max or P
+            uint64_t vis = lr < 0 ? 0ull : (nk >= 64 ? ~0ull : ((1ull << nk) - 1ull));
+            if (tail && vis) {
+                const uint32_t* mr = Ms + lr * kMaskWords;
+                const int w0 = kb >> 5, sh = kb & 31;
+                const uint32_t a0 = mr[w0], a1 = w0 + 1 < kMaskWords ? mr[w0 + 1] : 0u,
+                               a2 = w0 + 2 < kMaskWords ? mr[w0 + 2] : 0u;
+                const uint64_t lo = ((uint64_t)a1 << 32) | a0, hi = a2;
+                vis &= sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+            }
             float x[64];
             float mt = -CUDART_INF_F;
 #pragma unroll
@@ -251,12 +267,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const int col = 16 * u + j;
-                    bool vis = lr >= 0 && col < nk;
-                    if (vis && tail) {
-                        const int tt = kb + col;
-                        vis = ((Ms[lr * kMaskWords + (tt >> 5)] >> (tt & 31)) & 1u) != 0;
-                    }
-                    x[col] = vis ? __uint_as_float(r[u][j]) * p.scale_log2 : -CUDART_INF_F;
+                    x[col] = ((vis >> col) & 1ull) ? __uint_as_float(r[u][j]) * p.scale_log2 : -CUDART_INF_F;
                     mt = fmaxf(mt, x[col]);
                 }
             // lazy rescale: move the max only when it grows by > 2^8 (or from -inf)
@@ -285,11 +296,14 @@ __global__ void __launch_bounds__(192, 1)
             }
             m = m_new;
             // P (bf16) for this row, relative to the max in use
+            // ex2(-inf) = +0 for invisible keys; a row with no visible key so far
+            // (m = -inf) contributes nothing
             uint32_t pk[32];
+            const float mm = m == -CUDART_INF_F ? CUDART_INF_F : m;
 #pragma unroll
             for (int j = 0; j < 64; j += 2) {
-                const float p0 = x[j] == -CUDART_INF_F ? 0.f : exp2f(x[j] - m);
-                const float p1 = x[j + 1] == -CUDART_INF_F ? 0.f : exp2f(x[j + 1] - m);
+                const float p0 = ex2_approx(x[j] - mm);
+                const float p1 = ex2_approx(x[j + 1] - mm);
                 lsum += p0 + p1;
                 __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
                 pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h);
