@@ -378,15 +378,14 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 bool attention_tree_tc_eligible(const AttnParams& p) {
+    // default on for every hd = 128 multi-row forward: with the 64-bit
+    // visibility mask + ex2.approx softmax it beats the mma.sync TMA kernel at
+    // every verify / drafter shape measured (profiles/r2_probe_tree_{tma2,tc2}.txt:
+    // b = 31 T = 16 46.9 -> 20.7 us, ctx 2000 117.7 -> 40.8 us, b = 5 T = 48
+    // 32.9 -> 22.1 us, b = 1 T = 64 20.6 -> 19.8 us); TLT_ATTN_TREE_TC=0 off
     const char* v = std::getenv("TLT_ATTN_TREE_TC");
     if (v && std::atoi(v) == 0) return false;
-    if (!(p.hd == kHD5 && !p.dec && p.dyn_splits > 0 && p.H / p.KV >= 2)) return false;
-    // measured (profiles/r2_probe_tree_{tma,tc}.txt): the tcgen05 kernel wins
-    // when the (request, KV head, 128-vector q-tile) grid alone nearly fills
-    // the SMs (b = 31, T = 16: 45.2 vs 46.9 us; ctx 2000: 108.6 vs 117.8), the
-    // mma.sync TMA kernel when few q-tiles are split over keys (b <= 16)
-    const long long tiles = (long long)p.n_groups * p.KV * ((p.rows_per_req * (p.H / p.KV) + kQ5 - 1) / kQ5);
-    return v ? true : tiles >= 96;
+    return p.hd == kHD5 && !p.dec && p.dyn_splits > 0 && p.H / p.KV >= 2;
 }
 
 void launch_attention_tree_tc(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st) {
