@@ -13,7 +13,7 @@ using namespace tlt;
 extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
                                     void* y_bf16, float* ws, long long ws_elems, int max_splits) {
     try {
-        GemmPlan g = plan_gemm(m, n, k);
+        GemmPlan g = plan_gemm(m, n, k, std::getenv("TLT_GEMM_FORCE_VARIANT") ? std::atoi(std::getenv("TLT_GEMM_FORCE_VARIANT")) : 0);
         if (max_splits > 0 && g.splits > max_splits) {
             g.kb_per_split = (g.kb_total + max_splits - 1) / max_splits;
             g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
@@ -42,7 +42,7 @@ extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, 
 extern "C" TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
                                          void* y_bf16, float* ws, long long ws_elems, int iters, float* avg_ms) {
     try {
-        GemmPlan g = plan_gemm(m, n, k);
+        GemmPlan g = plan_gemm(m, n, k, std::getenv("TLT_GEMM_FORCE_VARIANT") ? std::atoi(std::getenv("TLT_GEMM_FORCE_VARIANT")) : 0);
         CUtensorMap tw = make_tmap_bf16(w, n, k, k, 128);
         CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.box_rows);
         EpiParams ep{};

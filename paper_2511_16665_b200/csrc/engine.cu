@@ -343,7 +343,8 @@ GemmPlan Engine::make_plan(int M, int N, int K, int kind, int variant) const {
 
 // Per-shape plan autotuning (mid M, where the tensor-bound plans differ by up
 // to ~20% between shapes: CTA pairs at 2 CTAs/SM, pairs with a deep 1-CTA/SM
-// ring, the persistent pair kernel, single-CTA tiles). The first eager
+// ring, the persistent pair kernel, single-CTA tiles, pairs with <= 128-token
+// tiles, the pair split-K plan with 4 splits). The first eager
 // encounter of (M, N, K, epilogue) times every distinct candidate plan on
 // the engine stream (3 launches each, same inputs; a residual-add epilogue is
 // timed as an fp32 store into scratch, every other epilogue is idempotent)
@@ -373,7 +374,7 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
     }
     std::vector<GemmPlan> plans;
     std::vector<int> vars;
-    for (int v = 0; v < 4; ++v) {
+    for (int v : {0, 1, 2, 3, 4, 6}) {
         const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, v);
         bool dup = false;
         for (const auto& q : plans) dup = dup || q.same_as(g);

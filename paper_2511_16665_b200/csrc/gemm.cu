@@ -775,7 +775,10 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
     // Tensor-bound regime: CTA pairs (cta_group::2, 256 weight rows x up to
     // 256 tokens per pair), no split-K.
     static const int pair_min_m_env = env_knob("TLT_GEMM_PAIR_MIN_M", 192);
-    static const int pair_bn_max = env_knob("TLT_GEMM_PAIR_BN_MAX", 256);
+    static const int pair_bn_max_env = env_knob("TLT_GEMM_PAIR_BN_MAX", 256);
+    // 4 = CTA pairs with <= 128-token tiles (more tiles: fills the SMs on
+    // small-N shapes), 6 = the pair split-K plan with 4 splits
+    const int pair_bn_max = variant == 4 ? 128 : pair_bn_max_env;
     static const int pair_cps_env = env_knob("TLT_GEMM_PAIR_CPS", 2);
     // plan variants (the engine's per-shape autotuner times them once and
     // keeps the fastest): 1 = CTA pairs with a deep 1-CTA/SM ring, 2 = the
@@ -795,7 +798,8 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
     const int pair_ctas = 2 * ((n_out + 2 * kBlockM - 1) / (2 * kBlockM)) * ((m_tok + pair_bn_max - 1) / pair_bn_max);
     static const int pair_min_ctas = env_knob("TLT_GEMM_PAIR_MIN_CTAS", 148);
     static const int pair_split = env_knob("TLT_GEMM_PAIR_SPLIT", 1);
-    if (pair_split && variant == 0 && pair_min_m > 0 && m_tok >= pair_min_m && pair_ctas < pair_min_ctas) {
+    if (pair_split && (variant == 0 || variant == 6) && pair_min_m > 0 && m_tok >= pair_min_m &&
+        (pair_ctas < pair_min_ctas || variant == 6)) {
         // few weight tiles (N = d): CTA pairs with <= 128-token tiles and
         // split-K across a (2, 1, splits) cluster, reduced through DSMEM
         const int n_tt = (m_tok + 127) / 128;
@@ -804,6 +808,7 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
         const int n_wt = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
         const int ctas = 2 * n_wt * ((m_tok + bn - 1) / bn);
         int splits = std::max(1, std::min({(2 * num_sms()) / ctas, g.kb_total / 4, 4}));
+        if (variant == 6) splits = std::max(1, std::min(4, g.kb_total / 4));
         const int stage_bytes = kABytes + (bn / 2) * kBlockK * 2;
         const int stages = std::max(2, std::min(8, (112 * 1024 - fixed) / stage_bytes));
         if (splits > 1 && stages * stage_bytes >= bn * kBlockM * 4) {
@@ -821,7 +826,8 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
             return g;
         }
     }
-    if (pair_min_m > 0 && m_tok >= pair_min_m && (pair_ctas >= pair_min_ctas || variant == 1 || variant == 2)) {
+    if (pair_min_m > 0 && m_tok >= pair_min_m &&
+        (pair_ctas >= pair_min_ctas || variant == 1 || variant == 2 || variant == 4)) {
         g.pair = 2;
         g.wm = 1;
         static const int pair_wm2 = env_knob("TLT_GEMM_PAIR_WM2", 0);  // measured slower (exposed epilogue, 1 CTA/SM)
