@@ -374,7 +374,7 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
     }
     std::vector<GemmPlan> plans;
     std::vector<int> vars;
-    for (int v : {0, 1, 2, 3, 4, 6}) {
+    for (int v : {0, 1, 2, 3, 4, 6, 7}) {
         const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, v);
         bool dup = false;
         for (const auto& q : plans) dup = dup || q.same_as(g);

@@ -168,7 +168,7 @@ template <int PAIR, int FP8 = 0>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_swapab(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                   int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, int wm, int l2pf,
-                  EpiParams ep) {
+                  int mc, EpiParams ep) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int b_rows = bn / PAIR;  // token rows staged by this CTA
@@ -188,8 +188,16 @@ __global__ void __launch_bounds__(192, 1)
     // cluster is (2, 1, splits) and the pair of split z has cluster ranks
     // (2z, 2z+1): the leader (MMA issuer, full barriers) is rank 2z
     const uint32_t rank = PAIR == 2 ? (blockIdx.x & 1u) : 0u;
-    const uint32_t lead_rank = PAIR == 2 ? 2u * blockIdx.z : 0u;
+    // weight multicast (PAIR, mc > 1): a (2 mc, 1, 1) cluster holds mc CTA
+    // pairs on the same weight tile and consecutive token tiles; pair 0 loads
+    // each weight k-block once and multicasts it to the mc pairs, every
+    // pair's MMA completion releases the stage in all of them
+    const uint32_t mpair = (PAIR == 2 && mc > 1) ? (uint32_t)((blockIdx.x >> 1) % mc) : 0u;
+    const uint32_t lead_rank = PAIR == 2 ? (mc > 1 ? 2u * mpair : 2u * blockIdx.z) : 0u;
     const uint16_t pair_mask = (uint16_t)(0x3u << lead_rank);
+    const uint16_t all_mask = (uint16_t)((1u << (2 * mc)) - 1u);
+    const uint16_t w_mask = (uint16_t)(0x5555u & all_mask) << rank;  // CTAs of the same pair rank
+    const bool w_issuer = mc <= 1 || mpair == 0;
     // token tiles vary fastest: the CTAs sharing one weight tile run together,
     // so the weight tile is fetched from HBM once and re-read from L2
     const int n0 = (blockIdx.y * PAIR + rank) * kBlockM * wm;
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(192, 1)
         tma_prefetch_desc(&tmX);
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], mc > 1 ? mc : 1);
         }
         mbar_init(tfull, 1);
         fence_barrier_init();
@@ -243,15 +251,20 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t full_bar0 = PAIR == 2 ? mapa_shared(smem_u32(&full[0]), lead_rank) : 0u;
     if (warp == 0 && lane == 0) {
         // weight tiles beyond the smem ring: L2 prefetch l2pf k-blocks ahead
-        for (int i = npre; i < min(nkb, npre + l2pf); ++i)
-            for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, (kb0 + i) * kKel, n0 + a * kBlockM);
+        if (w_issuer)
+            for (int i = npre; i < min(nkb, npre + l2pf); ++i)
+                for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, (kb0 + i) * kKel, n0 + a * kBlockM);
         for (int i = 0; i < npre; ++i) {
             const int kc = (kb0 + i) * kKel;
             if (PAIR == 2) {
                 if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * (a_bytes + b_bytes));
-                for (int a = 0; a < wm; ++a)
-                    tma_load_2d_pair(sA + i * a_bytes + a * kABytes, &tmW, full_bar0 + 8u * i, kc, n0 + a * kBlockM,
-                                     pol_w);
+                if (mc > 1) {
+                    if (w_issuer) tma_load_2d_pair_mc(sA + i * a_bytes, &tmW, &full[i], kc, n0, w_mask, pol_w);
+                } else {
+                    for (int a = 0; a < wm; ++a)
+                        tma_load_2d_pair(sA + i * a_bytes + a * kABytes, &tmW, full_bar0 + 8u * i, kc,
+                                         n0 + a * kBlockM, pol_w);
+                }
             } else {
                 mbar_arrive_expect_tx(&full[i], a_bytes + b_bytes);
                 for (int a = 0; a < wm; ++a)
@@ -275,14 +288,18 @@ __global__ void __launch_bounds__(192, 1)
                         tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
                     continue;
                 }
-                if (i + l2pf < nkb)
+                if (w_issuer && i + l2pf < nkb)
                     for (int a = 0; a < wm; ++a) tma_prefetch_l2_2d(&tmW, kc + l2pf * kKel, n0 + a * kBlockM);
                 mbar_wait(&empty[s], ph ^ 1);
                 if (PAIR == 2) {
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
-                    for (int a = 0; a < wm; ++a)
-                        tma_load_2d_pair(sA + s * a_bytes + a * kABytes, &tmW, full_bar0 + 8u * s, kc,
-                                         n0 + a * kBlockM, pol_w);
+                    if (mc > 1) {
+                        if (w_issuer) tma_load_2d_pair_mc(sA + s * a_bytes, &tmW, &full[s], kc, n0, w_mask, pol_w);
+                    } else {
+                        for (int a = 0; a < wm; ++a)
+                            tma_load_2d_pair(sA + s * a_bytes + a * kABytes, &tmW, full_bar0 + 8u * s, kc,
+                                             n0 + a * kBlockM, pol_w);
+                    }
                     tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows, pol_x);
                 } else {
                     mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
@@ -322,7 +339,7 @@ __global__ void __launch_bounds__(192, 1)
                         }
                     }
                     if (PAIR == 2) {
-                        tc_commit_pair_mc(&empty[s], pair_mask);
+                        tc_commit_pair_mc(&empty[s], mc > 1 ? all_mask : pair_mask);
                         if (i == nkb - 1) tc_commit_pair_mc(tfull, pair_mask);
                     } else {
                         tc_commit(&empty[s]);
@@ -827,7 +844,7 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
         }
     }
     if (pair_min_m > 0 && m_tok >= pair_min_m &&
-        (pair_ctas >= pair_min_ctas || variant == 1 || variant == 2 || variant == 4)) {
+        (pair_ctas >= pair_min_ctas || variant == 1 || variant == 2 || variant == 4 || variant == 7)) {
         g.pair = 2;
         g.wm = 1;
         static const int pair_wm2 = env_knob("TLT_GEMM_PAIR_WM2", 0);  // measured slower (exposed epilogue, 1 CTA/SM)
@@ -850,6 +867,25 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
             g.smem = g.stages * stage_bytes + fixed;
             g.tmem_cols = 2 * bn <= 256 ? 256 : 512;
             return g;
+        }
+        if (variant == 7) {
+            // weight multicast across the token tiles of one weight tile: a
+            // (2 mc, 1, 1) cluster, each weight k-block read from L2 once per
+            // cluster instead of once per token tile
+            int mc = 1;
+            for (int c = 4; c >= 2; --c)
+                if (g.n_ttiles % c == 0) {
+                    mc = c;
+                    break;
+                }
+            if (mc > 1) {
+                g.mc = mc;
+                const int budget = (pair_cps == 2 ? 112 * 1024 : 220 * 1024) - fixed;
+                g.stages = std::max(2, std::min(8, budget / stage_bytes));
+                g.smem = g.stages * stage_bytes + fixed;
+                g.tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+                return g;
+            }
         }
         if (persist >= 1 && m_tok >= pair_persist_min_m) {
             // persistent: one pair per 2 SMs, full smem ring, 2 TMEM accumulators
@@ -1009,7 +1045,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     // the split-K CTAs of one output tile form one cluster (DSMEM reduction);
     // CTA pairs are (2, 1, 1) clusters
     at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = g.pair;
+    at[na].val.clusterDim.x = g.pair * g.mc;
     at[na].val.clusterDim.y = 1;
     at[na].val.clusterDim.z = g.splits;
     ++na;
@@ -1018,8 +1054,10 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     auto kern = g.fp8 ? (g.pair == 2 ? k_gemm_swapab<2, 1> : k_gemm_swapab<1, 1>)
                       : (g.pair == 2 ? k_gemm_swapab<2, 0> : k_gemm_swapab<1, 0>);
     if (g.fp8 && (g.persist || g.splits != 1)) throw CudaError("e4m3 GEMM: only the single-split non-persistent plan");
+    if (g.mc > 1 && (g.pair != 2 || g.splits != 1 || g.wm != 1 || g.n_ttiles % g.mc || g.mc > 4 || g.fp8))
+        throw CudaError("invalid weight-multicast GEMM plan");
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                                       g.tmem_cols, g.wm, g.l2pf, epd);
+                                       g.tmem_cols, g.wm, g.l2pf, g.mc, epd);
     if (e != cudaSuccess) throw CudaError(std::string("gemm launch: ") + cudaGetErrorString(e));
 }
 

@@ -223,6 +223,19 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
         "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(cache_hint)
         : "memory");
 }
+// CTA-pair TMA load multicast to every CTA of `mask` (same smem offset in
+// each); the transaction bytes signal the barrier at `bar_cta`'s offset in
+// each destination's pair leader (the peer bit of the address cleared, as
+// CUTLASS's SM100_TMA_2SM_LOAD_MULTICAST does).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const CUtensorMap* m, uint64_t* bar_cta, int c0,
+                                                    int c1, uint16_t mask, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar_cta) & 0xFEFFFFFFu), "h"(mask), "r"(c0), "r"(c1),
+        "l"(cache_hint)
+        : "memory");
+}
 __device__ __forceinline__ void tc_mma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                                  uint32_t accumulate) {
     asm volatile(

@@ -43,9 +43,10 @@ struct GemmPlan {
     int l2pf = 0;      // weight k-blocks prefetched into L2 ahead of the smem ring
     int persist = 0;   // 1: persistent kernel (double-buffered TMEM accumulators)
     int fp8 = 0;       // 1: e4m3 operands (kind::f8f6f4), per-row / per-token scales in the epilogue
+    int mc = 1;        // CTA pairs per cluster sharing one weight k-block by TMA multicast (pair plans)
     bool same_as(const GemmPlan& o) const {
         return bn == o.bn && n_ttiles == o.n_ttiles && n_wtiles == o.n_wtiles && splits == o.splits &&
-               stages == o.stages && wm == o.wm && pair == o.pair && persist == o.persist;
+               stages == o.stages && wm == o.wm && pair == o.pair && persist == o.persist && mc == o.mc;
     }
 };
 

@@ -52,3 +52,24 @@ def test_gemm_swiglu(m):
     g, u = acc[:, 0::2], acc[:, 1::2]
     ref = torch.nn.functional.silu(g) * u
     assert (y.float() - ref).abs().max().item() < 2e-2 * max(1.0, ref.abs().max().item())
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6, 7])
+@pytest.mark.parametrize("m,k,n", [(272, 3584, 4608), (528, 3584, 3584), (512, 1024, 2304), (1024, 512, 1536),
+                                   (768, 256, 5000), (196, 18944, 512), (300, 4096, 512)])
+def test_gemm_plan_variants(monkeypatch, variant, m, k, n):
+    """Every plan variant the engine's autotuner can pick (deep-ring pairs,
+    persistent pairs, single-CTA tiles, <=128-token pair tiles, pair split-K
+    x4, weight multicast across a (2 mc, 1, 1) cluster) computes the same GEMM."""
+    monkeypatch.setenv("TLT_GEMM_FORCE_VARIANT", str(variant))
+    torch.manual_seed(m + k + n + variant)
+    x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    y = torch.full((m, n), float("nan"), device="cuda", dtype=torch.float32)
+    ws = torch.empty(64 << 20, device="cuda", dtype=torch.float32)
+    rc = _lib.lib().tlt_dev_gemm(x.data_ptr(), m, k, w.data_ptr(), n, 0, y.data_ptr(), None, ws.data_ptr(),
+                                 ws.numel(), 0)
+    assert rc >= 1, _lib.last_error()
+    ref = x.float() @ w.float().t()
+    err = (y - ref).abs().max().item()
+    assert err < 2e-3 * max(1.0, ref.abs().max().item()), (err, rc)
