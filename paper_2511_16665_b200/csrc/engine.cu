@@ -357,6 +357,20 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
     static const int min_m = env_int("TLT_GEMM_AUTOTUNE_MIN_M", 128);
     if (!on || M < min_m || ep_in.norm_w || ep_in.row_scale) return 0;
     const auto key = std::make_tuple(M, N, K, (int)ep_in.kind);
+    // TLT_GEMM_AUTOTUNE_CACHE=path: decisions persisted across processes
+    // (lines "M N K epilogue variant"); a profiler run (ncu replays every
+    // launch, so in-process timings are meaningless there) reuses the plans
+    // an unprofiled run chose
+    static const char* cache_path = std::getenv("TLT_GEMM_AUTOTUNE_CACHE");
+    if (cache_path && !tune_cache_loaded_) {
+        tune_cache_loaded_ = true;
+        if (FILE* f = std::fopen(cache_path, "r")) {
+            int m, n, k, kind, v;
+            while (std::fscanf(f, "%d %d %d %d %d", &m, &n, &k, &kind, &v) == 5)
+                gemm_variant_[std::make_tuple(m, n, k, kind)] = v;
+            std::fclose(f);
+        }
+    }
     auto it = gemm_variant_.find(key);
     if (it != gemm_variant_.end()) return it->second;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -374,7 +388,10 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
     }
     std::vector<GemmPlan> plans;
     std::vector<int> vars;
-    for (int v : {0, 1, 2, 3, 4, 6, 7}) {
+    // variants 6 (pair split-K x4) and 7 (weight multicast) are kept for
+    // experiments (TLT_GEMM_FORCE_VARIANT / tests) but not autotuned: they
+    // win on too few shapes (profiles/r2_gemm_variants.txt, r2_gemm_multicast.txt)
+    for (int v : {0, 1, 2, 3, 4}) {
         const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, v);
         bool dup = false;
         for (const auto& q : plans) dup = dup || q.same_as(g);
@@ -411,6 +428,11 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
         }
     }
     gemm_variant_[key] = best;
+    if (cache_path)
+        if (FILE* f = std::fopen(cache_path, "a")) {
+            std::fprintf(f, "%d %d %d %d %d\n", M, N, K, (int)ep_in.kind, best);
+            std::fclose(f);
+        }
     return best;
 }
 

@@ -124,6 +124,7 @@ private:
     int tuned_variant(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, int N, const EpiParams& ep);
     std::map<std::tuple<int, int, int, int>, int> gemm_variant_;  // autotuned plan variant per (M, N, K, epilogue)
     cudaEvent_t tune_ev0_ = nullptr, tune_ev1_ = nullptr;
+    bool tune_cache_loaded_ = false;
     void layer_forward(const LayerW& w, bf16* kc, bf16* vc, int cache_cap, const Rows& rw, const Groups& gp, int R,
                        int rpr, int ngroups, int max_keys, bool h_ready, const bf16* next_norm);
     void gemm_resid_norm(const bf16* X, int M, int K, long long ldx, const CUtensorMap& tmW, const bf16* norm_w);
