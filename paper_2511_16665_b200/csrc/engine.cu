@@ -391,7 +391,9 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
     // variants 6 (pair split-K x4) and 7 (weight multicast) are kept for
     // experiments (TLT_GEMM_FORCE_VARIANT / tests) but not autotuned: they
     // win on too few shapes (profiles/r2_gemm_variants.txt, r2_gemm_multicast.txt)
-    for (int v : {0, 1, 2, 3, 4}) {
+    static const bool all_variants = env_int("TLT_GEMM_AUTOTUNE_ALL", 0) != 0;
+    for (int v : {0, 1, 2, 3, 4, 6, 7}) {
+        if (!all_variants && v >= 6) continue;
         const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, v);
         bool dup = false;
         for (const auto& q : plans) dup = dup || q.same_as(g);
