@@ -472,6 +472,40 @@ def token_match(sd_tokens, ar_tokens):
             "prefix_match_rate": round(same / max(1, tot), 6), "first_divergence_positions": first_div[:16]}
 
 
+def divergence_margins(eng, prompts, sd_tokens, ar_tokens, limit=16, atol=0.05, rtol=0.01):
+    """At each diverging request's first SD/AR difference: the target's fp32
+    logits for the two candidate tokens, from a prefill of prompt ++ the
+    common prefix and one debug plain-decode step. Greedy SD is lossless up to
+    floating-point near-ties of the top-2 target logits (the verify forward
+    runs another row batch / GEMM tiling than plain decode, so bf16 rounding
+    differs); a margin within the tests' tolerance (tests/parity_util.py
+    greedy_streams_agree: 2 (atol + rtol |logit|)) is a tie, not an error."""
+    out = []
+    eng.set_debug(True)
+    try:
+        for p, s, r in zip(prompts, sd_tokens, ar_tokens):
+            if s == r or len(out) >= limit:
+                continue
+            k = next((j for j in range(min(len(s), len(r))) if s[j] != r[j]), None)
+            if k is None:  # one stream is a prefix of the other (EOS / max_len cut)
+                continue
+            eng.prefill([0], [p + r[:k]])
+            eng.ar_step([0])
+            lg = eng.debug_ar_logits(1)[0]
+            eng.release(0)
+            a, b = float(lg[r[k]]), float(lg[s[k]])
+            top2 = np.sort(lg)[-2:]
+            out.append({"pos": k, "margin": abs(a - b), "tol": 2 * (atol + rtol * max(abs(a), abs(b))),
+                        "top2_gap": float(top2[1] - top2[0])})
+    finally:
+        eng.set_debug(False)
+    return {"checked": len(out), "within_tol": sum(1 for x in out if x["margin"] <= x["tol"]),
+            "max_margin": round(max((x["margin"] for x in out), default=0.0), 5),
+            "min_tol": round(min((x["tol"] for x in out), default=0.0), 5),
+            "note": "first SD/AR divergences: |logit(ar tok) - logit(sd tok)| of the target at that position vs "
+                    "2 (0.05 + 0.01 |logit|); within tol = a floating-point near-tie"}
+
+
 def run_ours(a):
     world, rank, local, pg = dist_setup(a.gpus)
     import torch
@@ -592,6 +626,8 @@ def run_ours(a):
     ar_tok_s = ar["emitted_total"] / (ar["device_ms"] / 1e3) if ar else None
     sd_same = res[0] if res else None
     match = token_match(sd_same["tokens"], ar["tokens"]) if (ar and sd_same) else None
+    if match is not None and rank == 0 and match["identical_requests"] < match["requests"]:
+        match["divergences"] = divergence_margins(eng, workload(a.warmup)[1], sd_same["tokens"], ar["tokens"])
     out = None
     if rank == 0:
         print("[bench] probes", file=sys.stderr, flush=True)

@@ -472,6 +472,10 @@ TLT_API int tlt_probe_attention(tlt_engine* e, int b, int ctx, int rows_per_req,
  * 3 SwiGLU (W rows interleaved gate/up). Returns the split-K factor used. */
 TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32, void* y_bf16,
                          float* ws, long long ws_elems, int max_splits);
+/* tlt_dev_gemm with a device-resident live-row count (the graph pool's
+ * padding-tile skip, EpiParams::dyn_n): rows >= *live_rows may stay unwritten. */
+TLT_API int tlt_dev_gemm_live(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
+                              void* y_bf16, float* ws, long long ws_elems, const int* live_rows);
 /* Average device ms of one GEMM launch over `iters` back-to-back launches
  * (CUDA events on a private stream). Returns the split-K factor. */
 TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,

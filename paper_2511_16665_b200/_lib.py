@@ -51,6 +51,9 @@ def _declare(L: C.CDLL) -> None:
     L.tlt_dev_gemm.restype = C.c_int
     L.tlt_dev_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int]
+    L.tlt_dev_gemm_live.restype = C.c_int
+    L.tlt_dev_gemm_live.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]
     L.tlt_dev_gemm_e4m3.restype = C.c_int
     L.tlt_dev_gemm_e4m3.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int] + [C.c_void_p] * 5
     L.tlt_dev_attention.restype = C.c_int

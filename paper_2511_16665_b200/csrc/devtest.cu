@@ -10,8 +10,8 @@
 
 using namespace tlt;
 
-extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
-                                    void* y_bf16, float* ws, long long ws_elems, int max_splits) {
+static int dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32, void* y_bf16,
+                    float* ws, long long ws_elems, int max_splits, const int* dyn_n) {
     try {
         GemmPlan g = plan_gemm(m, n, k, std::getenv("TLT_GEMM_FORCE_VARIANT") ? std::atoi(std::getenv("TLT_GEMM_FORCE_VARIANT")) : 0);
         if (max_splits > 0 && g.splits > max_splits) {
@@ -28,6 +28,8 @@ extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, 
         ep.ld_f32 = kind == EPI_SWIGLU ? n / 2 : n;
         ep.out_bf16 = static_cast<__nv_bfloat16*>(y_bf16);
         ep.ld_bf16 = kind == EPI_SWIGLU ? n / 2 : n;
+        ep.dyn_n = dyn_n;
+        ep.dyn_rpr = 1;
         launch_gemm(g, tw, tx, ep, ws, static_cast<size_t>(ws_elems), 0);
         CUDA_CHECK(cudaDeviceSynchronize());
         return g.splits;
@@ -35,6 +37,18 @@ extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, 
         tlt_set_last_error(e.what());
         return -1;
     }
+}
+
+extern "C" TLT_API int tlt_dev_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
+                                    void* y_bf16, float* ws, long long ws_elems, int max_splits) {
+    return dev_gemm(x, m, k, w, n, kind, y_f32, y_bf16, ws, ws_elems, max_splits, nullptr);
+}
+
+// As tlt_dev_gemm with a device-resident live-row count (the bucketed graph
+// pool's padding skip): rows >= *live_rows may be left unwritten.
+extern "C" TLT_API int tlt_dev_gemm_live(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,
+                                         void* y_bf16, float* ws, long long ws_elems, const int* live_rows) {
+    return dev_gemm(x, m, k, w, n, kind, y_f32, y_bf16, ws, ws_elems, 0, live_rows);
 }
 
 // Average device time of one GEMM launch (incl. its split-K reduce), `iters`

@@ -204,10 +204,14 @@ __global__ void __launch_bounds__(192, 1)
     const int t0 = (blockIdx.x / PAIR) * bn;
     const int z = blockIdx.z;
     const int kb0 = z * kb_per_split;
-    // padding token tile of a bucketed graph: no loads, no MMA, no epilogue
-    // (every CTA of a pair / split-K cluster shares t0, so they skip together)
+    // padding token tile of a bucketed graph: no loads, no MMA, no epilogue.
+    // Every CTA of a pair / split-K cluster shares t0, so they skip together;
+    // a multicast cluster spans mc token tiles and must skip as a whole (its
+    // weight issuer signals every pair's barriers): it skips only when its
+    // first token tile is padding, otherwise all its pairs run
     const int m_live = epi_live_rows(ep);
-    const bool skip = t0 >= m_live;
+    const int t_first = mc > 1 ? (int)((blockIdx.x / PAIR) / mc * mc) * bn : t0;
+    const bool skip = t_first >= m_live;
     const int nkb = skip ? 0 : min(kb_total, kb0 + kb_per_split) - kb0;
 
     if (warp == 0 && lane == 0) {

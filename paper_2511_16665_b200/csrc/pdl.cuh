@@ -8,7 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
 #include <string>
+#include <unordered_set>
 
 #include "tlt_internal.h"
 
@@ -39,8 +41,32 @@ inline int pdl_mask() {
 }
 inline bool pdl_enabled(int bit = 2) { return (pdl_mask() & bit) != 0; }
 
+// TLT_SMEM_CARVEOUT=1: every engine kernel prefers the maximum shared-memory
+// carveout, the one the tcgen05 GEMMs (226 KB) need, so the L1 / shared split
+// of an SM is never reconfigured between consecutive kernels of a step (a
+// reconfiguration drains the SM and keeps a PDL-launched GEMM CTA from
+// co-residing with the previous kernel's tail).
+inline bool smem_carveout_max() {
+    static const bool on = [] {
+        const char* v = std::getenv("TLT_SMEM_CARVEOUT");
+        return v ? std::atoi(v) != 0 : false;
+    }();
+    return on;
+}
+
+template <typename... KArgs>
+inline void set_max_carveout(void (*kern)(KArgs...)) {
+    if (!smem_carveout_max()) return;
+    static std::mutex mu;
+    static std::unordered_set<const void*> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert(reinterpret_cast<const void*>(kern)).second)
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    set_max_carveout(kern);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;

@@ -73,3 +73,28 @@ def test_gemm_plan_variants(monkeypatch, variant, m, k, n):
     ref = x.float() @ w.float().t()
     err = (y - ref).abs().max().item()
     assert err < 2e-3 * max(1.0, ref.abs().max().item()), (err, rc)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 6, 7])
+@pytest.mark.parametrize("m,k,n,live", [(1024, 512, 1536, 130), (1024, 512, 1536, 1), (528, 3584, 3584, 300),
+                                        (768, 256, 5000, 767), (272, 3584, 4608, 0)])
+def test_gemm_live_rows_skip(monkeypatch, variant, m, k, n, live):
+    """The graph pool's padding skip (device live-row count): rows below the
+    live count are exact for every plan variant, including weight multicast,
+    whose (2 mc, 1, 1) cluster spans several token tiles and must skip as a
+    whole (a partially live multicast cluster once wedged / faulted)."""
+    monkeypatch.setenv("TLT_GEMM_FORCE_VARIANT", str(variant))
+    torch.manual_seed(m + n + live + variant)
+    x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    y = torch.full((m, n), float("nan"), device="cuda", dtype=torch.float32)
+    ws = torch.empty(64 << 20, device="cuda", dtype=torch.float32)
+    lv = torch.tensor([live], device="cuda", dtype=torch.int32)
+    for _ in range(3):
+        rc = _lib.lib().tlt_dev_gemm_live(x.data_ptr(), m, k, w.data_ptr(), n, 0, y.data_ptr(), None,
+                                          ws.data_ptr(), ws.numel(), lv.data_ptr())
+        assert rc >= 1, _lib.last_error()
+    if live:
+        ref = x[:live].float() @ w.float().t()
+        err = (y[:live] - ref).abs().max().item()
+        assert err < 2e-3 * max(1.0, ref.abs().max().item()), (err, rc)
