@@ -51,6 +51,34 @@ extern "C" TLT_API int tlt_dev_gemm_live(const void* x, int m, int k, const void
     return dev_gemm(x, m, k, w, n, kind, y_f32, y_bf16, ws, ws_elems, 0, live_rows);
 }
 
+// LM head with the fused top-k epilogue (EPI_TOPK, whole-K accumulators) and
+// the per-row merge, as Engine::lm_topk runs it: logits never leave the SM.
+// part: [ceil(n/128)][m][2 + 2k] floats. Returns the plan's CTA-pair factor.
+extern "C" TLT_API int tlt_dev_lm_topk(const void* x, int m, int k, const void* w, int n, int topk, float* part,
+                                       int* out_tok, float* out_logit, float* out_M, float* out_S) {
+    try {
+        if (topk < 1 || topk > 8) throw ConfigErr("topk", "must be in [1, 8]");
+        GemmPlan g = plan_gemm(m, n, k, std::getenv("TLT_GEMM_FORCE_VARIANT") ? std::atoi(std::getenv("TLT_GEMM_FORCE_VARIANT")) : 0);
+        g.kb_per_split = g.kb_total;
+        g.splits = 1;
+        CUtensorMap tw = make_tmap_bf16(w, n, k, k, 128);
+        CUtensorMap tx = make_tmap_bf16(x, m, k, k, g.box_rows);
+        EpiParams ep{};
+        ep.kind = EPI_TOPK;
+        ep.n_out = n;
+        ep.m_tok = m;
+        ep.out_f32 = part;
+        ep.topk_k = topk;
+        launch_gemm(g, tw, tx, ep, nullptr, 0, 0);
+        launch_topk_merge(part, (n + 127) / 128, m, topk, nullptr, out_tok, out_logit, out_M, out_S, 0);
+        CUDA_CHECK(cudaDeviceSynchronize());
+        return g.pair;
+    } catch (const std::exception& e) {
+        tlt_set_last_error(e.what());
+        return -1;
+    }
+}
+
 // Average device time of one GEMM launch (incl. its split-K reduce), `iters`
 // back-to-back launches on a private stream bracketed by CUDA events.
 extern "C" TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n, int kind, float* y_f32,

@@ -125,6 +125,103 @@ __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem
     }
 }
 
+// k > 1 (drafter children, k <= 8): the same partial record by K extraction
+// rounds instead of per-element sorted insertion. Each of the 8 threads of a
+// token keeps only its current best of its 16 entries; a round is a 3-step
+// butterfly argmax over the 8 threads (logit desc, id asc), the winning
+// thread drops that entry and rescans its 16. About a third of the
+// instructions of the insertion merge, so the epilogue of one tile hides
+// under the co-resident CTA's mainloop and the drafter's fp32 logits never
+// reach HBM.
+template <int KM>
+__device__ __forceinline__ void epi_topk_tile_rounds(const EpiParams& ep, uint32_t tmem, int q, int lane, int n0,
+                                                     int t0, int bn, float* tr, int tile) {
+    const int K = ep.topk_k;
+    const int W = 2 + 2 * K;
+    const int ep_tid = threadIdx.x - 64;  // 0..127
+    const int col = ep_tid >> 3, part = ep_tid & 7;
+    const int id0 = n0 + part * 16;
+    for (int c = 0; c < bn; c += 16) {
+        if (t0 + c >= ep.m_tok) break;
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tr[j * 128 + q * 32 + lane] = v[j];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const float* src = tr + col * 128 + part * 16;
+        float xs[16];
+        float bv = -CUDART_INF_F;
+        int bi = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            xs[i] = id0 + i < ep.n_out ? src[i] : -CUDART_INF_F;
+            if (xs[i] > bv) {  // strict: the lowest index among equal values
+                bv = xs[i];
+                bi = i;
+            }
+        }
+        // (m, s) of the tile's 128 entries for this token
+        float m = bv, s = 0.f;
+        if (m != -CUDART_INF_F) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) s += __expf(xs[i] - m);  // exp(-inf) = 0
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const float om = __shfl_xor_sync(0xffffffffu, m, o);
+            const float os = __shfl_xor_sync(0xffffffffu, s, o);
+            const float nm = fmaxf(m, om);
+            const float a = m == -CUDART_INF_F ? 0.f : s * __expf(m - nm);
+            const float b = om == -CUDART_INF_F ? 0.f : os * __expf(om - nm);
+            s = a + b;
+            m = nm;
+        }
+        float lv[KM];
+        int li[KM];
+#pragma unroll
+        for (int r = 0; r < KM; ++r) {
+            float wv = bv;
+            int wi = bv == -CUDART_INF_F ? 0x7fffffff : id0 + bi;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, wv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, wi, o);
+                if (ov > wv || (ov == wv && oi < wi)) {
+                    wv = ov;
+                    wi = oi;
+                }
+            }
+            lv[r] = wv;
+            li[r] = wi;
+            if (r + 1 < KM && wv != -CUDART_INF_F && wi == id0 + bi) {  // this thread's entry won: next best
+#pragma unroll
+                for (int i = 0; i < 16; ++i) xs[i] = i == bi ? -CUDART_INF_F : xs[i];
+                bv = -CUDART_INF_F;
+                bi = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (xs[i] > bv) {
+                        bv = xs[i];
+                        bi = i;
+                    }
+            }
+        }
+        const int tok = t0 + c + col;
+        if (part == 0 && tok < ep.m_tok) {
+            float* out = ep.out_f32 + ((long long)tile * ep.m_tok + tok) * W;
+            out[0] = m;
+            out[1] = s;
+#pragma unroll
+            for (int r = 0; r < KM; ++r) {
+                if (r < K) {
+                    out[2 + r] = lv[r];
+                    out[2 + K + r] = __int_as_float(li[r]);
+                }
+            }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+}
 
 __device__ __forceinline__ float* align16f(void* p) {
     return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
@@ -386,7 +483,7 @@ __global__ void __launch_bounds__(192, 1)
             if (ep.topk_k <= 1)
                 epi_topk_tile<1>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
             else
-                epi_topk_tile<kEpiTopkMax>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
+                epi_topk_tile_rounds<kEpiTopkMax>(ep, tm_a, q, lane, na, t0, bn, tr, tile);
         } else {
             epi_tile_staged(ep, tm_a, q, lane, na, t0, bn, reinterpret_cast<float*>(smem));
         }
@@ -677,7 +774,7 @@ __global__ void __launch_bounds__(192, 1)
                     if (ep.topk_k <= 1)
                         epi_topk_tile<1>(ep, acc, q, lane, n0, t0, bn, tr, tile);
                     else
-                        epi_topk_tile<kEpiTopkMax>(ep, acc, q, lane, n0, t0, bn, tr, tile);
+                        epi_topk_tile_rounds<kEpiTopkMax>(ep, acc, q, lane, n0, t0, bn, tr, tile);
                 } else {
                     epi_tile_staged(ep, acc, q, lane, n0, t0, bn, tr);
                 }

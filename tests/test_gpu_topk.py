@@ -49,3 +49,46 @@ def test_row_topk(R, V, k, pattern):
     assert torch.equal(M, x.max(dim=1).values)
     Sref = torch.exp(x.double() - x.max(dim=1, keepdim=True).values.double()).sum(dim=1)
     assert torch.allclose(S.double(), Sref, rtol=1e-4)
+
+
+def lm_topk(x, w, k):
+    m, n = x.shape[0], w.shape[0]
+    part = torch.empty(((n + 127) // 128) * m * (2 + 2 * k), device="cuda")
+    tok = torch.empty(m, k, dtype=torch.int32, device="cuda")
+    val = torch.empty(m, k, device="cuda")
+    M = torch.empty(m, device="cuda")
+    S = torch.empty(m, device="cuda")
+    rc = _lib.lib().tlt_dev_lm_topk(x.data_ptr(), m, x.shape[1], w.data_ptr(), n, k, part.data_ptr(), tok.data_ptr(),
+                                    val.data_ptr(), M.data_ptr(), S.data_ptr())
+    assert rc >= 1, _lib.last_error()
+    return tok, val, M, S
+
+
+@pytest.mark.parametrize("variant", [0, 2, 3])
+@pytest.mark.parametrize("m,n,k", [(8, 152064, 3584), (64, 152064, 3584), (248, 152064, 3584), (496, 20000, 512),
+                                   (3, 1000, 256), (130, 4099, 512)])
+@pytest.mark.parametrize("topk", [8, 4, 2, 1])
+def test_fused_lm_head_topk(monkeypatch, variant, m, n, k, topk):
+    """The LM head's fused top-k epilogue (drafter children, logits never in
+    HBM) against the same tcgen05 GEMM's materialised fp32 logits (whole-K
+    accumulators, one split): ids by (logit desc, id asc) and values exact,
+    M exact, S within fp32 tolerance."""
+    monkeypatch.setenv("TLT_GEMM_FORCE_VARIANT", str(variant))
+    g = torch.Generator(device="cuda").manual_seed(m + n + topk)
+    x = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda", generator=g) / k ** 0.5).to(torch.bfloat16)
+    if m >= 8:  # exact ties across vocabulary tiles: duplicate weight rows
+        w[n // 2] = w[3]
+        w[n - 1] = w[3]
+    logits = torch.empty(m, n, device="cuda")
+    ws = torch.empty(1 << 20, device="cuda")
+    assert _lib.lib().tlt_dev_gemm(x.data_ptr(), m, k, w.data_ptr(), n, 0, logits.data_ptr(), None, ws.data_ptr(),
+                                   ws.numel(), 1) >= 1, _lib.last_error()
+    tok, val, M, S = lm_topk(x, w, topk)
+    torch.cuda.synchronize()
+    want = ref_topk(logits, topk)
+    assert torch.equal(tok.long(), want), (tok[:2], want[:2])
+    assert torch.equal(val, torch.gather(logits, 1, want))
+    assert torch.equal(M, logits.max(dim=1).values)
+    Sref = torch.exp(logits.double() - logits.max(dim=1, keepdim=True).values.double()).sum(dim=1)
+    assert torch.allclose(S.double(), Sref, rtol=1e-4)
