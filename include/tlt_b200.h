@@ -482,9 +482,11 @@ TLT_API int tlt_dev_time_gemm(const void* x, int m, int k, const void* w, int n,
                               void* y_bf16, float* ws, long long ws_elems, int iters, float* avg_ms);
 /* LM head with the fused top-k epilogue: per row the top-k of x W^T by
  * (logit desc, id asc), M = max and S = sum exp(l - M), without materialising
- * the logits (part: [ceil(n/128)][m][2+2k] floats of scratch). Returns >= 1. */
+ * the logits (part: [ceil(n/128)][m][2+2k] floats of scratch; thr: null or m
+ * zeroed uints for the per-row k-th-value bounds, zeroed again on return).
+ * Returns >= 1. */
 TLT_API int tlt_dev_lm_topk(const void* x, int m, int k, const void* w, int n, int topk, float* part, int* out_tok,
-                            float* out_logit, float* out_M, float* out_S);
+                            float* out_logit, float* out_M, float* out_S, unsigned* thr);
 /* Row top-k by (logit desc, id asc) + row max M and S = sum exp(l - M) over
  * fp32 logits [R][V] (the drafter child selection); `part` is scratch of
  * [ceil(V/128)][R][2+2k] floats. Average ms over `iters` launches. Returns the

@@ -52,7 +52,7 @@ def _declare(L: C.CDLL) -> None:
     L.tlt_dev_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int]
     L.tlt_dev_lm_topk.restype = C.c_int
-    L.tlt_dev_lm_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 5
+    L.tlt_dev_lm_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 6
     L.tlt_dev_gemm_live.restype = C.c_int
     L.tlt_dev_gemm_live.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]

@@ -53,9 +53,11 @@ extern "C" TLT_API int tlt_dev_gemm_live(const void* x, int m, int k, const void
 
 // LM head with the fused top-k epilogue (EPI_TOPK, whole-K accumulators) and
 // the per-row merge, as Engine::lm_topk runs it: logits never leave the SM.
-// part: [ceil(n/128)][m][2 + 2k] floats. Returns the plan's CTA-pair factor.
+// part: [ceil(n/128)][m][2 + 2k] floats; thr: null or [m] zeroed uints (the
+// per-row k-th-value bounds, left zeroed by the merge). Returns the plan's
+// CTA-pair factor.
 extern "C" TLT_API int tlt_dev_lm_topk(const void* x, int m, int k, const void* w, int n, int topk, float* part,
-                                       int* out_tok, float* out_logit, float* out_M, float* out_S) {
+                                       int* out_tok, float* out_logit, float* out_M, float* out_S, unsigned* thr) {
     try {
         if (topk < 1 || topk > 8) throw ConfigErr("topk", "must be in [1, 8]");
         GemmPlan g = plan_gemm(m, n, k, std::getenv("TLT_GEMM_FORCE_VARIANT") ? std::atoi(std::getenv("TLT_GEMM_FORCE_VARIANT")) : 0);
@@ -69,8 +71,9 @@ extern "C" TLT_API int tlt_dev_lm_topk(const void* x, int m, int k, const void* 
         ep.m_tok = m;
         ep.out_f32 = part;
         ep.topk_k = topk;
+        ep.topk_thr = topk > 1 ? thr : nullptr;
         launch_gemm(g, tw, tx, ep, nullptr, 0, 0);
-        launch_topk_merge(part, (n + 127) / 128, m, topk, nullptr, out_tok, out_logit, out_M, out_S, 0);
+        launch_topk_merge(part, (n + 127) / 128, m, topk, nullptr, out_tok, out_logit, out_M, out_S, 0, ep.topk_thr);
         CUDA_CHECK(cudaDeviceSynchronize());
         return g.pair;
     } catch (const std::exception& e) {

@@ -151,7 +151,9 @@ Engine::~Engine() {
     f(arena_), f(arena_n_), f(kept_), f(kept_n_), f(exp_n_), f(done_);
     f(tree_tok_), f(tree_par_), f(tree_dep_), f(tree_n_), f(tree_prob_), f(tree_pp_);
     f(acc_nodes_), f(acc_tok_), f(acc_len_), f(bonus_), f(kv_len_), f(ar_tok_), f(d_step_);
+    f(topk_part_), f(topk_thr_), f(d_nreal_);
     if (h_step_) cudaFreeHost(h_step_);
+    if (h_nreal_) cudaFreeHost(h_nreal_);
     void* hp[] = {ho_.acc_len, ho_.bonus, ho_.acc_tok, ho_.acc_nodes, ho_.tree_tok, ho_.tree_par,
                   ho_.tree_dep, ho_.tree_prob, ho_.tree_pp, ho_.tree_n, ho_.ar_tok};
     for (void* p : hp)
@@ -273,6 +275,8 @@ void Engine::alloc_state() {
     tk_S_ = dmalloc<float>(R_);
     argmax_ = dmalloc<int>(R_);
     topk_part_ = dmalloc<float>((size_t)((V + 127) / 128) * R_ * (2 + 2 * kEpiTopkMax));
+    topk_thr_ = dmalloc<unsigned>(R_);
+    CUDA_CHECK(cudaMemset(topk_thr_, 0, sizeof(unsigned) * R_));
     arena_ = dmalloc<Cand>((size_t)S * arena_cap_);
     arena_n_ = dmalloc<int>(S);
     kept_ = dmalloc<int>((size_t)S * kMaxT);
@@ -702,9 +706,10 @@ void Engine::lm_topk(const float* x, int n, int k, const int* live, bool want_lo
     e.kind = EPI_TOPK;
     e.out_f32 = topk_part_;
     e.topk_k = k;
+    e.topk_thr = k > 1 ? topk_thr_ : nullptr;
     gemm(h_, n, cfg.hidden, cfg.hidden, tm_lm_, cfg.vocab, e);
     const int n_tiles = (cfg.vocab + 127) / 128;
-    launch_topk_merge(topk_part_, n_tiles, n, k, live, tk_tok_, tk_logit_, tk_M_, tk_S_, st_);
+    launch_topk_merge(topk_part_, n_tiles, n, k, live, tk_tok_, tk_logit_, tk_M_, tk_S_, st_, e.topk_thr);
     count_launch();
     if (want_logits) {
         EpiParams f{};

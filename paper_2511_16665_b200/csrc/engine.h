@@ -144,6 +144,7 @@ private:
     float *lm8_s_ = nullptr, *h8_s_ = nullptr;
     CUtensorMap tm_lm8_;
     float* topk_part_ = nullptr;  // EPI_TOPK partials [vocab tiles][R][2 + 2k]
+    unsigned* topk_thr_ = nullptr;  // EPI_TOPK k > 1 per-row k-th-value bounds [R] (0 = none)
     void scatter_features(const Rows& rw, int R, const bf16* feat);
     float catchup_drafter(int b, const int32_t* slots);
     void sd_device_sequence(int b_hi, int D, int k, int T, bool dbg, int b_real, bool verify = true);

@@ -165,8 +165,9 @@ bool attention_tree_tc_eligible(const AttnParams& p);
 void launch_attention_tree_tc(const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, cudaStream_t st);
 
 int launch_row_topk_chunked(const float* logits, int R, int V, const int* live, int k, float* part, cudaStream_t st);
+// thr_reset: the fused LM head's per-row bound array (EpiParams::topk_thr), cleared per row
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,
-                       float* out_M, float* out_S, cudaStream_t st);
+                       float* out_M, float* out_S, cudaStream_t st, unsigned* thr_reset = nullptr);
 void launch_row_probs(const float* logits, int R, int V, const float* M, const float* S, double* out,
                       cudaStream_t st);
 void launch_rows_level1(const StepIn* st, int b, int b_hi, int D1, const Rows& rows, const Groups& g, int* root_row,

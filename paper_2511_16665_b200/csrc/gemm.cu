@@ -125,6 +125,15 @@ __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem
     }
 }
 
+// order-preserving float <-> uint (x < y  <=>  ord(x) < ord(y); ord > 0)
+__device__ __forceinline__ unsigned float_to_ord(float f) {
+    const unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord_to_float(unsigned o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
 // k > 1 (drafter children, k <= 8): the same partial record by K extraction
 // rounds instead of per-element sorted insertion. Each of the 8 threads of a
 // token keeps only its current best of its 16 entries; a round is a 3-step
@@ -132,7 +141,11 @@ __device__ __forceinline__ void epi_topk_tile(const EpiParams& ep, uint32_t tmem
 // thread drops that entry and rescans its 16. About a third of the
 // instructions of the insertion merge, so the epilogue of one tile hides
 // under the co-resident CTA's mainloop and the drafter's fp32 logits never
-// reach HBM.
+// reach HBM. With ep.topk_thr the rounds stop once the winner falls below the
+// token's running k-th-value bound (most vocabulary tiles after the first
+// wave stop after round 0); the record is then padded with -inf, which the
+// merge ignores, so the merged top-k (and M, S, computed in full) does not
+// depend on which tiles stopped early.
 template <int KM>
 __device__ __forceinline__ void epi_topk_tile_rounds(const EpiParams& ep, uint32_t tmem, int q, int lane, int n0,
                                                      int t0, int bn, float* tr, int tile) {
@@ -176,8 +189,22 @@ __device__ __forceinline__ void epi_topk_tile_rounds(const EpiParams& ep, uint32
             s = a + b;
             m = nm;
         }
+        const int tok = t0 + c + col;
+        // entries below a proven lower bound of the token's k-th largest
+        // logit (some finished tile's k-th value) cannot reach the top-k
+        float thr_v = -CUDART_INF_F;
+        if (ep.topk_thr && tok < ep.m_tok) {
+            const unsigned o = __ldcg(ep.topk_thr + tok);
+            if (o) thr_v = ord_to_float(o);
+        }
         float lv[KM];
         int li[KM];
+#pragma unroll
+        for (int r = 0; r < KM; ++r) {
+            lv[r] = -CUDART_INF_F;
+            li[r] = 0x7fffffff;
+        }
+        bool stop = false;
 #pragma unroll
         for (int r = 0; r < KM; ++r) {
             float wv = bv;
@@ -191,9 +218,12 @@ __device__ __forceinline__ void epi_topk_tile_rounds(const EpiParams& ep, uint32
                     wi = oi;
                 }
             }
-            lv[r] = wv;
-            li[r] = wi;
-            if (r + 1 < KM && wv != -CUDART_INF_F && wi == id0 + bi) {  // this thread's entry won: next best
+            if (!stop) {
+                lv[r] = wv;
+                li[r] = wi;
+            }
+            stop = stop || wv == -CUDART_INF_F || wv < thr_v;
+            if (r + 1 < KM && !stop && wi == id0 + bi) {  // this thread's entry won: next best
 #pragma unroll
                 for (int i = 0; i < 16; ++i) xs[i] = i == bi ? -CUDART_INF_F : xs[i];
                 bv = -CUDART_INF_F;
@@ -205,8 +235,15 @@ __device__ __forceinline__ void epi_topk_tile_rounds(const EpiParams& ep, uint32
                         bi = i;
                     }
             }
+            if (__all_sync(0xffffffffu, stop)) break;  // the warp's 4 tokens are done
         }
-        const int tok = t0 + c + col;
+        if (ep.topk_thr && part == 0 && tok < ep.m_tok) {
+            float kth = -CUDART_INF_F;
+#pragma unroll
+            for (int r = 0; r < KM; ++r)
+                if (r == K - 1) kth = lv[r];
+            if (kth != -CUDART_INF_F && kth > thr_v) atomicMax(ep.topk_thr + tok, float_to_ord(kth));
+        }
         if (part == 0 && tok < ep.m_tok) {
             float* out = ep.out_f32 + ((long long)tile * ep.m_tok + tok) * W;
             out[0] = m;

@@ -52,6 +52,11 @@ struct EpiParams {
     int max_ctx;
     // EPI_TOPK: out_f32 = partials [n_wtiles][m_tok][2 + 2*topk_k] (m, s, vals[k], ids[k])
     int topk_k;
+    // k > 1: per-token running lower bound of the row's k-th largest logit
+    // (order-preserving uint encoding, 0 = none; atomicMax'ed by finished
+    // tiles, reset to 0 by k_topk_merge): a tile whose maximum is below it
+    // cannot contribute and skips its extraction rounds. Null: off.
+    unsigned* topk_thr;
     int dbg;  // diagnostics (TLT_GEMM_DBG): bit0 skip MMA, bit1 skip epilogue
     // fused RMSNorm after EPI_RESID_ADD (long-tail M): the last CTA writes
     // norm_out[t] = bf16(rmsnorm(out_f32[t]) * norm_w) for every token row

@@ -755,12 +755,15 @@ template <int K>
 __global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ part, int n_tiles, int m_tok, int k,
                                                     const int* __restrict__ live, int* __restrict__ out_tok,
                                                     float* __restrict__ out_logit, float* __restrict__ out_M,
-                                                    float* __restrict__ out_S) {
+                                                    float* __restrict__ out_S, unsigned* __restrict__ thr_reset) {
     pdl_wait();
     __shared__ float sv[8 * K];
     __shared__ int si[8 * K];
     __shared__ float sm[8], ss[8];
     const int r = blockIdx.x;
+    // the LM head's per-row k-th-value bound (EpiParams::topk_thr) is spent:
+    // clear it for the next launch, dead rows included
+    if (thr_reset && threadIdx.x == 0) thr_reset[r] = 0u;
     if (live && live[r] < 0) return;
     const int W = 2 + 2 * k;
     float m = -CUDART_INF_F, s = 0.f;
@@ -850,15 +853,19 @@ __global__ void __launch_bounds__(256) k_topk_merge(const float* __restrict__ pa
     }
 }
 void launch_topk_merge(const float* part, int n_tiles, int R, int k, const int* live, int* out_tok, float* out_logit,
-                       float* out_M, float* out_S, cudaStream_t st) {
+                       float* out_M, float* out_S, cudaStream_t st, unsigned* thr_reset) {
     if (k <= 1)
-        launch_pdl(k_topk_merge<1>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<1>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S,
+                   thr_reset);
     else if (k <= 2)
-        launch_pdl(k_topk_merge<2>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<2>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S,
+                   thr_reset);
     else if (k <= 4)
-        launch_pdl(k_topk_merge<4>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<4>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S,
+                   thr_reset);
     else
-        launch_pdl(k_topk_merge<8>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S);
+        launch_pdl(k_topk_merge<8>, R, 256, 0, st, part, n_tiles, R, k, live, out_tok, out_logit, out_M, out_S,
+                   thr_reset);
 }
 
 // full fp64 distribution of a row (parity/debug export): p = exp((double)(l-M))/S

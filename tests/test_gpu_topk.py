@@ -51,7 +51,7 @@ def test_row_topk(R, V, k, pattern):
     assert torch.allclose(S.double(), Sref, rtol=1e-4)
 
 
-def lm_topk(x, w, k):
+def lm_topk(x, w, k, thr=None):
     m, n = x.shape[0], w.shape[0]
     part = torch.empty(((n + 127) // 128) * m * (2 + 2 * k), device="cuda")
     tok = torch.empty(m, k, dtype=torch.int32, device="cuda")
@@ -59,20 +59,23 @@ def lm_topk(x, w, k):
     M = torch.empty(m, device="cuda")
     S = torch.empty(m, device="cuda")
     rc = _lib.lib().tlt_dev_lm_topk(x.data_ptr(), m, x.shape[1], w.data_ptr(), n, k, part.data_ptr(), tok.data_ptr(),
-                                    val.data_ptr(), M.data_ptr(), S.data_ptr())
+                                    val.data_ptr(), M.data_ptr(), S.data_ptr(), None if thr is None else thr.data_ptr())
     assert rc >= 1, _lib.last_error()
     return tok, val, M, S
 
 
 @pytest.mark.parametrize("variant", [0, 2, 3])
 @pytest.mark.parametrize("m,n,k", [(8, 152064, 3584), (64, 152064, 3584), (248, 152064, 3584), (496, 20000, 512),
-                                   (3, 1000, 256), (130, 4099, 512)])
+                                   (3, 1000, 256), (130, 4100, 512)])
 @pytest.mark.parametrize("topk", [8, 4, 2, 1])
-def test_fused_lm_head_topk(monkeypatch, variant, m, n, k, topk):
+@pytest.mark.parametrize("bound", [True, False])
+def test_fused_lm_head_topk(monkeypatch, variant, m, n, k, topk, bound):
     """The LM head's fused top-k epilogue (drafter children, logits never in
     HBM) against the same tcgen05 GEMM's materialised fp32 logits (whole-K
     accumulators, one split): ids by (logit desc, id asc) and values exact,
-    M exact, S within fp32 tolerance."""
+    M exact, S within fp32 tolerance. bound: with the per-row running
+    k-th-value bound (tiles below it stop early), reused across two calls
+    on different inputs (the merge must leave it cleared)."""
     monkeypatch.setenv("TLT_GEMM_FORCE_VARIANT", str(variant))
     g = torch.Generator(device="cuda").manual_seed(m + n + topk)
     x = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
@@ -84,7 +87,12 @@ def test_fused_lm_head_topk(monkeypatch, variant, m, n, k, topk):
     ws = torch.empty(1 << 20, device="cuda")
     assert _lib.lib().tlt_dev_gemm(x.data_ptr(), m, k, w.data_ptr(), n, 0, logits.data_ptr(), None, ws.data_ptr(),
                                    ws.numel(), 1) >= 1, _lib.last_error()
-    tok, val, M, S = lm_topk(x, w, topk)
+    thr = torch.zeros(m, dtype=torch.int32, device="cuda") if bound else None
+    if bound:  # a first call on other inputs leaves bounds that must not leak
+        lm_topk(torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16) * 4, w, topk, thr)
+        torch.cuda.synchronize()
+        assert int(thr.abs().sum()) == 0
+    tok, val, M, S = lm_topk(x, w, topk, thr)
     torch.cuda.synchronize()
     want = ref_topk(logits, topk)
     assert torch.equal(tok.long(), want), (tok[:2], want[:2])

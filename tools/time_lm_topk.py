@@ -23,10 +23,15 @@ for m in [8, 64, 128, 248, 496]:
     S = torch.empty(m, device="cuda")
     logits = torch.empty(m, V, device="cuda")
     ms = C.c_float()
+    thr = torch.zeros(m, dtype=torch.int32, device="cuda")
 
     def fused():
         assert L.tlt_dev_lm_topk(x.data_ptr(), m, D, w.data_ptr(), V, K, part.data_ptr(), tok.data_ptr(),
-                                 val.data_ptr(), M.data_ptr(), S.data_ptr()) >= 1
+                                 val.data_ptr(), M.data_ptr(), S.data_ptr(), thr.data_ptr()) >= 1
+
+    def fused_nobound():
+        assert L.tlt_dev_lm_topk(x.data_ptr(), m, D, w.data_ptr(), V, K, part.data_ptr(), tok.data_ptr(),
+                                 val.data_ptr(), M.data_ptr(), S.data_ptr(), None) >= 1
 
     def unfused():
         assert L.tlt_dev_gemm(x.data_ptr(), m, D, w.data_ptr(), V, 0, logits.data_ptr(), None, ws.data_ptr(),
@@ -35,11 +40,12 @@ for m in [8, 64, 128, 248, 496]:
                                   M.data_ptr(), S.data_ptr(), 1, C.byref(ms)) >= 1
 
     res = {}
-    for name, f in [("fused", fused), ("unfused", unfused)]:
+    for name, f in [("fused", fused), ("fused_nobound", fused_nobound), ("unfused", unfused)]:
         for _ in range(3):
             f()
         t0 = time.perf_counter()
         for _ in range(20):
             f()
         res[name] = (time.perf_counter() - t0) / 20 * 1e6
-    print(f"m={m}: fused {res['fused']:.0f} us  unfused {res['unfused']:.0f} us", flush=True)
+    print(f"m={m}: fused {res['fused']:.0f} us  fused w/o bound {res['fused_nobound']:.0f} us  "
+          f"unfused {res['unfused']:.0f} us", flush=True)
