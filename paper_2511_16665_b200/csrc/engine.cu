@@ -348,7 +348,8 @@ GemmPlan Engine::make_plan(int M, int N, int K, int kind, int variant) const {
 // Per-shape plan autotuning (mid M, where the tensor-bound plans differ by up
 // to ~20% between shapes: CTA pairs at 2 CTAs/SM, pairs with a deep 1-CTA/SM
 // ring, the persistent pair kernel, single-CTA tiles, pairs with <= 128-token
-// tiles, the pair split-K plan with 4 splits). The first eager
+// tiles, pairs with up to 512-token tiles as two MMA sub-tiles, the pair
+// split-K plan with 4 splits). The first eager
 // encounter of (M, N, K, epilogue) times every distinct candidate plan on
 // the engine stream (3 launches each, same inputs; a residual-add epilogue is
 // timed as an fp32 store into scratch, every other epilogue is idempotent)
@@ -396,8 +397,8 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
     // experiments (TLT_GEMM_FORCE_VARIANT / tests) but not autotuned: they
     // win on too few shapes (profiles/r2_gemm_variants.txt, r2_gemm_multicast.txt)
     static const bool all_variants = env_int("TLT_GEMM_AUTOTUNE_ALL", 0) != 0;
-    for (int v : {0, 1, 2, 3, 4, 6, 7}) {
-        if (!all_variants && v >= 6) continue;
+    for (int v : {0, 1, 2, 3, 4, 8, 6, 7}) {
+        if (!all_variants && (v == 6 || v == 7)) continue;
         const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, v);
         bool dup = false;
         for (const auto& q : plans) dup = dup || q.same_as(g);

@@ -302,11 +302,18 @@ template <int PAIR, int FP8 = 0>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_swapab(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                   int bn, int stages, int kb_total, int kb_per_split, uint32_t tmem_cols, int wm, int l2pf,
-                  int mc, EpiParams ep) {
+                  int mc, int wn, EpiParams ep) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int b_rows = bn / PAIR;  // token rows staged by this CTA
     const int b_bytes = b_rows * kBlockK * 2;
+    // wn token sub-tiles of bn / wn tokens (one MMA of N = bn / wn each) share
+    // every weight k-block: a token tile of up to 512 tokens reads each
+    // weight tile once (TMEM columns = token offset within the tile). Pair:
+    // each sub-tile is itself split between the two CTAs.
+    const int bn_sub = bn / wn;
+    const int sub_rows = bn_sub / PAIR;
+    const int sub_bytes = sub_rows * kBlockK * 2;
     const int a_bytes = wm * kABytes;  // wm weight sub-tiles of 128 rows share every token tile
     uint8_t* sA = smem;
     uint8_t* sB = smem + stages * a_bytes;
@@ -419,11 +426,17 @@ __global__ void __launch_bounds__(192, 1)
                 const int s = i % stages;
                 const uint32_t ph = (i / stages) & 1;
                 const int kc = (kb0 + i) * kKel;
+                auto load_x = [&] {  // this CTA's rows of every token sub-tile
+                    for (int j = 0; j < wn; ++j) {
+                        if (PAIR == 2)
+                            tma_load_2d_pair(sB + s * b_bytes + j * sub_bytes, &tmX, full_bar0 + 8u * s, kc,
+                                             t0 + j * bn_sub + (int)rank * sub_rows, pol_x);
+                        else
+                            tma_load_2d(sB + s * b_bytes + j * sub_bytes, &tmX, &full[s], kc, t0 + j * bn_sub, pol_x);
+                    }
+                };
                 if (i < npre) {  // weight tile already in flight: activations only
-                    if (PAIR == 2)
-                        tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows, pol_x);
-                    else
-                        tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+                    load_x();
                     continue;
                 }
                 if (w_issuer && i + l2pf < nkb)
@@ -438,43 +451,47 @@ __global__ void __launch_bounds__(192, 1)
                             tma_load_2d_pair(sA + s * a_bytes + a * kABytes, &tmW, full_bar0 + 8u * s, kc,
                                              n0 + a * kBlockM, pol_w);
                     }
-                    tma_load_2d_pair(sB + s * b_bytes, &tmX, full_bar0 + 8u * s, kc, t0 + (int)rank * b_rows, pol_x);
+                    load_x();
                 } else {
                     mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
                     for (int a = 0; a < wm; ++a)
                         tma_load_2d(sA + s * a_bytes + a * kABytes, &tmW, &full[s], kc, n0 + a * kBlockM, pol_w);
-                    tma_load_2d(sB + s * b_bytes, &tmX, &full[s], kc, t0, pol_x);
+                    load_x();
                 }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (single elected thread; pair: leader CTA only)
         if (PAIR == 1 || rank == 0) {
-            const uint32_t idesc = FP8 ? idesc_e4m3_f32(kBlockM * PAIR, bn) : idesc_bf16_f32(kBlockM * PAIR, bn);
+            const uint32_t idesc =
+                FP8 ? idesc_e4m3_f32(kBlockM * PAIR, bn_sub) : idesc_bf16_f32(kBlockM * PAIR, bn_sub);
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % stages;
                 const uint32_t ph = (i / stages) & 1;
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 if (elect_one()) {
-                    const uint64_t db = sdesc_kmajor_sw128(sB + s * b_bytes);
                     for (int a = 0; a < wm; ++a) {
                         const uint64_t da = sdesc_kmajor_sw128(sA + s * a_bytes + a * kABytes);
+                        for (int j = 0; j < wn; ++j) {
+                        const uint64_t db = sdesc_kmajor_sw128(sB + s * b_bytes + j * sub_bytes);
+                        const uint32_t acc = tmem + a * bn + j * bn_sub;
 #pragma unroll
                         for (int kk = 0; kk < kBlockK / 16; ++kk) {
                             // +32 bytes along K inside the 128B swizzle row == +2 in the >>4 address field
                             if (ep.dbg & 1) continue;  // diagnostics: loads only
                             if (FP8) {
                                 if (PAIR == 2)
-                                    tc_mma_e4m3_pair(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                                    tc_mma_e4m3_pair(acc, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
                                 else
-                                    tc_mma_e4m3(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                                    tc_mma_e4m3(acc, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
                             } else if (PAIR == 2) {
-                                tc_mma_bf16_pair(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                                tc_mma_bf16_pair(acc, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
                             } else {
-                                tc_mma_bf16(tmem + a * bn, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+                                tc_mma_bf16(acc, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
                             }
                         }
+                        }  // j
                     }
                     if (PAIR == 2) {
                         tc_commit_pair_mc(&empty[s], mc > 1 ? all_mask : pair_mask);
@@ -953,6 +970,35 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
     const int pair_ctas = 2 * ((n_out + 2 * kBlockM - 1) / (2 * kBlockM)) * ((m_tok + pair_bn_max - 1) / pair_bn_max);
     static const int pair_min_ctas = env_knob("TLT_GEMM_PAIR_MIN_CTAS", 148);
     static const int pair_split = env_knob("TLT_GEMM_PAIR_SPLIT", 1);
+    if (variant == 8 && m_tok > 256) {
+        // CTA pairs with token tiles of up to 512 tokens as two MMA sub-tiles
+        // (N = bn / 2 each, 2 x bn TMEM columns -> 1 CTA per SM): each weight
+        // tile is read once per 512 tokens instead of once per <= 256, which
+        // cuts the L2 -> SM traffic (the limit at mid M: ~6.3 KB/clk chip-wide
+        // L2 throughput) by up to a third; split-K in a (2, 1, splits) cluster
+        // when the weight tiles alone cannot fill the SMs
+        const int n_tt = (m_tok + 511) / 512;
+        const int per = (m_tok + n_tt - 1) / n_tt;
+        const int bn_sub = std::max(32, ((per + 1) / 2 + 15) / 16 * 16);
+        g.pair = 2;
+        g.wm = 1;
+        g.wn = 2;
+        g.bn = 2 * bn_sub;
+        g.box_rows = bn_sub / 2;
+        g.n_ttiles = (m_tok + g.bn - 1) / g.bn;
+        g.n_wtiles = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
+        const int stage_bytes = kABytes + (g.bn / 2) * kBlockK * 2;
+        g.stages = std::max(2, std::min(8, (220 * 1024 - fixed) / stage_bytes));
+        g.smem = g.stages * stage_bytes + fixed;
+        g.tmem_cols = g.bn <= 256 ? 256 : 512;
+        const int pairs = g.n_wtiles * g.n_ttiles;
+        int splits = 1;
+        if (pairs < num_sms() / 2) splits = std::max(1, std::min({(num_sms() / 2) / pairs, g.kb_total / 4, 4}));
+        if (splits > 1 && g.stages * stage_bytes < g.bn * kBlockM * 4) splits = 1;  // partials must fit the ring
+        g.kb_per_split = (g.kb_total + splits - 1) / splits;
+        g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+        return g;
+    }
     if (pair_split && (variant == 0 || variant == 6) && pair_min_m > 0 && m_tok >= pair_min_m &&
         (pair_ctas < pair_min_ctas || variant == 6)) {
         // few weight tiles (N = d): CTA pairs with <= 128-token tiles and
@@ -1118,15 +1164,19 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         CUDA_CHECK(cudaFuncSetAttribute(k_gemm_swapab<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         attr_set = true;
     }
     if (ep.kind == EPI_TOPK && g.splits > 1) throw CudaError("EPI_TOPK needs whole-K accumulators");
     if (g.splits > kMaxSplits) throw CudaError("split-K cluster larger than the portable cluster size");
-    if (g.pair == 2 && ((g.wm != 1 && (g.splits != 1 || g.persist)) || g.bn % 16 || g.bn < 32 || g.bn > 256 || (g.splits > 1 && g.bn > 128) ||
-                        2 * g.splits > kMaxSplits))
+    if (g.pair == 2 && ((g.wm != 1 && (g.splits != 1 || g.persist)) || g.bn % 16 || g.bn < 32 ||
+                        g.bn > 256 * g.wn || (g.splits > 1 && g.bn > 128 && g.wn == 1) || 2 * g.splits > kMaxSplits))
         throw CudaError("invalid CTA-pair GEMM plan");
+    if (g.wn != 1 && (g.wn != 2 || g.persist || g.mc != 1 || g.wm != 1 || (g.bn / g.wn) % 16 ||
+                      g.wm * g.bn > (int)g.tmem_cols || g.fp8))
+        throw CudaError("invalid token sub-tile GEMM plan");
     if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.box_rows * kBlockK * 2) < g.bn * kBlockM * 4))
         throw CudaError("split-K partial does not fit the pipeline smem");
     dim3 grid(g.n_ttiles * g.pair, g.n_wtiles, g.splits);
@@ -1195,7 +1245,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     if (g.mc > 1 && (g.pair != 2 || g.splits != 1 || g.wm != 1 || g.n_ttiles % g.mc || g.mc > 4 || g.fp8))
         throw CudaError("invalid weight-multicast GEMM plan");
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmW, tmX, g.bn, g.stages, g.kb_total, g.kb_per_split,
-                                       g.tmem_cols, g.wm, g.l2pf, g.mc, epd);
+                                       g.tmem_cols, g.wm, g.l2pf, g.mc, g.wn, epd);
     if (e != cudaSuccess) throw CudaError(std::string("gemm launch: ") + cudaGetErrorString(e));
 }
 

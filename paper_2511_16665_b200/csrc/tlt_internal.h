@@ -44,9 +44,11 @@ struct GemmPlan {
     int persist = 0;   // 1: persistent kernel (double-buffered TMEM accumulators)
     int fp8 = 0;       // 1: e4m3 operands (kind::f8f6f4), per-row / per-token scales in the epilogue
     int mc = 1;        // CTA pairs per cluster sharing one weight k-block by TMA multicast (pair plans)
+    int wn = 1;        // token sub-tiles (MMAs of N = bn / wn) sharing each weight k-block (bn up to 512)
     bool same_as(const GemmPlan& o) const {
         return bn == o.bn && n_ttiles == o.n_ttiles && n_wtiles == o.n_wtiles && splits == o.splits &&
-               stages == o.stages && wm == o.wm && pair == o.pair && persist == o.persist && mc == o.mc;
+               stages == o.stages && wm == o.wm && pair == o.pair && persist == o.persist && mc == o.mc &&
+               wn == o.wn;
     }
 };
 

@@ -54,7 +54,7 @@ def test_gemm_swiglu(m):
     assert (y.float() - ref).abs().max().item() < 2e-2 * max(1.0, ref.abs().max().item())
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6, 7])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 6, 7, 8])
 @pytest.mark.parametrize("m,k,n", [(272, 3584, 4608), (528, 3584, 3584), (512, 1024, 2304), (1024, 512, 1536),
                                    (768, 256, 5000), (196, 18944, 512), (300, 4096, 512)])
 def test_gemm_plan_variants(monkeypatch, variant, m, k, n):
@@ -75,7 +75,7 @@ def test_gemm_plan_variants(monkeypatch, variant, m, k, n):
     assert err < 2e-3 * max(1.0, ref.abs().max().item()), (err, rc)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 6, 7])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 6, 7, 8])
 @pytest.mark.parametrize("m,k,n,live", [(1024, 512, 1536, 130), (1024, 512, 1536, 1), (528, 3584, 3584, 300),
                                         (768, 256, 5000, 767), (272, 3584, 4608, 0)])
 def test_gemm_live_rows_skip(monkeypatch, variant, m, k, n, live):

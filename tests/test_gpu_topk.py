@@ -64,7 +64,7 @@ def lm_topk(x, w, k, thr=None):
     return tok, val, M, S
 
 
-@pytest.mark.parametrize("variant", [0, 2, 3])
+@pytest.mark.parametrize("variant", [0, 2, 3, 8])
 @pytest.mark.parametrize("m,n,k", [(8, 152064, 3584), (64, 152064, 3584), (248, 152064, 3584), (496, 20000, 512),
                                    (3, 1000, 256), (130, 4100, 512)])
 @pytest.mark.parametrize("topk", [8, 4, 2, 1])
