@@ -1177,7 +1177,7 @@ void launch_gemm(const GemmPlan& g, const CUtensorMap& tmW, const CUtensorMap& t
     if (g.wn != 1 && (g.wn != 2 || g.persist || g.mc != 1 || g.wm != 1 || (g.bn / g.wn) % 16 ||
                       g.wm * g.bn > (int)g.tmem_cols || g.fp8))
         throw CudaError("invalid token sub-tile GEMM plan");
-    if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.box_rows * kBlockK * 2) < g.bn * kBlockM * 4))
+    if (g.splits > 1 && (g.wm != 1 || g.stages * (kABytes + g.bn / g.pair * kBlockK * 2) < g.bn * kBlockM * 4))
         throw CudaError("split-K partial does not fit the pipeline smem");
     dim3 grid(g.n_ttiles * g.pair, g.n_wtiles, g.splits);
     EpiParams epd = ep;

@@ -415,26 +415,58 @@ __global__ void k_attn_combine(AttnParams p) {
     const int grp = (int)(gw / ((long long)p.KV * nqv));
     const int row = grp * p.rows_per_req + gqv / G;
     const int head = kvh * G + gqv % G;
-    if (p.rows.slot[row] < 0) return;
-    const int nsplit = split_count(p, p.g.lc[grp] + p.g.ntail[grp]);
+    const int slot = p.rows.slot[row], lc = p.g.lc[grp], nt = p.g.ntail[grp];  // loads in flight together
+    if (slot < 0) return;
+    const int nsplit = split_count(p, lc + nt);
     if (nsplit <= 1 && p.direct1) return;  // written by the attention kernel itself
     constexpr int DPL = HD / 32;
+    constexpr int kB = 16;  // splits whose partials are loaded in one round trip
     float M = -CUDART_INF_F;
-    for (int s = 0; s < nsplit; ++s) {
-        const long long pidx = ((long long)(grp * p.max_splits + s) * p.qv_cap + gqv) * p.KV + kvh;
-        M = fmaxf(M, p.ws_m[pidx]);
-    }
     float L = 0.f, o[DPL];
 #pragma unroll
     for (int e = 0; e < DPL; ++e) o[e] = 0.f;
-    for (int s = 0; s < nsplit; ++s) {  // fixed order
-        const long long pidx = ((long long)(grp * p.max_splits + s) * p.qv_cap + gqv) * p.KV + kvh;
-        const float ms = p.ws_m[pidx];
-        if (ms == -CUDART_INF_F) continue;
-        const float w = exp2f(ms - M);
-        L += p.ws_l[pidx] * w;
+    const long long pbase = ((long long)grp * p.max_splits * p.qv_cap + gqv) * p.KV + kvh;
+    const long long pstride = (long long)p.qv_cap * p.KV;
+    if (nsplit <= kB) {
+        // every partial (m, l, o) of the <= 16 splits loaded at once (one
+        // dependent L2 round trip instead of two per split), then the same
+        // arithmetic as the loop below: max over all splits, fixed-order sum
+        float ms[kB], ls[kB], ov[kB][DPL];
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) o[e] += p.ws_o[pidx * HD + lane * DPL + e] * w;
+        for (int s = 0; s < kB; ++s) {
+            ms[s] = -CUDART_INF_F;
+            ls[s] = 0.f;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) ov[s][e] = 0.f;
+            if (s < nsplit) {
+                const long long pidx = pbase + s * pstride;
+                ms[s] = p.ws_m[pidx];
+                ls[s] = p.ws_l[pidx];
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) ov[s][e] = p.ws_o[pidx * HD + lane * DPL + e];
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < kB; ++s) M = fmaxf(M, ms[s]);
+#pragma unroll
+        for (int s = 0; s < kB; ++s) {  // fixed order
+            if (s >= nsplit || ms[s] == -CUDART_INF_F) continue;
+            const float w = exp2f(ms[s] - M);
+            L += ls[s] * w;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) o[e] += ov[s][e] * w;
+        }
+    } else {
+        for (int s = 0; s < nsplit; ++s) M = fmaxf(M, p.ws_m[pbase + s * pstride]);
+        for (int s = 0; s < nsplit; ++s) {  // fixed order
+            const long long pidx = pbase + s * pstride;
+            const float ms = p.ws_m[pidx];
+            if (ms == -CUDART_INF_F) continue;
+            const float w = exp2f(ms - M);
+            L += p.ws_l[pidx] * w;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) o[e] += p.ws_o[pidx * HD + lane * DPL + e] * w;
+        }
     }
     const float inv = L > 0.f ? 1.0f / L : 0.f;
 #pragma unroll
