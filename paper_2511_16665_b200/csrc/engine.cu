@@ -348,8 +348,8 @@ GemmPlan Engine::make_plan(int M, int N, int K, int kind, int variant) const {
 // Per-shape plan autotuning (mid M, where the tensor-bound plans differ by up
 // to ~20% between shapes: CTA pairs at 2 CTAs/SM, pairs with a deep 1-CTA/SM
 // ring, the persistent pair kernel, single-CTA tiles, pairs with <= 128-token
-// tiles, pairs with up to 512-token tiles as two MMA sub-tiles, the pair
-// split-K plan with 4 splits). The first eager
+// tiles; opt-in: pairs with up to 512-token tiles as two MMA sub-tiles, the
+// pair split-K plan with 4 splits, weight multicast). The first eager
 // encounter of (M, N, K, epilogue) times every distinct candidate plan on
 // the engine stream (3 launches each, same inputs; a residual-add epilogue is
 // timed as an fp32 store into scratch, every other epilogue is idempotent)
@@ -393,12 +393,15 @@ int Engine::tuned_variant(const bf16* X, int M, int K, long long ldx, const CUte
     }
     std::vector<GemmPlan> plans;
     std::vector<int> vars;
-    // variants 6 (pair split-K x4) and 7 (weight multicast) are kept for
-    // experiments (TLT_GEMM_FORCE_VARIANT / tests) but not autotuned: they
-    // win on too few shapes (profiles/r2_gemm_variants.txt, r2_gemm_multicast.txt)
+    // variants 6 (pair split-K x4), 7 (weight multicast) and 8 (512-token
+    // tiles as two MMA sub-tiles) are kept for experiments
+    // (TLT_GEMM_FORCE_VARIANT / tests) but not autotuned: they win on too few
+    // shapes in isolation (profiles/r2_gemm_variants.txt, r2_gemm_multicast.txt,
+    // r2_gemm_variant8.txt) and 8 (1 CTA/SM, all 512 TMEM columns) lost
+    // ~2% of rollout throughput where the tuner took it (down-proj, M = 288)
     static const bool all_variants = env_int("TLT_GEMM_AUTOTUNE_ALL", 0) != 0;
     for (int v : {0, 1, 2, 3, 4, 8, 6, 7}) {
-        if (!all_variants && (v == 6 || v == 7)) continue;
+        if (!all_variants && (v == 6 || v == 7 || v == 8)) continue;
         const GemmPlan g = make_plan(M, N, K, (int)ep_in.kind, v);
         bool dup = false;
         for (const auto& q : plans) dup = dup || q.same_as(g);
