@@ -76,7 +76,7 @@ __host__ __device__ constexpr uint32_t idesc_tc(uint32_t M, uint32_t N, uint32_t
 }  // namespace
 
 __global__ void __launch_bounds__(256, 1) k_attention_tc(AttnParams p, int dbg_stage) {
-    pdl_wait();
+    pdl_wait_only();  // dependents are released after the TMEM allocation (pdl.cuh)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // layout: Q 2 x 16 KB | K (later P) 64 KB | V 64 KB | masks | barriers
@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(256, 1) k_attention_tc(AttnParams p, int dbg_s
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_launch_dependents();
     const uint32_t tmem = *tmem_holder;
     const uint32_t tS = tmem, tO = tmem + 256;
     if (dbg_stage == 1) { tc_fence_before(); __syncthreads(); if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory"); return; }

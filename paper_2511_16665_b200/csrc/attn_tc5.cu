@@ -89,7 +89,7 @@ __device__ __forceinline__ void cp_async16_5(uint32_t saddr, const void* gmem, b
 
 __global__ void __launch_bounds__(192, 1)
     k_attention_tree_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p) {
-    pdl_wait();
+    pdl_wait_only();  // dependents are released after the TMEM allocation below
     extern __shared__ __align__(1024) uint8_t smem5[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem5) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = sm;                                   // [2 halves][128 rows][128 B]      32 KB
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(192, 1)
     const int total = slot >= 0 ? lc + ntail : 0;
     const int chunk = split_chunk(p, total);
     const int k0 = split * chunk;
-    if (k0 >= total) return;
+    if (k0 >= total) return;  // exited CTAs count as having released the dependents
     const int k1 = min(total, k0 + chunk);
     const bool single = p.max_splits == 1 || (p.direct1 && split_count(p, total) == 1);
     const int pe = min(k1, lc);
@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_launch_dependents();  // this CTA holds its TMEM: dependents may start allocating theirs
     const uint32_t tmem = tmem_holder;
     const uint32_t tS[2] = {tmem, tmem + 64}, tO = tmem + 128;
     const uint32_t aQ = smem_u32(sQ), aRing = smem_u32(ring), aP = smem_u32(sP);

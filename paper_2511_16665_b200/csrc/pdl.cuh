@@ -20,6 +20,17 @@ __device__ __forceinline__ void pdl_wait() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// Kernels that allocate TMEM signal their dependents only AFTER every CTA
+// holds its allocation: a PDL-launched dependent (the next GEMM) allocates
+// TMEM before its own griddepcontrol.wait, so if it could start while a CTA
+// of this grid had not yet allocated, that CTA's tcgen05.alloc could block on
+// the dependent's columns while the dependent waits for this grid — a
+// deadlock. (Dependents launch only once every CTA of this grid has issued
+// launch_dependents or exited.)
+__device__ __forceinline__ void pdl_wait_only() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // TLT_PDL: "gemm" = tcgen05 GEMM launches only (default), 1 = every engine
 // kernel, 0 = plain stream serialization, "other" = all but the GEMMs.
