@@ -341,6 +341,7 @@ GemmPlan Engine::make_plan(int M, int N, int K, int kind, int variant) const {
         // scatter) after the in-cluster reduction prefers <= 4 splits
         g.kb_per_split = (g.kb_total + qkv_max_splits - 1) / qkv_max_splits;
         g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+        gemm_one_wave(g);
     }
     return g;
 }

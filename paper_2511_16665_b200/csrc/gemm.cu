@@ -936,6 +936,28 @@ int gemm_dbg_flags() {
     return f;
 }
 
+// Weight-streaming plans (single-CTA tiles, split-K over few weight tiles):
+// TLT_GEMM_ONE_WAVE=1 caps the split count so every CTA gets its own SM
+// (tiles x splits <= #SMs; the 2-per-SM packing otherwise leaves half the
+// SMs with twice the bytes to stream) and gives each CTA the whole smem ring
+// (up to 12 stages, ~200 KB of weight tiles in flight per SM).
+void gemm_one_wave(GemmPlan& g) {
+    static const int on = env_knob("TLT_GEMM_ONE_WAVE", 0);
+    if (!on || g.pair != 1 || g.persist || g.wm != 1 || g.fp8 || g.mc != 1) return;
+    const int tiles = g.n_wtiles * g.n_ttiles;
+    if (tiles > num_sms()) return;
+    int splits = g.splits;
+    if (tiles * splits > num_sms()) {
+        splits = std::max(1, num_sms() / tiles);
+        g.kb_per_split = (g.kb_total + splits - 1) / splits;
+        g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+    }
+    const int fixed = 1024 + 256;
+    const int stage_bytes = kABytes + g.box_rows * kBlockK * 2;
+    g.stages = std::max(2, std::min(12, (220 * 1024 - fixed) / stage_bytes));
+    g.smem = g.stages * stage_bytes + fixed;
+}
+
 GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
     GemmPlan g;
     static const int l2pf = env_knob("TLT_GEMM_L2PF", 0);
@@ -1123,6 +1145,7 @@ GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant) {
     if (g.wm != 1 || g.stages * stage_bytes < bn * kBlockM * 4) splits = 1;
     g.kb_per_split = (g.kb_total + splits - 1) / splits;
     g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+    gemm_one_wave(g);
     if (g.splits == 1 && persist >= 2 && g.wm == 1 && m_tok >= persist1_min_m) {
         const int pfixed = 1024 + 32 * 8 + 16 + 16 * 128 * 4;
         g.persist = 1;

@@ -55,6 +55,7 @@ struct GemmPlan {
 int num_sms();
 CUtensorMap make_tmap_bf16(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
 GemmPlan plan_gemm(int m_tok, int n_out, int k, int variant = 0);
+void gemm_one_wave(GemmPlan& g);  // TLT_GEMM_ONE_WAVE: <= 1 CTA per SM with the full smem ring
 GemmPlan plan_gemm_e4m3(int m_tok, int n_out, int k);
 CUtensorMap make_tmap_e4m3(const void* base, int rows, int cols, long long row_stride_elems, int box_rows);
 int* gemm_norm_counter();
