@@ -340,7 +340,8 @@ def traffic_table():
 
 def kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind):
     """Each probe: the engine's own GEMM site, successive layers' weights,
-    CUDA events on the engine stream (tlt_probe_kernel)."""
+    CUDA events on the engine stream (tlt_probe_kernel; best of 5 timed
+    passes of 56 launches after a warm-up pass)."""
     traffic = traffic_table()
     out = []
     for name, kind, m, bound in PROBES:

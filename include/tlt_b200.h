@@ -455,15 +455,17 @@ TLT_API int tlt_debug_ar_logits(tlt_engine* e, float* logits, int b);
 /* Live timing of one of the engine's own GEMM sites on its stream with its
  * own weights (successive layers, so every launch streams fresh weights):
  * kind 0 gate_up+SwiGLU, 1 qkv (+RoPE, KV write), 2 down (+residual),
- * 3 LM head fp32 logits, 4 LM head + fused top-1. Reports the average launch
- * duration and the algorithmic bytes / flops of one launch. */
+ * 3 LM head fp32 logits, 4 LM head + fused top-1, 5 o-proj (+residual),
+ * 6 drafter LM head. Reports the average launch duration (best of 5 timed
+ * passes of `iters` launches) and the algorithmic bytes / flops of one launch. */
 TLT_API int tlt_probe_kernel(tlt_engine* e, int kind, int m_tok, int iters, float* avg_ms, double* bytes,
                              double* flops);
 
 /* Live timing of the engine's attention (flash-decode + split combine) on
  * its stream over successive layers' caches: b requests x ctx committed keys
  * x rows_per_req query rows (1 = plain decode, T+1 = tree verify). Reports
- * the average per-layer duration and the algorithmic bytes (K/V read + q/out). */
+ * the average per-layer duration (graph replay, best of 5) and the
+ * algorithmic bytes (K/V read + q/out). */
 TLT_API int tlt_probe_attention(tlt_engine* e, int b, int ctx, int rows_per_req, int iters, float* avg_ms,
                                 double* bytes);
 
