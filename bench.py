@@ -209,7 +209,7 @@ def cpu_rollout_sample(model_name, n_threads, gen_tokens, prompt_len, strategy, 
     cfg = O.ModelCfg(m["vocab"], m["hidden"], m["layers"], m["heads"], m["kv_heads"], m["head_dim"], m["ffn"],
                      m["qkv_bias"], m["rope_theta"], m["rms_eps"], prompt_len + gen_tokens + 64)
     icfg = O.InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"],
-                     ini["fc_noise"])
+                     ini["fc_noise"], int(ini.get("drafter_lm_fp8", 0)))
     t0 = time.time()
     om = L.orc_model_create(C.byref(cfg), C.byref(icfg), n_threads)
     init_s = time.time() - t0
@@ -243,7 +243,7 @@ def cpu_rows(model_name, prompt_len, strategy):
     cfg = O.ModelCfg(m["vocab"], m["hidden"], m["layers"], m["heads"], m["kv_heads"], m["head_dim"], m["ffn"],
                      m["qkv_bias"], m["rope_theta"], m["rms_eps"], prompt_len + 64)
     icfg = O.InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"],
-                     ini["fc_noise"])
+                     ini["fc_noise"], int(ini.get("drafter_lm_fp8", 0)))
     cores = os.cpu_count() or 1
     om = L.orc_model_create(C.byref(cfg), C.byref(icfg), cores)
     L.orc_neural_spec_generate.argtypes = [C.c_void_p] * 11

@@ -37,6 +37,8 @@ struct orc_model {
     orc_model_cfg c;
     tlt_init_params ip;
     uint16_t *embed, *lm_head, *final_norm, *fc;
+    uint16_t* lm8;   /* drafter_lm_fp8: unscaled e4m3 values of lm_head rows (exact in bf16) */
+    float* lm8_s;    /* [vocab] row scales */
     orc_layer* layers;
     orc_layer drafter;
     float *rope_cos, *rope_sin; /* [max_ctx][hd/2] */
@@ -105,6 +107,49 @@ static int init_layer(orc_model* m, orc_layer* L, int layer) {
     return (L->attn_norm && L->qkv && L->o && L->mlp_norm && L->gu && L->down) ? 0 : -1;
 }
 
+/* e4m3 (fn: bias 7, max 448, subnormal quantum 2^-9), round to nearest even,
+ * saturating to +-448 -- __nv_cvt_float_to_fp8(x, __NV_SATFINITE, __NV_E4M3). */
+static float e4m3_rne(float x) {
+    const float a = fabsf(x);
+    float q;
+    if (!(a < 448.f)) {
+        q = 448.f;
+    } else if (a < 0.015625f) { /* below 2^-6: subnormals */
+        q = nearbyintf(a * 512.f) / 512.f;
+    } else {
+        int e;
+        frexpf(a, &e); /* a in [2^(e-1), 2^e) */
+        const float quantum = ldexpf(1.f, e - 4);
+        q = nearbyintf(a / quantum) * quantum;
+    }
+    return copysignf(q, x);
+}
+
+float orc_e4m3_quant_row(const float* x, int n, float* q) {
+    float amax = 0.f;
+    for (int i = 0; i < n; ++i) amax = fmaxf(amax, fabsf(x[i]));
+    const float s = amax > 0.f ? amax / 448.0f : 1.0f; /* IEEE division, as the GPU's __fdiv_rn */
+    for (int i = 0; i < n; ++i) q[i] = e4m3_rne(x[i] / s);
+    return s;
+}
+
+typedef struct {
+    orc_model* m;
+    int64_t lo, hi;
+} q8_job;
+static void* q8_worker(void* a) {
+    q8_job* j = (q8_job*)a;
+    const int d = j->m->c.hidden;
+    float* row = (float*)malloc(sizeof(float) * 2 * (size_t)d);
+    for (int64_t v = j->lo; v < j->hi; ++v) {
+        for (int i = 0; i < d; ++i) row[i] = bf(j->m->lm_head[v * d + i]);
+        j->m->lm8_s[v] = orc_e4m3_quant_row(row, d, row + d);
+        for (int i = 0; i < d; ++i) j->m->lm8[v * d + i] = tlt_f32_to_bf16_bits(row[d + i]); /* exact */
+    }
+    free(row);
+    return NULL;
+}
+
 orc_model* orc_model_create(const orc_model_cfg* cfg, const orc_init_cfg* init, int n_threads) {
     orc_model* m = (orc_model*)calloc(1, sizeof(orc_model));
     if (!m) return NULL;
@@ -121,6 +166,23 @@ orc_model* orc_model_create(const orc_model_cfg* cfg, const orc_init_cfg* init, 
     int ok = m->embed && m->lm_head && m->final_norm && m->fc && m->layers;
     for (int l = 0; ok && l < cfg->layers; ++l) ok = init_layer(m, &m->layers[l], l) == 0;
     if (ok) ok = init_layer(m, &m->drafter, TLT_DRAFTER_LAYER) == 0;
+    if (ok && init->drafter_lm_fp8) {
+        m->lm8 = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(V * d));
+        m->lm8_s = (float*)malloc(sizeof(float) * (size_t)V);
+        ok = m->lm8 && m->lm8_s;
+        int nt = m->n_threads;
+        pthread_t th[256];
+        q8_job jobs[256];
+        for (int i = 0; ok && i < nt; ++i) {
+            jobs[i] = (q8_job){m, V * i / nt, V * (i + 1) / nt};
+            if (nt > 1)
+                pthread_create(&th[i], NULL, q8_worker, &jobs[i]);
+            else
+                q8_worker(&jobs[i]);
+        }
+        if (ok && nt > 1)
+            for (int i = 0; i < nt; ++i) pthread_join(th[i], NULL);
+    }
     /* RoPE table: angle = pos * theta^(-2i/hd) in double, stored fp32 */
     int half = cfg->head_dim / 2;
     m->rope_cos = (float*)malloc(sizeof(float) * (size_t)cfg->max_ctx * (size_t)half);
@@ -157,6 +219,8 @@ void orc_model_destroy(orc_model* m) {
     if (!m) return;
     free(m->embed);
     free(m->lm_head);
+    free(m->lm8);
+    free(m->lm8_s);
     free(m->final_norm);
     free(m->fc);
     if (m->layers)
@@ -391,12 +455,22 @@ static void layer_rows(orc_seq* s, const orc_layer* L, uint16_t* kc, uint16_t* v
     mm(m, s->act, n, F, L->down, d, x, 1);
 }
 
-static void lm_logits(orc_seq* s, const float* x_row, float* logits) {
+/* drafter && lm8: the e4m3 drafter LM head (engine drafter_logits with
+ * drafter_fp8_): the normed row and the weight rows quantised per row, fp32
+ * dot products of the e4m3 values, then x (row scale x token scale) as the
+ * GEMM epilogue applies it (gemm.cuh epi_vec8, row_scale / tok_scale). */
+static void lm_logits(orc_seq* s, const float* x_row, float* logits, int drafter) {
     orc_model* m = s->m;
     const int d = m->c.hidden;
-    float* h = (float*)malloc(sizeof(float) * (size_t)d);
+    float* h = (float*)malloc(sizeof(float) * 2 * (size_t)d);
     rmsnorm(x_row, m->final_norm, d, m->c.rms_eps, h);
-    mm(m, h, 1, d, m->lm_head, m->c.vocab, logits, 0);
+    if (drafter && m->lm8) {
+        const float sh = orc_e4m3_quant_row(h, d, h + d);
+        mm(m, h + d, 1, d, m->lm8, m->c.vocab, logits, 0);
+        for (int v = 0; v < m->c.vocab; ++v) logits[v] *= m->lm8_s[v] * sh;
+    } else {
+        mm(m, h, 1, d, m->lm_head, m->c.vocab, logits, 0);
+    }
     free(h);
 }
 
@@ -413,7 +487,7 @@ static int target_rows(orc_seq* s, const int32_t* toks, int n, int base, uint16_
     if (feat_out)
         for (int t = 0; t < n; ++t)
             for (int i = 0; i < d; ++i) feat_out[(size_t)t * d + i] = tlt_f32_to_bf16_bits(x[(size_t)t * d + i]);
-    if (logits) lm_logits(s, x + (size_t)(n - 1) * d, logits);
+    if (logits) lm_logits(s, x + (size_t)(n - 1) * d, logits, 0);
     return 0;
 }
 
@@ -439,7 +513,7 @@ static int drafter_rows(orc_seq* s, const uint16_t* prev_feat, const int32_t* to
     if (out_feat)
         for (int t = 0; t < n; ++t)
             for (int i = 0; i < d; ++i) out_feat[(size_t)t * d + i] = tlt_f32_to_bf16_bits(x[(size_t)t * d + i]);
-    if (logits) lm_logits(s, x + (size_t)(n - 1) * d, logits);
+    if (logits) lm_logits(s, x + (size_t)(n - 1) * d, logits, 1);
     return 0;
 }
 

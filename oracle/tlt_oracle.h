@@ -174,6 +174,11 @@ typedef struct {
 typedef struct {
     uint64_t seed;
     float layer_scale, lm_gain, lm_alt, lm_noise, fc_noise;
+    /* 1: the drafter's LM head in e4m3 as the engine runs it (tlt_init_cfg.
+     * drafter_lm_fp8): per-row scale amax/448, RNE saturating e4m3 of the
+     * weight rows and of the normed drafter row, fp32 dot product, logits x
+     * (row scale x token scale). The target's LM head stays bf16. */
+    int32_t drafter_lm_fp8;
 } orc_init_cfg;
 
 typedef struct orc_model orc_model;
@@ -184,6 +189,10 @@ void orc_model_destroy(orc_model* m);
 int orc_model_weight(orc_model* m, int tensor_id, int layer, const uint16_t** ptr, int64_t* n);
 /* The counter-hash init value of element idx of tensor (tensor_id, layer). */
 uint16_t orc_init_value(const orc_init_cfg* init, const orc_model_cfg* cfg, int tensor_id, int layer, int64_t idx);
+/* e4m3 quantisation of one row as the engine's k_quant_rows_e4m3: scale =
+ * amax / 448 (1 for an all-zero row), q[i] = the e4m3 value (RNE,
+ * saturating) of x[i] / scale, returned as a float. Returns the scale. */
+float orc_e4m3_quant_row(const float* x, int n, float* q);
 
 /* Per-request decoding state: target KV (all layers), drafter KV, feature
  * history. */

@@ -144,7 +144,10 @@ MODELS = {
 # Structure knob per model: mean accept length in a realistic band.
 INITS = {
     "tiny": dict(seed=42, layer_scale=1.0, lm_gain=10.0, lm_alt=0.9, lm_noise=1.0, fc_noise=0.05),
-    "qwen2.5-7b": dict(seed=42, layer_scale=1.0, lm_gain=13.0, lm_alt=0.9, lm_noise=1.0, fc_noise=0.05),
+    # 7B: the drafter's LM head in e4m3 (half its weight stream per draft level;
+    # profiles/r2_drafter_fp8_ab.txt), emulated by the oracle (orc_neural.c lm_logits)
+    "qwen2.5-7b": dict(seed=42, layer_scale=1.0, lm_gain=13.0, lm_alt=0.9, lm_noise=1.0, fc_noise=0.05,
+                       drafter_lm_fp8=1),
     "qwen2.5-32b": dict(seed=42, layer_scale=0.3, lm_gain=13.0, lm_alt=0.9, lm_noise=1.0, fc_noise=0.05),
 }
 

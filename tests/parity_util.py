@@ -83,7 +83,8 @@ def tiny_oracle_model():
     L = O.orc()
     cfg = O.ModelCfg(T["vocab"], T["hidden"], T["layers"], T["heads"], T["kv_heads"], T["head_dim"], T["ffn"],
                      T["qkv_bias"], T["rope_theta"], T["rms_eps"], 1024)
-    ini = O.InitCfg(I["seed"], I["layer_scale"], I["lm_gain"], I["lm_alt"], I["lm_noise"], I["fc_noise"])
+    ini = O.InitCfg(I["seed"], I["layer_scale"], I["lm_gain"], I["lm_alt"], I["lm_noise"], I["fc_noise"],
+                    int(I.get("drafter_lm_fp8", 0)))
     return L.orc_model_create(C.byref(cfg), C.byref(ini), 8)
 
 

@@ -37,7 +37,8 @@ def o7b():
     L = O.orc()
     cfg = O.ModelCfg(V, M7["hidden"], M7["layers"], M7["heads"], M7["kv_heads"], M7["head_dim"], M7["ffn"],
                      M7["qkv_bias"], M7["rope_theta"], M7["rms_eps"], 128)
-    ini = O.InitCfg(I7["seed"], I7["layer_scale"], I7["lm_gain"], I7["lm_alt"], I7["lm_noise"], I7["fc_noise"])
+    ini = O.InitCfg(I7["seed"], I7["layer_scale"], I7["lm_gain"], I7["lm_alt"], I7["lm_noise"], I7["fc_noise"],
+                    int(I7.get("drafter_lm_fp8", 0)))
     m = L.orc_model_create(C.byref(cfg), C.byref(ini), os.cpu_count() or 8)
     assert m
     yield m

@@ -41,7 +41,8 @@ def omodel():
     L = O.orc()
     cfg = O.ModelCfg(TINY["vocab"], TINY["hidden"], TINY["layers"], TINY["heads"], TINY["kv_heads"],
                      TINY["head_dim"], TINY["ffn"], TINY["qkv_bias"], TINY["rope_theta"], TINY["rms_eps"], 1024)
-    ini = O.InitCfg(INIT["seed"], INIT["layer_scale"], INIT["lm_gain"], INIT["lm_alt"], INIT["lm_noise"], INIT["fc_noise"])
+    ini = O.InitCfg(INIT["seed"], INIT["layer_scale"], INIT["lm_gain"], INIT["lm_alt"], INIT["lm_noise"], INIT["fc_noise"],
+                    int(INIT.get("drafter_lm_fp8", 0)))
     m = L.orc_model_create(C.byref(cfg), C.byref(ini), 8)
     assert m
     yield m
@@ -221,3 +222,46 @@ def test_rollout_tokens_match_oracle(omodel, use_graphs):
     assert res["sd_steps"] > 0 and res["plain_steps"] == 0
     assert ar["plain_steps"] > 0 and ar["sd_steps"] == 0
     eng.close()
+
+
+def test_fp8_drafter_lm_head_rows_and_tree_match_oracle():
+    """drafter_lm_fp8 (the 7B default): the engine's e4m3 drafter LM head
+    (per-row scales, kind::f8f6f4 GEMM) against the oracle's emulation of the
+    same quantisation -- drafter rows within the log-prob tolerance, the tree
+    bit-exact with the oracle-in-the-loop, and SD still lossless vs AR."""
+    L = O.orc()
+    ini8 = dict(INIT, drafter_lm_fp8=1)
+    cfg = O.ModelCfg(TINY["vocab"], TINY["hidden"], TINY["layers"], TINY["heads"], TINY["kv_heads"],
+                     TINY["head_dim"], TINY["ffn"], TINY["qkv_bias"], TINY["rope_theta"], TINY["rms_eps"], 1024)
+    icfg = O.InitCfg(ini8["seed"], ini8["layer_scale"], ini8["lm_gain"], ini8["lm_alt"], ini8["lm_noise"],
+                     ini8["fc_noise"], 1)
+    m8 = L.orc_model_create(C.byref(cfg), C.byref(icfg), 8)
+    assert m8
+    eng = Engine("tiny", max_slots=4, max_ctx=512, init={"drafter_lm_fp8": 1})
+    eng.set_debug(True)
+    prompts = _prompts(seed=11)
+    eng.prefill(range(4), prompts)
+    r = eng.sd_step(STRAT, list(range(4)))
+    for i in range(4):
+        exps = eng.debug_expansions(i)
+        for path, row in exps[:6]:
+            ref = _odrafter_row(m8, prompts[i], path)
+            msk = ref > 1e-6
+            err = np.abs(np.log(row[msk]) - np.log(ref[msk]))
+            assert err.max() < 2 * (LOGIT_ATOL + LOGIT_RTOL * 10), (i, path, err.max())
+        table = dict(exps)
+
+        def cb(user, path, n, out, table=table):
+            row = table.get(tuple(path[j] for j in range(n)))
+            if row is None:
+                return -1
+            C.memmove(out, row.ctypes.data, TINY["vocab"] * 8)
+            return 0
+
+        fn = O.ROW_FN(cb)
+        out = (O.Node * STRAT[2])()
+        L.orc_build_draft_tree.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        n = L.orc_build_draft_tree(C.cast(fn, C.c_void_p), None, TINY["vocab"], C.byref(O.Strategy(*STRAT)), out)
+        assert [(out[j].token, out[j].parent, out[j].depth, out[j].prob, out[j].path_prob) for j in range(n)] == r.tree[i]
+    eng.close()
+    L.orc_model_destroy(m8)

@@ -33,7 +33,7 @@ def omodel():
     cfg = O.ModelCfg(TINY["vocab"], TINY["hidden"], TINY["layers"], TINY["heads"], TINY["kv_heads"],
                      TINY["head_dim"], TINY["ffn"], TINY["qkv_bias"], TINY["rope_theta"], TINY["rms_eps"], 1024)
     ini = O.InitCfg(INIT["seed"], INIT["layer_scale"], INIT["lm_gain"], INIT["lm_alt"], INIT["lm_noise"],
-                    INIT["fc_noise"])
+                    INIT["fc_noise"], int(INIT.get("drafter_lm_fp8", 0)))
     m = L.orc_model_create(C.byref(cfg), C.byref(ini), 8)
     assert m
     yield m

@@ -129,7 +129,8 @@ def test_reference_adapter_runs_spec_generate_on_gpu(strategy):
     L = O.orc()
     cfg = O.ModelCfg(tiny["vocab"], tiny["hidden"], tiny["layers"], tiny["heads"], tiny["kv_heads"],
                      tiny["head_dim"], tiny["ffn"], tiny["qkv_bias"], tiny["rope_theta"], tiny["rms_eps"], 512)
-    icfg = O.InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"], ini["fc_noise"])
+    icfg = O.InitCfg(ini["seed"], ini["layer_scale"], ini["lm_gain"], ini["lm_alt"], ini["lm_noise"], ini["fc_noise"],
+                    int(ini.get("drafter_lm_fp8", 0)))
     m = L.orc_model_create(C.byref(cfg), C.byref(icfg), 4)
     L.orc_neural_spec_generate.argtypes = [C.c_void_p] * 11
     pa = (C.c_int32 * len(prompt))(*prompt)
