@@ -4,7 +4,7 @@ import sys
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2511_16665_b200.engine import Engine  # noqa: E402
 
-eng = Engine("qwen2.5-7b", max_slots=8, max_ctx=512)
+eng = Engine("qwen2.5-7b", max_slots=32, max_ctx=512)
 for spec in sys.argv[1:]:
     kind, m = (int(x) for x in spec.split(":"))
     ms, b, f = eng.probe_kernel(kind, m, 56)
