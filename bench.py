@@ -330,12 +330,17 @@ ATTN_PROBES = [  # (name, requests, committed keys, query rows per request)
 
 
 def traffic_table():
-    """dram bytes per launch from the committed ncu --set full captures."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            return json.load(f)
-    except Exception:
-        return {}
+    """dram bytes per launch from the committed ncu captures: round 1's --set
+    full GEMM captures, overridden by round 2's per-site engine probes
+    (tools/traffic_json.py over tools/gpu_r2_s3_final.sh)."""
+    out = {}
+    for name in ("r1_traffic.json", "r2_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                out.update({k: v for k, v in json.load(f).items() if not k.startswith("_")})
+        except Exception:
+            pass
+    return out
 
 
 def kernel_rooflines(eng, peak_gbs, peak_tf, peak_kind):
@@ -438,22 +443,30 @@ def gemm_class(eng, M, bound, peak_gbs, peak_tf):
     L = eng.model["layers"]
     t = byts = fl = 0.0
     parts = []
+    tt = traffic_table()
+    traffic = 0.0
     for kind, name in GEMM_SITES:
         ms, b_, f_ = eng.probe_kernel(kind, M, 56)
         t, byts, fl = t + ms * L, byts + b_ * L, fl + f_ * L
-        parts.append({"site": name, "avg_launch_us": round(ms * 1e3, 2), "bytes": int(b_), "flops": int(f_)})
+        tr = tt.get(f"{kind}:{M}")
+        traffic = traffic + tr * L if (tr is not None and traffic is not None) else None
+        parts.append({"site": name, "avg_launch_us": round(ms * 1e3, 2), "bytes": int(b_), "flops": int(f_),
+                      "traffic": tr})
     ms, b_, f_ = eng.probe_kernel(4, M, 8)
     t, byts, fl = t + ms, byts + b_, fl + f_
+    tr = tt.get(f"4:{M}")
+    traffic = traffic + tr if (tr is not None and traffic is not None) else None
     parts.append({"site": "LM head (+fused top-1)", "avg_launch_us": round(ms * 1e3, 2), "bytes": int(b_),
-                  "flops": int(f_)})
+                  "flops": int(f_), "traffic": tr})
+    traffic = int(traffic) if traffic is not None else None  # ncu DRAM bytes of one forward's GEMMs
     if bound == "hbm":
         ach = byts / (t * 1e-3) / 1e9
         return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
-                "frac": round(ach / peak_gbs, 3), "traffic": None, "M": M, "forward_gemm_ms": round(t, 3),
+                "frac": round(ach / peak_gbs, 3), "traffic": traffic, "M": M, "forward_gemm_ms": round(t, 3),
                 "algorithmic_bytes": int(byts), "sites": parts}
     ach = fl / (t * 1e-3) / 1e12
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": round(ach / peak_tf, 3), "traffic": None, "M": M, "forward_gemm_ms": round(t, 3),
+            "frac": round(ach / peak_tf, 3), "traffic": traffic, "M": M, "forward_gemm_ms": round(t, 3),
             "flops": int(fl), "sites": parts}
 
 
