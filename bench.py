@@ -54,28 +54,32 @@ def peaks():
         return 6650.0, 1590.0, 1373.0, "fallback"
 
 
-def model_costs(m):
+def model_costs(m, drafter_fp8=False):
     """Algorithmic bytes / flops of the Qwen-shaped target and the EAGLE drafter
     (SURVEY.md 8(d)): weights streamed per forward (the embedding is a row
-    gather), KV bytes per token, matmul flops per row."""
+    gather), KV bytes per token, matmul flops per row. drafter_fp8: the
+    drafter's LM head streams one byte per weight (+ a scale per row) and its
+    flops run at twice the bf16 rate (counted as half as many bf16 flops)."""
     d, L, H, KV, hd, F, V = (m[k] for k in ("hidden", "layers", "heads", "kv_heads", "head_dim", "ffn", "vocab"))
     nqkv = (H + 2 * KV) * hd
     mat_layer = d * nqkv + H * hd * d + 2 * d * F + F * d
     layer_b = (mat_layer + nqkv + 2 * d) * 2
+    lm_d = V * d + V * 4 if drafter_fp8 else V * d * 2
     return dict(
         target_w=L * layer_b + V * d * 2 + d * 2,
-        drafter_w=(2 * d * d) * 2 + layer_b + V * d * 2 + d * 2,
+        drafter_w=(2 * d * d) * 2 + layer_b + lm_d + d * 2,
         kv_tok=L * 2 * KV * hd * 2, dkv_tok=2 * KV * hd * 2,
-        fl_row_t=2 * (L * mat_layer + V * d), fl_row_d=2 * (2 * d * d + mat_layer + V * d),
+        fl_row_t=2 * (L * mat_layer + V * d),
+        fl_row_d=2 * (2 * d * d + mat_layer) + (V * d if drafter_fp8 else 2 * V * d),
         attn_fl=4 * H * hd, layers=L)
 
 
-def step_roofline(m, b, ctx, strategy, bw_gbs, tflops):
+def step_roofline(m, b, ctx, strategy, bw_gbs, tflops, drafter_fp8=False):
     """t_roof of one engine step = sum over phases of max(bytes / BW, flops /
     peak) (SURVEY.md 8(d)). strategy None = plain AR decode (R = b rows);
     else (D, k, T): D drafter levels (level 1: b LM rows, level l: b *
     min(T, k^(l-1)) rows) + one verify forward over b (T + 1) rows."""
-    c = model_costs(m)
+    c = model_costs(m, drafter_fp8)
     bw, pk = bw_gbs * 1e9, tflops * 1e12
 
     def phase(w, rows, kv_read, kv_write, attn_rows_keys, fl_row, layers):
@@ -316,7 +320,8 @@ PROBES = [  # (name, probe kind, M, bound)  -- SURVEY.md 8(d) per-kernel rooflin
     ("LM head + fused top-1, long-tail verify (b=1, T=16)", 4, 17, "hbm"),
     ("gate_up GEMM+SwiGLU, verify b=31 T=16", 0, 527, "tensor"),
     ("down GEMM+residual, verify b=31 T=16", 2, 527, "tensor"),
-    ("LM head fp32 logits, drafter level b=31 (496 rows)", 3, 496, "tensor"),
+    ("LM head bf16 -> fp32 logits, 496 rows (drafter level width at b=31)", 3, 496, "tensor"),
+    ("drafter LM head as configured (7B: e4m3) -> fp32 logits, drafter level b=1 (8 rows)", 6, 8, "hbm"),
     ("gate_up GEMM+SwiGLU, verify b=16 T=64", 0, 1040, "tensor"),
 ]
 
@@ -419,7 +424,8 @@ def bucket_rows(eng, a, peak_gbs, peak_tf_sus):
                 emitted += int(r.accept_len.sum()) + b
                 acc += int(r.accept_len.sum())
             ctx_sd = int(np.mean(L0))
-            roof = step_roofline(eng.model, b, ctx_sd, arm, peak_gbs, peak_tf_sus)["t_roof_ms"]
+            roof = step_roofline(eng.model, b, ctx_sd, arm, peak_gbs, peak_tf_sus,
+                                 bool(eng.init.get("drafter_lm_fp8", 0)))["t_roof_ms"]
             tps = emitted / (ms / 1e3)
             row["arms"].append({"strategy": list(arm), "sd_tok_s": round(tps, 1), "speedup_vs_ar": round(tps / ar_tps, 3),
                                 "ms_per_step": round(ms / steps, 3), "mean_accept_len": round(acc / (b * steps), 3),

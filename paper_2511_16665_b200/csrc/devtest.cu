@@ -278,6 +278,9 @@ extern "C" TLT_API int tlt_dev_gemm_e4m3(const void* x, int m, int k, const void
     try {
         launch_quant_rows_e4m3(static_cast<const __nv_bfloat16*>(x), m, k, k, qx, sx, 0);
         launch_quant_rows_e4m3(static_cast<const __nv_bfloat16*>(w), n, k, k, qw, sw, 0);
+        // the GEMM streams its weight stages before griddepcontrol.wait (weights
+        // are static in the engine): here they were just written, so finish first
+        CUDA_CHECK(cudaDeviceSynchronize());
         GemmPlan g = plan_gemm_e4m3(m, n, k);
         CUtensorMap tw = make_tmap_e4m3(qw, n, k, k, 128);
         CUtensorMap tx = make_tmap_e4m3(qx, m, k, k, g.box_rows);

@@ -202,6 +202,9 @@ void Engine::alloc_weights(const tlt_init_cfg& init) {
         lm8_ = dmalloc<uint8_t>((size_t)V * d);
         lm8_s_ = dmalloc<float>((size_t)V);
         launch_quant_rows_e4m3(lm_head_, (int)V, (int)d, d, lm8_, lm8_s_, st_);
+        // weight operands are prefetched by the GEMMs before griddepcontrol.wait
+        // (they are static): the e4m3 copy must be complete before any GEMM
+        CUDA_CHECK(cudaStreamSynchronize(st_));
         tm_lm8_ = make_tmap_e4m3(lm8_, (int)V, (int)d, d, 128);
     }
     tm_fc_ = make_tmap_bf16(fc_, (int)d, (int)(2 * d), 2 * d, 128);
@@ -1157,7 +1160,9 @@ float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* fl
     CUDA_CHECK(cudaGraphExecDestroy(ex));
     const double out_b = kind == 0 ? (double)M * N / 2 * 2 : kind == 1 ? (double)M * N * 2
                          : (kind == 2 || kind == 5) ? (double)M * N * 8 : kind == 6 ? (double)M * N * 4 : kind == 3 ? (double)M * N * 4 : (double)M * 16;
-    if (bytes) *bytes = (double)N * K * 2 + (double)M * K * 2 + out_b;
+    // the e4m3 drafter LM head streams one byte per weight + one fp32 scale per row
+    const double w_b = (kind == 6 && drafter_fp8_) ? (double)N * K + (double)N * 4 : (double)N * K * 2;
+    if (bytes) *bytes = w_b + (double)M * K * 2 + out_b;
     if (flops) *flops = 2.0 * M * N * K;
     return ms / iters;
 }

@@ -1173,21 +1173,6 @@ GemmPlan plan_gemm_e4m3(int m_tok, int n_out, int k) {
         const int cols = g.bn;
         g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256;
     }
-    // TLT_FP8_WM=2: 256 weight rows per single CTA (two M = 128 MMAs sharing
-    // the token tile). A one-byte k-block halves each CTA's bytes, so the
-    // 1-CTA-per-128-rows plan pays its per-CTA prologue / epilogue over twice
-    // as many short CTAs (drafter LM head at b <= 8: 4 waves of 448 KB).
-    const int fp8_wm = env_knob("TLT_FP8_WM", 1);  // read per plan (tests switch it)
-    if (fp8_wm == 2 && g.pair == 1 && g.wm == 1 && g.bn <= 128 && n_out > 256) {
-        const int fixed = 1024 + 256;
-        g.wm = 2;
-        g.n_wtiles = (n_out + 2 * kBlockM - 1) / (2 * kBlockM);
-        const int stage_bytes = 2 * kABytes + g.box_rows * kBlockK * 2;
-        g.stages = std::max(2, std::min(8, (112 * 1024 - fixed) / stage_bytes));
-        g.smem = g.stages * stage_bytes + fixed;
-        const int cols = 2 * g.bn;
-        g.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256;
-    }
     g.fp8 = 1;
     return g;
 }

@@ -12,10 +12,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("m,k,n", [(1, 256, 4096), (17, 3584, 8192), (96, 512, 1000), (240, 3584, 20000),
                                    (496, 256, 152064), (1000, 512, 4608), (8, 3584, 152064), (64, 1024, 1000)])
-@pytest.mark.parametrize("wm", ["1", "2"])
-def test_gemm_e4m3(monkeypatch, m, k, n, wm):
-    """wm = 2: the 256-weight-row single-CTA plan (TLT_FP8_WM)."""
-    monkeypatch.setenv("TLT_FP8_WM", wm)
+def test_gemm_e4m3(m, k, n):
     g = torch.Generator(device="cuda").manual_seed(m + k + n)
     x = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(n, k, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
