@@ -11,7 +11,10 @@ from paper_2511_16665_b200.engine import Engine  # noqa: E402
 
 SHAPES = [(1, 1024, 1), (8, 1024, 1), (32, 1024, 1), (64, 1024, 1), (1, 1024, 65), (1, 1024, 17), (5, 700, 49),
           (8, 1024, 33), (16, 700, 17), (31, 700, 17), (31, 2000, 17), (4, 700, 9)]
-TREE = [("148", "256"), ("296", "256"), ("148", "128"), ("296", "128"), ("592", "64"), ("74", "256")]
+TREE = [("148", "256"), ("296", "256"), ("148", "128"), ("296", "128"), ("592", "64"), ("74", "256"),
+        ("592", "128"), ("296", "64"), ("1184", "64")]
+if "--tree-only" in sys.argv:  # the tcgen05 tree kernel's split plan only
+    SHAPES = [s for s in SHAPES if s[2] * 7 > 16]
 DEC = [("296", "256"), ("592", "128"), ("1184", "64")]
 
 eng = Engine("qwen2.5-7b", max_slots=64, max_ctx=2400)
