@@ -16,6 +16,9 @@ TREE = [("148", "256"), ("296", "256"), ("148", "128"), ("296", "128"), ("592", 
 if "--tree-only" in sys.argv:  # the tcgen05 tree kernel's split plan only
     SHAPES = [s for s in SHAPES if s[2] * 7 > 16]
 DEC = [("296", "256"), ("592", "128"), ("1184", "64")]
+if "--dec-only" in sys.argv:  # decode split targets at the AR-phase batch sizes
+    SHAPES = [(32, 1024, 1), (48, 1500, 1), (64, 1024, 1), (64, 2048, 1)]
+    DEC = [("296", "256"), ("444", "256"), ("592", "256"), ("888", "256"), ("592", "512"), ("148", "256")]
 
 eng = Engine("qwen2.5-7b", max_slots=64, max_ctx=2400)
 
