@@ -11,7 +11,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("m,k,n", [(1, 256, 4096), (17, 3584, 8192), (96, 512, 1000), (240, 3584, 20000),
-                                   (496, 256, 152064), (1000, 512, 4608), (8, 3584, 152064), (64, 1024, 1000)])
+                                   (496, 256, 152064), (1000, 512, 4608), (8, 3584, 152064), (64, 1024, 1000),
+                                   (3, 8448, 512)])
 def test_gemm_e4m3(m, k, n):
     g = torch.Generator(device="cuda").manual_seed(m + k + n)
     x = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
