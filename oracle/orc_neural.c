@@ -141,6 +141,7 @@ static void* q8_worker(void* a) {
     q8_job* j = (q8_job*)a;
     const int d = j->m->c.hidden;
     float* row = (float*)malloc(sizeof(float) * 2 * (size_t)d);
+    if (!row) return (void*)1;
     for (int64_t v = j->lo; v < j->hi; ++v) {
         for (int i = 0; i < d; ++i) row[i] = bf(j->m->lm_head[v * d + i]);
         j->m->lm8_s[v] = orc_e4m3_quant_row(row, d, row + d);
@@ -177,11 +178,15 @@ orc_model* orc_model_create(const orc_model_cfg* cfg, const orc_init_cfg* init, 
             jobs[i] = (q8_job){m, V * i / nt, V * (i + 1) / nt};
             if (nt > 1)
                 pthread_create(&th[i], NULL, q8_worker, &jobs[i]);
-            else
-                q8_worker(&jobs[i]);
+            else if (q8_worker(&jobs[i]) != NULL)
+                ok = 0;
         }
         if (ok && nt > 1)
-            for (int i = 0; i < nt; ++i) pthread_join(th[i], NULL);
+            for (int i = 0; i < nt; ++i) {
+                void* rc = NULL;
+                pthread_join(th[i], &rc);
+                if (rc) ok = 0;
+            }
     }
     /* RoPE table: angle = pos * theta^(-2i/hd) in double, stored fp32 */
     int half = cfg->head_dim / 2;
