@@ -50,6 +50,14 @@ __global__ void k_draft_in(Rows rows, const bf16* __restrict__ E, int d, const b
     const bf16* e = E + (long long)(live ? rows.tok[r] : 0) * d;
     bf16* o = X2 + (long long)r * 2 * d;
     const bf16 z = __float2bfloat16(0.f);
+    if ((d & 7) == 0) {  // 16-byte copies (rows are 16-byte aligned when d % 8 == 0)
+        const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+            *reinterpret_cast<uint4*>(o + i) = src ? *reinterpret_cast<const uint4*>(src + i) : z4;
+            *reinterpret_cast<uint4*>(o + d + i) = live ? *reinterpret_cast<const uint4*>(e + i) : z4;
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < d; i += blockDim.x) {
         o[i] = src ? src[i] : z;
         o[d + i] = live ? e[i] : z;
