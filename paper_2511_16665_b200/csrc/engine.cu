@@ -1036,16 +1036,17 @@ int Engine::ar_bucket_for(int b) const {
 
 
 // ------------------------------------------------------------ kernel probe
+// kernel probes (bench rooflines): best of this many timed passes
+constexpr int kProbePasses = 5;
+
 // Live per-kernel timing on the engine stream with the engine's own weights:
 // `iters` launches of one GEMM site over successive layers (every launch
 // streams a different weight matrix from HBM, as in a real forward), CUDA
 // events around the whole sequence. Activations are whatever the buffers
 // hold (values do not change the timing). kind: 0 gate_up (+SwiGLU), 1 qkv
-// (+bias/RoPE/KV write into slot 0), 2 down (+residual), 3 LM head fp32
-// logits (drafter k > 1 path), 4 LM head + fused top-1 (verify / decode).
-// kernel probes (bench rooflines): best of this many timed passes
-constexpr int kProbePasses = 5;
-
+// (+bias/RoPE/KV write into slot 0), 2 down (+residual), 3 bf16 LM head fp32
+// logits, 4 LM head + fused top-1 (verify / decode), 5 o-proj (+residual),
+// 6 the drafter's LM head as configured (e4m3 when drafter_lm_fp8).
 float Engine::probe_kernel(int kind, int M, int iters, double* bytes, double* flops) {
     if (M < 1 || M > R_) throw ConfigErr("M", "out of range for the activation buffers");
     const int d = cfg.hidden, L = cfg.layers;
